@@ -1,0 +1,196 @@
+"""CPU oracle for the AMR-level advance of arXiv 1808.02638 (2D acoustics).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+package.  It wraps ``claw_oracle.c`` (plain C99, fp64, no FMA contraction) via
+ctypes and shares no code with the CUDA path in ``paper_1808_02638_b200``.
+
+Every function documents the PAPER.md passage it follows (P:a-b = line range
+of /root/reference/PAPER.md).  Pins: tests/test_oracle_pins.py,
+tests/test_oracle_brute.py, tests/test_oracle_ghost.py.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "claw_oracle.c")
+_HDR = os.path.join(_HERE, "claw_oracle.h")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+# Mirror of oracle_patch_desc (C layout, natural alignment).
+ORACLE_PATCH_DTYPE = np.dtype(
+    [("mx", "<i4"), ("my", "<i4"), ("dx", "<f8"), ("dy", "<f8"),
+     ("xlower", "<f8"), ("ylower", "<f8"), ("mbc", "<i4"),
+     ("rho", "<f8"), ("K", "<f8")], align=True)
+assert ORACLE_PATCH_DTYPE.itemsize == 64
+
+
+class _Config(ctypes.Structure):
+    _fields_ = [("xlo", ctypes.c_double), ("xhi", ctypes.c_double),
+                ("ylo", ctypes.c_double), ("yhi", ctypes.c_double),
+                ("bc", ctypes.c_int32 * 4), ("limiter", ctypes.c_int32),
+                ("order_trans", ctypes.c_int32), ("nthreads", ctypes.c_int32)]
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so (gcc -O2 -std=c11 -ffp-contract=off -fopenmp)."""
+    stale = (not os.path.exists(_LIB)) or any(
+        os.path.getmtime(s) > os.path.getmtime(_LIB) for s in (_SRC, _HDR))
+    if force or stale:
+        cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math",
+               "-fopenmp", "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm"]
+        subprocess.run(cmd, check=True)
+    return _LIB
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        dp = ctypes.POINTER(ctypes.c_double)
+        vp = ctypes.c_void_p
+        L.oracle_create.argtypes = [ctypes.POINTER(_Config), ctypes.POINTER(vp)]
+        L.oracle_destroy.argtypes = [vp]
+        L.oracle_last_error.argtypes = [vp]
+        L.oracle_last_error.restype = ctypes.c_char_p
+        L.oracle_set_level.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, dp]
+        L.oracle_fill_ghost.argtypes = [vp, ctypes.c_int, ctypes.c_double]
+        L.oracle_advance_level.argtypes = [vp, ctypes.c_int, ctypes.c_double, dp]
+        for f in ("oracle_read", "oracle_read_padded"):
+            getattr(L, f).argtypes = [vp, ctypes.c_int, ctypes.c_int, dp]
+        L.oracle_write.argtypes = [vp, ctypes.c_int, ctypes.c_int, dp]
+        L.oracle_patch_cfl.argtypes = [vp, ctypes.c_int, ctypes.c_int, dp]
+        L.oracle_level_time.argtypes = [vp, ctypes.c_int, dp, dp]
+        L.oracle_step_patch.argtypes = [ctypes.c_int, ctypes.c_int, dp, ctypes.c_double,
+                                        ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                        ctypes.c_double, ctypes.c_int, ctypes.c_int, dp, dp]
+        L.oracle_rpn2.argtypes = [ctypes.c_int, dp, dp, ctypes.c_double, ctypes.c_double,
+                                  dp, dp, dp, dp]
+        L.oracle_rpt2.argtypes = [ctypes.c_int, dp, ctypes.c_double, ctypes.c_double, dp, dp]
+        L.oracle_philim.argtypes = [ctypes.c_int, ctypes.c_double]
+        L.oracle_philim.restype = ctypes.c_double
+        _lib = L
+    return _lib
+
+
+def _dp(a: np.ndarray):
+    assert a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+class Oracle:
+    """One AMR hierarchy on the CPU.  Mirrors the C-ABI call shapes
+    (create / set_level / fill_ghost / advance_level / read)."""
+
+    def __init__(self, domain=(-1.0, 1.0, -1.0, 1.0), bc=(1, 1, 1, 1), limiter=4,
+                 order_trans=2, nthreads=0):
+        cfg = _Config(*[float(v) for v in domain], (ctypes.c_int32 * 4)(*bc),
+                      int(limiter), int(order_trans), int(nthreads))
+        self._h = ctypes.c_void_p()
+        rc = lib().oracle_create(ctypes.byref(cfg), ctypes.byref(self._h))
+        if rc != 0:
+            raise OracleError(f"oracle_create failed ({rc})")
+        self._descs = {}
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().oracle_destroy(self._h)
+            self._h = None
+
+    def _check(self, rc):
+        if rc != 0:
+            raise OracleError(f"rc={rc}: {lib().oracle_last_error(self._h).decode()}")
+
+    def set_level(self, level: int, descs: np.ndarray, q0: np.ndarray | None = None):
+        d = np.ascontiguousarray(descs.astype(ORACLE_PATCH_DTYPE))
+        q = None if q0 is None else np.ascontiguousarray(q0, dtype=np.float64)
+        if q is not None:
+            assert q.size == 3 * int((d["mx"].astype(np.int64) * d["my"]).sum())
+        self._descs[level] = d
+        self._check(lib().oracle_set_level(self._h, level, len(d), d.ctypes.data,
+                                           None if q is None else _dp(q)))
+
+    def fill_ghost(self, level: int, t: float = 0.0):
+        self._check(lib().oracle_fill_ghost(self._h, level, float(t)))
+
+    def advance_level(self, level: int, dt: float) -> float:
+        c = ctypes.c_double()
+        self._check(lib().oracle_advance_level(self._h, level, float(dt), ctypes.byref(c)))
+        return c.value
+
+    def read(self, level: int, patch: int) -> np.ndarray:
+        d = self._descs[level][patch]
+        out = np.empty((3, int(d["my"]), int(d["mx"])))
+        self._check(lib().oracle_read(self._h, level, patch, _dp(out)))
+        return out
+
+    def read_level(self, level: int) -> np.ndarray:
+        """All patches concatenated as [patch][3][my][mx] (flat)."""
+        return np.concatenate([self.read(level, p).ravel()
+                               for p in range(len(self._descs[level]))])
+
+    def write(self, level: int, patch: int, q: np.ndarray):
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        self._check(lib().oracle_write(self._h, level, patch, _dp(q)))
+
+    def read_padded(self, level: int, patch: int) -> np.ndarray:
+        d = self._descs[level][patch]
+        out = np.empty((3, int(d["my"]) + 4, int(d["mx"]) + 4))
+        self._check(lib().oracle_read_padded(self._h, level, patch, _dp(out)))
+        return out
+
+    def patch_cfl(self, level: int, patch: int) -> float:
+        c = ctypes.c_double()
+        self._check(lib().oracle_patch_cfl(self._h, level, patch, ctypes.byref(c)))
+        return c.value
+
+    def level_time(self, level: int):
+        a, b = ctypes.c_double(), ctypes.c_double()
+        self._check(lib().oracle_level_time(self._h, level, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+
+def step_patch(qpad: np.ndarray, dx, dy, dt, rho=1.0, K=1.0, limiter=4, order_trans=2):
+    """One step of eq. (W) on a padded [3][my+4][mx+4] patch; returns
+    (qout_pad, cfl)."""
+    qpad = np.ascontiguousarray(qpad, dtype=np.float64)
+    _, py, px = qpad.shape
+    out = np.empty_like(qpad)
+    c = ctypes.c_double()
+    rc = lib().oracle_step_patch(px - 4, py - 4, _dp(qpad), dx, dy, dt, rho, K,
+                                 limiter, order_trans, _dp(out), ctypes.byref(c))
+    if rc != 0:
+        raise OracleError("oracle_step_patch failed")
+    return out, c.value
+
+
+def rpn2(ixy, ql, qr, rho=1.0, K=1.0):
+    ql = np.ascontiguousarray(ql, dtype=np.float64)
+    qr = np.ascontiguousarray(qr, dtype=np.float64)
+    wave = np.empty((2, 3)); s = np.empty(2); am = np.empty(3); ap = np.empty(3)
+    lib().oracle_rpn2(ixy, _dp(ql), _dp(qr), rho, K, _dp(wave), _dp(s), _dp(am), _dp(ap))
+    return wave, s, am, ap
+
+
+def rpt2(ixy, asdq, rho=1.0, K=1.0):
+    a = np.ascontiguousarray(asdq, dtype=np.float64)
+    bm = np.empty(3); bp = np.empty(3)
+    lib().oracle_rpt2(ixy, _dp(a), rho, K, _dp(bm), _dp(bp))
+    return bm, bp
+
+
+def philim(limiter: int, r: float) -> float:
+    return lib().oracle_philim(limiter, float(r))

@@ -1,0 +1,690 @@
+/*
+ * claw_oracle.c -- CPU ORACLE (test infrastructure only; see claw_oracle.h).
+ *
+ * A plain, slow, literal implementation of one AMR-level step of the
+ * wave-propagation method of arXiv 1808.02638 for 2D linear acoustics.
+ * The per-patch step follows Clawpack's classic structure (P:50, P:433-440
+ * name Clawpack's rpn2/rpt2 "normal" and "transverse" Riemann solvers):
+ *
+ *   step2  : x-sweeps over rows j = 0..my+1, then y-sweeps over columns
+ *            i = 0..mx+1, accumulating fm/fp/gm/gp, then the flux-difference
+ *            update, which is eq. (W);
+ *   flux2  : Riemann solves at every interface 0..n+2 of the 1D slice
+ *            (rpn2), wave limiting (limiter), second-order correction
+ *            cqxx = sum |s|(1-|s|dt/dx) W~ (the F~ terms of eq. (W)),
+ *            transverse splitting of A-dq, A+dq (rpt2; "corner transport",
+ *            P:500) into the transverse fluxes gadd;
+ *   rpn2   : eigen-decomposition of A (or B) for acoustics;
+ *   rpt2   : eigen-decomposition of B (or A) applied to A-dq / A+dq.
+ *
+ * Ghost fill follows the three cases of P:125-132 with the composite reading
+ * of DESIGN.md ("Readings" R1, R8-R10): per-axis clamp (extrapolation) or
+ * wrap (periodic) of the global index, then a copy from the same-level patch
+ * holding the mapped cell, else (level > 1) space-time interpolation from the
+ * coarser level.
+ *
+ * Index convention (Clawpack, 1-based): interior cells i = 1..mx,
+ * j = 1..my; ghost cells -1, 0 and mx+1, mx+2.  Interface i is the left edge
+ * of cell i (x_{i-1/2}).  Padded storage index = i + 1.
+ */
+#include "claw_oracle.h"
+
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#define NTHREADS(c) ((c)->cfg.nthreads > 0 ? (c)->cfg.nthreads : omp_get_max_threads())
+#else
+#define NTHREADS(c) 1
+#endif
+
+#define MAXLEVEL 8
+#define MEQN 3
+#define MWAVES 2
+#define BUCKET 16
+
+typedef struct {
+  int npatch;
+  oracle_patch_desc* desc;
+  int64_t* i0; /* global 0-based index of interior cell (1,1) */
+  int64_t* j0;
+  double** qpad;  /* current time level, padded [3][my+4][mx+4] */
+  double** qold;  /* previous time level, interior [3][my][mx] */
+  double* pcfl;   /* per-patch max Courant number of the last step */
+  double dx, dy;
+  int64_t nx, ny; /* level index extent of the domain */
+  int ratio_to_coarser; /* R_{L-1}; 0 for level 1 */
+  double t_old, t_new;
+  /* bucket grid for "which patch holds cell (I,J)" */
+  int64_t nbx, nby;
+  int64_t* bstart; /* CSR offsets, nbx*nby+1 */
+  int* blist;
+} olevel;
+
+struct oracle_ctx {
+  oracle_config cfg;
+  olevel lev[MAXLEVEL + 1];
+  char err[512];
+};
+
+static int fail(oracle_ctx* c, int code, const char* msg) {
+  if (c) snprintf(c->err, sizeof c->err, "%s", msg);
+  return code;
+}
+
+const char* oracle_last_error(const oracle_ctx* c) { return c ? c->err : "null ctx"; }
+
+/* ------------------------------------------------------------------------ */
+/* Riemann solvers: linear acoustics, A = [[0,K,0],[1/rho,0,0],[0,0,0]],    */
+/* B = [[0,0,K],[0,0,0],[1/rho,0,0]].  c = sqrt(K/rho),          */
+/* Z = rho c.  Eigenvalues -c, 0, +c; the zero-speed wave carries nothing     */
+/* into the flux and is omitted (mwaves = 2), as in Clawpack's acoustics.     */
+/* ------------------------------------------------------------------------ */
+
+void oracle_rpn2(int ixy, const double* ql, const double* qr, double rho,
+                 double K, double* wave, double* s, double* amdq, double* apdq) {
+  /* ql = state of cell i-1 (left of the interface), qr = state of cell i. */
+  const double cc = sqrt(K / rho);
+  const double zz = rho * cc;
+  const int mu = (ixy == 1) ? 1 : 2; /* normal velocity component */
+  const int mv = (ixy == 1) ? 2 : 1; /* tangential velocity component */
+  const double delta1 = qr[0] - ql[0];
+  const double delta2 = qr[mu] - ql[mu];
+  const double a1 = (-delta1 + zz * delta2) / (2.0 * zz);
+  const double a2 = (delta1 + zz * delta2) / (2.0 * zz);
+  /* wave 1: left-going, speed -c, eigenvector (-Z, 1, 0) */
+  wave[0 * MEQN + 0] = -a1 * zz;
+  wave[0 * MEQN + mu] = a1;
+  wave[0 * MEQN + mv] = 0.0;
+  s[0] = -cc;
+  /* wave 2: right-going, speed +c, eigenvector (Z, 1, 0) */
+  wave[1 * MEQN + 0] = a2 * zz;
+  wave[1 * MEQN + mu] = a2;
+  wave[1 * MEQN + mv] = 0.0;
+  s[1] = cc;
+  for (int m = 0; m < MEQN; ++m) {
+    amdq[m] = s[0] * wave[0 * MEQN + m];
+    apdq[m] = s[1] * wave[1 * MEQN + m];
+  }
+}
+
+void oracle_rpt2(int ixy, const double* asdq, double rho, double K,
+                 double* bmasdq, double* bpasdq) {
+  /* Split asdq into down-going (B^-) and up-going (B^+) parts with the
+   * eigenvectors of the matrix for the transverse direction. */
+  const double cc = sqrt(K / rho);
+  const double zz = rho * cc;
+  const int mu = (ixy == 1) ? 1 : 2;
+  const int mv = (ixy == 1) ? 2 : 1;
+  const double a1 = (-asdq[0] + zz * asdq[mv]) / (2.0 * zz);
+  const double a2 = (asdq[0] + zz * asdq[mv]) / (2.0 * zz);
+  bmasdq[0] = cc * a1 * zz;
+  bmasdq[mu] = 0.0;
+  bmasdq[mv] = -cc * a1;
+  bpasdq[0] = cc * a2 * zz;
+  bpasdq[mu] = 0.0;
+  bpasdq[mv] = cc * a2;
+}
+
+/* Wave limiter function phi(theta) (P:501 names van Leer; BASELINE configs use
+ * MC and minmod).  Clawpack numbering. */
+double oracle_philim(int limiter, double r) {
+  double c;
+  switch (limiter) {
+    case 1: /* minmod */
+      return fmax(0.0, fmin(1.0, r));
+    case 2: /* superbee */
+      return fmax(0.0, fmax(fmin(1.0, 2.0 * r), fmin(2.0, r)));
+    case 3: /* van Leer */
+      return (r + fabs(r)) / (1.0 + fabs(r));
+    case 4: /* monotonized centered */
+      c = (1.0 + r) / 2.0;
+      return fmax(0.0, fmin(c, fmin(2.0, 2.0 * r)));
+    default: /* 0: no limiting (Lax-Wendroff) */
+      return 1.0;
+  }
+}
+
+/* ------------------------------------------------------------------------ */
+/* flux2: one 1D slice of n cells with ghosts -1..n+2.                       */
+/* q1d[m][i+1], i=-1..n+2.  Outputs (index = i+1):                           */
+/*   faddm[m][i], faddp[m][i]   i = 1..n+1   (fluxes at interface i)         */
+/*   gadd[k][m][i]              i = 0..n+1   (k=0: B^- part -> edge of cell  */
+/*                              i at the "low" transverse side, k=1: high)   */
+/* ------------------------------------------------------------------------ */
+static void flux2(int ixy, int n, const double* q1d, double dtdx, double rho,
+                  double K, int limiter, int order_trans, double* faddm,
+                  double* faddp, double* gadd, double* cfl1d) {
+  const int W = n + 4; /* stride of every per-slice array */
+#define Q1(m, i) q1d[(m) * W + (i) + 1]
+#define FM(m, i) faddm[(m) * W + (i) + 1]
+#define FP(m, i) faddp[(m) * W + (i) + 1]
+#define GADD(k, m, i) gadd[((k) * MEQN + (m)) * W + (i) + 1]
+  double* wave = (double*)calloc((size_t)MWAVES * MEQN * W, sizeof(double));
+  double* s = (double*)calloc((size_t)MWAVES * W, sizeof(double));
+  double* amdq = (double*)calloc((size_t)MEQN * W, sizeof(double));
+  double* apdq = (double*)calloc((size_t)MEQN * W, sizeof(double));
+  double* cqxx = (double*)calloc((size_t)MEQN * W, sizeof(double));
+#define WAVE(mw, m, i) wave[((mw) * MEQN + (m)) * W + (i) + 1]
+#define S(mw, i) s[(mw) * W + (i) + 1]
+#define AM(m, i) amdq[(m) * W + (i) + 1]
+#define AP(m, i) apdq[(m) * W + (i) + 1]
+#define CQ(m, i) cqxx[(m) * W + (i) + 1]
+
+  for (int m = 0; m < MEQN; ++m)
+    for (int i = -1; i <= n + 2; ++i) {
+      FM(m, i) = 0.0;
+      FP(m, i) = 0.0;
+      GADD(0, m, i) = 0.0;
+      GADD(1, m, i) = 0.0;
+    }
+
+  /* Normal Riemann problems at interfaces i = 0..n+2 (between i-1 and i). */
+  for (int i = 0; i <= n + 2; ++i) {
+    double ql[MEQN], qr[MEQN], wv[MWAVES * MEQN], sp[MWAVES], am[MEQN], ap[MEQN];
+    for (int m = 0; m < MEQN; ++m) {
+      ql[m] = Q1(m, i - 1);
+      qr[m] = Q1(m, i);
+    }
+    oracle_rpn2(ixy, ql, qr, rho, K, wv, sp, am, ap);
+    for (int mw = 0; mw < MWAVES; ++mw) {
+      S(mw, i) = sp[mw];
+      for (int m = 0; m < MEQN; ++m) WAVE(mw, m, i) = wv[mw * MEQN + m];
+    }
+    for (int m = 0; m < MEQN; ++m) {
+      AM(m, i) = am[m];
+      AP(m, i) = ap[m];
+    }
+  }
+
+  /* First-order fluctuations enter the fluxes (eq. (W) terms A+-dq). */
+  for (int i = 1; i <= n + 1; ++i)
+    for (int m = 0; m < MEQN; ++m) {
+      FP(m, i) = FP(m, i) - AP(m, i);
+      FM(m, i) = FM(m, i) + AM(m, i);
+    }
+
+  /* CFL number nu = |s dt/dx|, max over the slice. */
+  double cfl = 0.0;
+  for (int mw = 0; mw < MWAVES; ++mw)
+    for (int i = 1; i <= n + 1; ++i) {
+      cfl = fmax(cfl, dtdx * S(mw, i));
+      cfl = fmax(cfl, -dtdx * S(mw, i));
+    }
+  *cfl1d = cfl;
+
+  /* Wave limiter (Clawpack limiter.f): theta = <W_up, W> / <W, W>, upwind
+   * side chosen by the sign of the speed; waves with <W,W> = 0 skipped. */
+  if (limiter != 0) {
+    for (int mw = 0; mw < MWAVES; ++mw) {
+      double dotr = 0.0;
+      for (int i = 0; i <= n + 1; ++i) {
+        double wnorm2 = 0.0, dotl = dotr;
+        dotr = 0.0;
+        for (int m = 0; m < MEQN; ++m) {
+          wnorm2 = wnorm2 + WAVE(mw, m, i) * WAVE(mw, m, i);
+          dotr = dotr + WAVE(mw, m, i) * WAVE(mw, m, i + 1);
+        }
+        if (i == 0) continue;
+        if (wnorm2 == 0.0) continue;
+        double r = (S(mw, i) > 0.0) ? dotl / wnorm2 : dotr / wnorm2;
+        double wlimitr = oracle_philim(limiter, r);
+        for (int m = 0; m < MEQN; ++m) WAVE(mw, m, i) = wlimitr * WAVE(mw, m, i);
+      }
+    }
+  }
+
+  /* Second-order corrections cqxx = sum_p |s_p| (1 - |s_p| dt/dx) W~_p. */
+  for (int i = 1; i <= n + 1; ++i) {
+    const double dtdxave = 0.5 * (dtdx + dtdx);
+    for (int m = 0; m < MEQN; ++m) {
+      CQ(m, i) = 0.0;
+      for (int mw = 0; mw < MWAVES; ++mw)
+        CQ(m, i) = CQ(m, i) + fabs(S(mw, i)) * (1.0 - fabs(S(mw, i)) * dtdxave) * WAVE(mw, m, i);
+      FM(m, i) = FM(m, i) + 0.5 * CQ(m, i);
+      FP(m, i) = FP(m, i) + 0.5 * CQ(m, i);
+    }
+  }
+
+  if (order_trans != 0) {
+    if (order_trans == 2)
+      for (int i = 1; i <= n + 1; ++i)
+        for (int m = 0; m < MEQN; ++m) {
+          AM(m, i) = AM(m, i) + CQ(m, i);
+          AP(m, i) = AP(m, i) - CQ(m, i);
+        }
+    /* Transverse propagation: A-dq at interface i enters cell i-1, A+dq cell i;
+     * each is split into B^- (to that cell's low transverse edge) and B^+
+     * (high edge). */
+    for (int i = 1; i <= n + 1; ++i) {
+      double asdq[MEQN], bm[MEQN], bp[MEQN];
+      for (int m = 0; m < MEQN; ++m) asdq[m] = AM(m, i);
+      oracle_rpt2(ixy, asdq, rho, K, bm, bp);
+      for (int m = 0; m < MEQN; ++m) {
+        GADD(0, m, i - 1) = GADD(0, m, i - 1) - 0.5 * dtdx * bm[m];
+        GADD(1, m, i - 1) = GADD(1, m, i - 1) - 0.5 * dtdx * bp[m];
+      }
+      for (int m = 0; m < MEQN; ++m) asdq[m] = AP(m, i);
+      oracle_rpt2(ixy, asdq, rho, K, bm, bp);
+      for (int m = 0; m < MEQN; ++m) {
+        GADD(0, m, i) = GADD(0, m, i) - 0.5 * dtdx * bm[m];
+        GADD(1, m, i) = GADD(1, m, i) - 0.5 * dtdx * bp[m];
+      }
+    }
+  }
+  free(wave);
+  free(s);
+  free(amdq);
+  free(apdq);
+  free(cqxx);
+#undef Q1
+#undef FM
+#undef FP
+#undef GADD
+#undef WAVE
+#undef S
+#undef AM
+#undef AP
+#undef CQ
+}
+
+/* ------------------------------------------------------------------------ */
+/* step2: one step of eq. (W) on one padded patch.                           */
+/* ------------------------------------------------------------------------ */
+int oracle_step_patch(int mx, int my, const double* qpad, double dx, double dy,
+                      double dt, double rho, double K, int limiter,
+                      int order_trans, double* qout_pad, double* cfl_out) {
+  if (mx < 1 || my < 1 || !(dx > 0.0) || !(dy > 0.0) || !(rho > 0.0) || !(K > 0.0))
+    return -1;
+  const int PX = mx + 4, PY = my + 4;
+  const size_t plane = (size_t)PX * PY;
+#define QP(m, i, j) qpad[(m) * plane + (size_t)((j) + 1) * PX + (i) + 1]
+#define QN(m, i, j) qout_pad[(m) * plane + (size_t)((j) + 1) * PX + (i) + 1]
+  double* fm = (double*)calloc(MEQN * plane, sizeof(double));
+  double* fp = (double*)calloc(MEQN * plane, sizeof(double));
+  double* gm = (double*)calloc(MEQN * plane, sizeof(double));
+  double* gp = (double*)calloc(MEQN * plane, sizeof(double));
+#define FMA_(m, i, j) fm[(m) * plane + (size_t)((j) + 1) * PX + (i) + 1]
+#define FPA_(m, i, j) fp[(m) * plane + (size_t)((j) + 1) * PX + (i) + 1]
+#define GMA_(m, i, j) gm[(m) * plane + (size_t)((j) + 1) * PX + (i) + 1]
+#define GPA_(m, i, j) gp[(m) * plane + (size_t)((j) + 1) * PX + (i) + 1]
+  const int NMAX = (mx > my ? mx : my) + 4;
+  double* q1d = (double*)calloc((size_t)MEQN * NMAX, sizeof(double));
+  double* faddm = (double*)calloc((size_t)MEQN * NMAX, sizeof(double));
+  double* faddp = (double*)calloc((size_t)MEQN * NMAX, sizeof(double));
+  double* gadd = (double*)calloc((size_t)2 * MEQN * NMAX, sizeof(double));
+  double cfl = 0.0, cfl1d;
+
+  /* x-sweeps: rows j = 0..my+1 */
+  const double dtdx = dt / dx;
+  const int WX = mx + 4;
+  for (int j = 0; j <= my + 1; ++j) {
+    for (int m = 0; m < MEQN; ++m)
+      for (int i = -1; i <= mx + 2; ++i) q1d[m * WX + i + 1] = QP(m, i, j);
+    flux2(1, mx, q1d, dtdx, rho, K, limiter, order_trans, faddm, faddp, gadd, &cfl1d);
+    cfl = fmax(cfl, cfl1d);
+    for (int i = 1; i <= mx + 1; ++i)
+      for (int m = 0; m < MEQN; ++m) {
+        FMA_(m, i, j) = FMA_(m, i, j) + faddm[m * WX + i + 1];
+        FPA_(m, i, j) = FPA_(m, i, j) + faddp[m * WX + i + 1];
+        GMA_(m, i, j) = GMA_(m, i, j) + gadd[(0 * MEQN + m) * WX + i + 1];
+        GPA_(m, i, j) = GPA_(m, i, j) + gadd[(0 * MEQN + m) * WX + i + 1];
+        GMA_(m, i, j + 1) = GMA_(m, i, j + 1) + gadd[(1 * MEQN + m) * WX + i + 1];
+        GPA_(m, i, j + 1) = GPA_(m, i, j + 1) + gadd[(1 * MEQN + m) * WX + i + 1];
+      }
+  }
+
+  /* y-sweeps: columns i = 0..mx+1 */
+  const double dtdy = dt / dy;
+  const int WY = my + 4;
+  for (int i = 0; i <= mx + 1; ++i) {
+    for (int m = 0; m < MEQN; ++m)
+      for (int j = -1; j <= my + 2; ++j) q1d[m * WY + j + 1] = QP(m, i, j);
+    flux2(2, my, q1d, dtdy, rho, K, limiter, order_trans, faddm, faddp, gadd, &cfl1d);
+    cfl = fmax(cfl, cfl1d);
+    for (int j = 1; j <= my + 1; ++j)
+      for (int m = 0; m < MEQN; ++m) {
+        GMA_(m, i, j) = GMA_(m, i, j) + faddm[m * WY + j + 1];
+        GPA_(m, i, j) = GPA_(m, i, j) + faddp[m * WY + j + 1];
+        FMA_(m, i, j) = FMA_(m, i, j) + gadd[(0 * MEQN + m) * WY + j + 1];
+        FPA_(m, i, j) = FPA_(m, i, j) + gadd[(0 * MEQN + m) * WY + j + 1];
+        FMA_(m, i + 1, j) = FMA_(m, i + 1, j) + gadd[(1 * MEQN + m) * WY + j + 1];
+        FPA_(m, i + 1, j) = FPA_(m, i + 1, j) + gadd[(1 * MEQN + m) * WY + j + 1];
+      }
+  }
+
+  /* Flux-difference update, eq. (W). */
+  memcpy(qout_pad, qpad, MEQN * plane * sizeof(double));
+  for (int m = 0; m < MEQN; ++m)
+    for (int j = 1; j <= my; ++j)
+      for (int i = 1; i <= mx; ++i)
+        QN(m, i, j) = QP(m, i, j) - dtdx * (FMA_(m, i + 1, j) - FPA_(m, i, j))
+                      - dtdy * (GMA_(m, i, j + 1) - GPA_(m, i, j));
+
+  *cfl_out = cfl;
+  free(fm); free(fp); free(gm); free(gp);
+  free(q1d); free(faddm); free(faddp); free(gadd);
+  return 0;
+#undef QP
+#undef QN
+#undef FMA_
+#undef FPA_
+#undef GMA_
+#undef GPA_
+}
+
+/* ------------------------------------------------------------------------ */
+/* Level bookkeeping                                                          */
+/* ------------------------------------------------------------------------ */
+
+static void free_level(olevel* L) {
+  if (L->qpad)
+    for (int p = 0; p < L->npatch; ++p) free(L->qpad[p]);
+  if (L->qold)
+    for (int p = 0; p < L->npatch; ++p) free(L->qold[p]);
+  free(L->qpad); free(L->qold); free(L->desc); free(L->i0); free(L->j0);
+  free(L->pcfl); free(L->bstart); free(L->blist);
+  memset(L, 0, sizeof *L);
+}
+
+int oracle_create(const oracle_config* cfg, oracle_ctx** out) {
+  if (!cfg || !out) return -1;
+  oracle_ctx* c = (oracle_ctx*)calloc(1, sizeof *c);
+  c->cfg = *cfg;
+  if (!(cfg->xhi > cfg->xlo) || !(cfg->yhi > cfg->ylo)) { free(c); return -1; }
+  for (int k = 0; k < 4; ++k)
+    if (cfg->bc[k] != 1 && cfg->bc[k] != 2) { free(c); return -1; }
+  if ((cfg->bc[0] == 2) != (cfg->bc[1] == 2) || (cfg->bc[2] == 2) != (cfg->bc[3] == 2)) {
+    free(c);
+    return -1;
+  }
+  if (cfg->limiter < 0 || cfg->limiter > 4 || cfg->order_trans < 0 || cfg->order_trans > 2) {
+    free(c);
+    return -1;
+  }
+  *out = c;
+  return 0;
+}
+
+int oracle_destroy(oracle_ctx* c) {
+  if (!c) return -1;
+  for (int l = 0; l <= MAXLEVEL; ++l) free_level(&c->lev[l]);
+  free(c);
+  return 0;
+}
+
+static int find_patch(const olevel* L, int64_t I, int64_t J) {
+  if (I < 0 || J < 0 || I >= L->nx || J >= L->ny) return -1;
+  const int64_t b = (J / BUCKET) * L->nbx + (I / BUCKET);
+  for (int64_t k = L->bstart[b]; k < L->bstart[b + 1]; ++k) {
+    const int p = L->blist[k];
+    const oracle_patch_desc* d = &L->desc[p];
+    if (I >= L->i0[p] && I < L->i0[p] + d->mx && J >= L->j0[p] && J < L->j0[p] + d->my)
+      return p;
+  }
+  return -1;
+}
+
+int oracle_set_level(oracle_ctx* c, int level, int npatch,
+                     const oracle_patch_desc* descs, const double* q0) {
+  if (!c || level < 1 || level > MAXLEVEL || npatch < 1 || !descs)
+    return fail(c, -1, "bad arguments");
+  if (level > 1 && c->lev[level - 1].npatch == 0)
+    return fail(c, -2, "coarser level not set");
+  olevel* L = &c->lev[level];
+  free_level(L);
+  L->npatch = npatch;
+  L->desc = (oracle_patch_desc*)malloc(sizeof(oracle_patch_desc) * npatch);
+  memcpy(L->desc, descs, sizeof(oracle_patch_desc) * npatch);
+  L->dx = descs[0].dx;
+  L->dy = descs[0].dy;
+  L->nx = llround((c->cfg.xhi - c->cfg.xlo) / L->dx);
+  L->ny = llround((c->cfg.yhi - c->cfg.ylo) / L->dy);
+  if (level > 1) {
+    L->ratio_to_coarser = (int)llround(c->lev[level - 1].dx / L->dx);
+    if (L->ratio_to_coarser < 1) return fail(c, -1, "bad refinement ratio");
+  }
+  L->i0 = (int64_t*)malloc(sizeof(int64_t) * npatch);
+  L->j0 = (int64_t*)malloc(sizeof(int64_t) * npatch);
+  for (int p = 0; p < npatch; ++p) {
+    const oracle_patch_desc* d = &descs[p];
+    if (d->mx < 1 || d->my < 1 || d->mbc != 2 || !(d->rho > 0) || !(d->K > 0) ||
+        d->dx != L->dx || d->dy != L->dy)
+      return fail(c, -1, "bad patch descriptor");
+    const double fi = (d->xlower - c->cfg.xlo) / L->dx, fj = (d->ylower - c->cfg.ylo) / L->dy;
+    L->i0[p] = llround(fi);
+    L->j0[p] = llround(fj);
+    if (fabs(fi - (double)L->i0[p]) > 1e-6 || fabs(fj - (double)L->j0[p]) > 1e-6)
+      return fail(c, -1, "patch not aligned to the level grid");
+    if (L->i0[p] < 0 || L->j0[p] < 0 || L->i0[p] + d->mx > L->nx || L->j0[p] + d->my > L->ny)
+      return fail(c, -1, "patch outside the domain");
+  }
+  /* bucket grid */
+  L->nbx = (L->nx + BUCKET - 1) / BUCKET;
+  L->nby = (L->ny + BUCKET - 1) / BUCKET;
+  const int64_t nb = L->nbx * L->nby;
+  L->bstart = (int64_t*)calloc((size_t)nb + 1, sizeof(int64_t));
+  for (int pass = 0; pass < 2; ++pass) {
+    int64_t* fillp = NULL;
+    if (pass == 1) {
+      for (int64_t b = 0; b < nb; ++b) L->bstart[b + 1] += L->bstart[b];
+      L->blist = (int*)malloc(sizeof(int) * (size_t)(L->bstart[nb] + 1));
+      fillp = (int64_t*)malloc(sizeof(int64_t) * (size_t)nb);
+      memcpy(fillp, L->bstart, sizeof(int64_t) * (size_t)nb);
+    }
+    for (int p = 0; p < npatch; ++p) {
+      const int64_t bx0 = L->i0[p] / BUCKET, bx1 = (L->i0[p] + descs[p].mx - 1) / BUCKET;
+      const int64_t by0 = L->j0[p] / BUCKET, by1 = (L->j0[p] + descs[p].my - 1) / BUCKET;
+      for (int64_t by = by0; by <= by1; ++by)
+        for (int64_t bx = bx0; bx <= bx1; ++bx) {
+          const int64_t b = by * L->nbx + bx;
+          if (pass == 0) L->bstart[b + 1] += 1;
+          else L->blist[fillp[b]++] = p;
+        }
+    }
+    free(fillp);
+  }
+  /* same-level overlap check */
+  for (int64_t b = 0; b < nb; ++b)
+    for (int64_t k = L->bstart[b]; k < L->bstart[b + 1]; ++k)
+      for (int64_t k2 = k + 1; k2 < L->bstart[b + 1]; ++k2) {
+        const int p = L->blist[k], q = L->blist[k2];
+        if (L->i0[p] < L->i0[q] + descs[q].mx && L->i0[q] < L->i0[p] + descs[p].mx &&
+            L->j0[p] < L->j0[q] + descs[q].my && L->j0[q] < L->j0[p] + descs[p].my)
+          return fail(c, -1, "same-level patches overlap");
+      }
+  if (level == 1) {
+    int64_t cells = 0;
+    for (int p = 0; p < npatch; ++p) cells += (int64_t)descs[p].mx * descs[p].my;
+    if (cells != L->nx * L->ny) return fail(c, -1, "level 1 does not tile the domain");
+  }
+  L->qpad = (double**)calloc(npatch, sizeof(double*));
+  L->qold = (double**)calloc(npatch, sizeof(double*));
+  L->pcfl = (double*)calloc(npatch, sizeof(double));
+  size_t off = 0;
+  for (int p = 0; p < npatch; ++p) {
+    const int mx = descs[p].mx, my = descs[p].my;
+    const size_t plane = (size_t)(mx + 4) * (my + 4);
+    L->qpad[p] = (double*)calloc(MEQN * plane, sizeof(double));
+    L->qold[p] = (double*)calloc((size_t)MEQN * mx * my, sizeof(double));
+    if (q0) {
+      for (int m = 0; m < MEQN; ++m)
+        for (int j = 0; j < my; ++j)
+          for (int i = 0; i < mx; ++i)
+            L->qpad[p][m * plane + (size_t)(j + 2) * (mx + 4) + i + 2] =
+                q0[off + ((size_t)m * my + j) * mx + i];
+      memcpy(L->qold[p], q0 + off, sizeof(double) * MEQN * mx * my);
+    }
+    off += (size_t)MEQN * mx * my;
+  }
+  L->t_old = L->t_new = (level > 1) ? c->lev[level - 1].t_old : 0.0;
+  return 0;
+}
+
+/* Value of component m of coarse level cell (I,J) (already inside the domain)
+ * at the time-interpolation weight alpha.  Returns 0 if no patch holds it. */
+static int coarse_value(const olevel* C, int64_t I, int64_t J, double alpha, double* v) {
+  const int p = find_patch(C, I, J);
+  if (p < 0) return 0;
+  const oracle_patch_desc* d = &C->desc[p];
+  const int li = (int)(I - C->i0[p]), lj = (int)(J - C->j0[p]);
+  const size_t plane = (size_t)(d->mx + 4) * (d->my + 4);
+  for (int m = 0; m < MEQN; ++m) {
+    const double qn = C->qpad[p][m * plane + (size_t)(lj + 2) * (d->mx + 4) + li + 2];
+    const double qo = C->qold[p][((size_t)m * d->my + lj) * d->mx + li];
+    v[m] = (1.0 - alpha) * qo + alpha * qn;
+  }
+  return 1;
+}
+
+static int64_t map_axis(int64_t I, int64_t n, int bc_lo, int bc_hi) {
+  if (I < 0) return (bc_lo == 2) ? ((I % n) + n) % n : 0;
+  if (I >= n) return (bc_hi == 2) ? I % n : n - 1;
+  return I;
+}
+
+int oracle_fill_ghost(oracle_ctx* c, int level, double t) {
+  if (!c || level < 1 || level > MAXLEVEL || c->lev[level].npatch == 0)
+    return fail(c, -2, "level not set");
+  olevel* L = &c->lev[level];
+  const olevel* C = (level > 1) ? &c->lev[level - 1] : NULL;
+  double alpha = 0.0;
+  if (C && C->t_new > C->t_old) alpha = (t - C->t_old) / (C->t_new - C->t_old);
+  const int* bc = c->cfg.bc;
+  int status = 0;
+#pragma omp parallel for schedule(dynamic, 4) num_threads(NTHREADS(c))
+  for (int p = 0; p < L->npatch; ++p) {
+    const oracle_patch_desc* d = &L->desc[p];
+    const int mx = d->mx, my = d->my, PX = mx + 4;
+    const size_t plane = (size_t)PX * (my + 4);
+    double* q = L->qpad[p];
+    for (int j = -1; j <= my + 2; ++j)
+      for (int i = -1; i <= mx + 2; ++i) {
+        if (i >= 1 && i <= mx && j >= 1 && j <= my) continue; /* interior */
+        const int64_t I = map_axis(L->i0[p] + i - 1, L->nx, bc[0], bc[1]);
+        const int64_t J = map_axis(L->j0[p] + j - 1, L->ny, bc[2], bc[3]);
+        double v[MEQN];
+        const int src = find_patch(L, I, J);
+        if (src >= 0) { /* case 1+2: physical BC mapping, then same-level copy */
+          const oracle_patch_desc* sd = &L->desc[src];
+          const size_t splane = (size_t)(sd->mx + 4) * (sd->my + 4);
+          const int li = (int)(I - L->i0[src]), lj = (int)(J - L->j0[src]);
+          for (int m = 0; m < MEQN; ++m)
+            v[m] = L->qpad[src][m * splane + (size_t)(lj + 2) * (sd->mx + 4) + li + 2];
+        } else if (C) { /* case 3: interpolate from the coarser level */
+          const int R = L->ratio_to_coarser;
+          const int64_t Ic = I / R, Jc = J / R;
+          double vc[MEQN], vxm[MEQN], vxp[MEQN], vym[MEQN], vyp[MEQN];
+          int ok = coarse_value(C, Ic, Jc, alpha, vc);
+          ok &= coarse_value(C, map_axis(Ic - 1, C->nx, bc[0], bc[1]), Jc, alpha, vxm);
+          ok &= coarse_value(C, map_axis(Ic + 1, C->nx, bc[0], bc[1]), Jc, alpha, vxp);
+          ok &= coarse_value(C, Ic, map_axis(Jc - 1, C->ny, bc[2], bc[3]), alpha, vym);
+          ok &= coarse_value(C, Ic, map_axis(Jc + 1, C->ny, bc[2], bc[3]), alpha, vyp);
+          if (!ok) {
+#pragma omp atomic write
+            status = -6;
+            continue;
+          }
+          const double xi = ((double)(I % R) + 0.5) / (double)R - 0.5;
+          const double eta = ((double)(J % R) + 0.5) / (double)R - 0.5;
+          for (int m = 0; m < MEQN; ++m) {
+            double sx = 0.0, sy = 0.0;
+            const double dxp = vxp[m] - vc[m], dxm = vc[m] - vxm[m];
+            const double dyp = vyp[m] - vc[m], dym = vc[m] - vym[m];
+            if (dxp * dxm > 0.0) sx = (dxp > 0.0 ? 1.0 : -1.0) * fmin(fabs(dxp), fabs(dxm));
+            if (dyp * dym > 0.0) sy = (dyp > 0.0 ? 1.0 : -1.0) * fmin(fabs(dyp), fabs(dym));
+            v[m] = vc[m] + sx * xi + sy * eta;
+          }
+        } else {
+#pragma omp atomic write
+          status = -6;
+          continue;
+        }
+        for (int m = 0; m < MEQN; ++m) q[m * plane + (size_t)(j + 1) * PX + i + 1] = v[m];
+      }
+  }
+  if (status) return fail(c, status, "ghost cell with no same-level or coarse donor");
+  return 0;
+}
+
+int oracle_advance_level(oracle_ctx* c, int level, double dt, double* cfl_max) {
+  if (!c || level < 1 || level > MAXLEVEL || c->lev[level].npatch == 0)
+    return fail(c, -2, "level not set");
+  olevel* L = &c->lev[level];
+  int status = 0;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(NTHREADS(c))
+  for (int p = 0; p < L->npatch; ++p) {
+    const oracle_patch_desc* d = &L->desc[p];
+    const int mx = d->mx, my = d->my;
+    const size_t plane = (size_t)(mx + 4) * (my + 4);
+    double* qn = (double*)malloc(MEQN * plane * sizeof(double));
+    double cfl = 0.0;
+    if (oracle_step_patch(mx, my, L->qpad[p], d->dx, d->dy, dt, d->rho, d->K,
+                          c->cfg.limiter, c->cfg.order_trans, qn, &cfl) != 0) {
+#pragma omp atomic write
+      status = -1;
+    }
+    for (int m = 0; m < MEQN; ++m)
+      for (int j = 0; j < my; ++j)
+        for (int i = 0; i < mx; ++i)
+          L->qold[p][((size_t)m * my + j) * mx + i] =
+              L->qpad[p][m * plane + (size_t)(j + 2) * (mx + 4) + i + 2];
+    memcpy(L->qpad[p], qn, MEQN * plane * sizeof(double));
+    free(qn);
+    L->pcfl[p] = cfl;
+  }
+  if (status) return fail(c, status, "step failed");
+  double cmax = 0.0;
+  for (int p = 0; p < L->npatch; ++p) cmax = fmax(cmax, L->pcfl[p]);
+  L->t_old = L->t_new;
+  L->t_new = L->t_new + dt;
+  *cfl_max = cmax;
+  return 0;
+}
+
+int oracle_read(const oracle_ctx* c, int level, int patch, double* q_out) {
+  if (!c || level < 1 || level > MAXLEVEL || patch < 0 || patch >= c->lev[level].npatch) return -1;
+  const olevel* L = &c->lev[level];
+  const int mx = L->desc[patch].mx, my = L->desc[patch].my;
+  const size_t plane = (size_t)(mx + 4) * (my + 4);
+  for (int m = 0; m < MEQN; ++m)
+    for (int j = 0; j < my; ++j)
+      for (int i = 0; i < mx; ++i)
+        q_out[((size_t)m * my + j) * mx + i] = L->qpad[patch][m * plane + (size_t)(j + 2) * (mx + 4) + i + 2];
+  return 0;
+}
+
+int oracle_write(oracle_ctx* c, int level, int patch, const double* q_in) {
+  if (!c || level < 1 || level > MAXLEVEL || patch < 0 || patch >= c->lev[level].npatch) return -1;
+  olevel* L = &c->lev[level];
+  const int mx = L->desc[patch].mx, my = L->desc[patch].my;
+  const size_t plane = (size_t)(mx + 4) * (my + 4);
+  for (int m = 0; m < MEQN; ++m)
+    for (int j = 0; j < my; ++j)
+      for (int i = 0; i < mx; ++i)
+        L->qpad[patch][m * plane + (size_t)(j + 2) * (mx + 4) + i + 2] = q_in[((size_t)m * my + j) * mx + i];
+  return 0;
+}
+
+int oracle_read_padded(const oracle_ctx* c, int level, int patch, double* q_out) {
+  if (!c || level < 1 || level > MAXLEVEL || patch < 0 || patch >= c->lev[level].npatch) return -1;
+  const olevel* L = &c->lev[level];
+  const size_t n = (size_t)MEQN * (L->desc[patch].mx + 4) * (L->desc[patch].my + 4);
+  memcpy(q_out, L->qpad[patch], n * sizeof(double));
+  return 0;
+}
+
+int oracle_patch_cfl(const oracle_ctx* c, int level, int patch, double* cfl) {
+  if (!c || level < 1 || level > MAXLEVEL || patch < 0 || patch >= c->lev[level].npatch) return -1;
+  *cfl = c->lev[level].pcfl[patch];
+  return 0;
+}
+
+int oracle_level_time(const oracle_ctx* c, int level, double* t_old, double* t_new) {
+  if (!c || level < 1 || level > MAXLEVEL || c->lev[level].npatch == 0) return -1;
+  *t_old = c->lev[level].t_old;
+  *t_new = c->lev[level].t_new;
+  return 0;
+}

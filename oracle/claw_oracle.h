@@ -1,0 +1,105 @@
+/*
+ * claw_oracle.h -- CPU ORACLE for the batched AMR-level advance of
+ * arXiv 1808.02638 (Qin, LeVeque & Motley), 2D linear acoustics.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * The product path (paper_1808_02638_b200/, libclaw.so) never links, loads
+ * or calls it, and this oracle shares no code, header, table or constant
+ * generator with the CUDA path.
+ *
+ * What it computes (citations: P:a-b = /root/reference/PAPER.md lines a-b,
+ * S:a-b = SPEC.md lines a-b; "Clawpack convention" = readings listed in
+ * DESIGN.md section "Readings"):
+ *   - eq. (W) (sec. 2.1): unsplit wave-propagation update with
+ *     second-order corrections and transverse waves, written in Clawpack's
+ *     classic step2 / flux2 / rpn2 / rpt2 / limiter structure;
+ *   - the acoustics system q_t + A q_x + B q_y = 0 (sec. 4.1)
+ *     solved exactly by rpn2 (normal) and rpt2 (transverse) eigen-splits;
+ *   - ghost-cell fill, three cases (sec. 2.2): physical BC,
+ *     same-level copy, coarse-level interpolation;
+ *   - the CFL number nu = |s dt/dx| (sec. 2.4), maximised over
+ *     every swept interface of a patch, then over the level.
+ *
+ * Arithmetic: IEEE binary64, built with -O2 -ffp-contract=off (no FMA
+ * contraction, no fast-math) so every operation is a single rounding in the
+ * order written.  OpenMP is used only across patches; each patch is computed
+ * sequentially, so results do not depend on the thread count.
+ *
+ * Storage conventions of this API: a patch's interior is exchanged as
+ * [3][my][mx] (component p,u,v; x fastest).  A "padded" patch is
+ * [3][my+4][mx+4] including the two-deep ghost frame (mbc = 2).
+ *
+ * Parity pins for every function here live in tests/test_oracle_*.py.
+ */
+#ifndef CLAW_ORACLE_H
+#define CLAW_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Per-patch description, the north_star's descriptor fields. */
+typedef struct {
+  int32_t mx, my;          /* interior cells */
+  double dx, dy;           /* cell sizes (identical for all patches of a level) */
+  double xlower, ylower;   /* physical lower-left corner of the interior */
+  int32_t mbc;             /* ghost width, must be 2 */
+  double rho, K;           /* density, bulk modulus */
+} oracle_patch_desc;
+
+typedef struct {
+  double xlo, xhi, ylo, yhi; /* physical domain */
+  int32_t bc[4];             /* left,right,bottom,top: 1 extrapolation, 2 periodic */
+  int32_t limiter;           /* 0 none, 1 minmod, 2 superbee, 3 van Leer, 4 MC */
+  int32_t order_trans;       /* 0 none, 1 fluctuations only, 2 incl. corrections */
+  int32_t nthreads;          /* OpenMP threads over patches (<=0: runtime default) */
+} oracle_config;
+
+typedef struct oracle_ctx oracle_ctx;
+
+/* All calls return 0 on success, <0 on error (message via oracle_last_error). */
+int oracle_create(const oracle_config* cfg, oracle_ctx** out);
+int oracle_destroy(oracle_ctx* ctx);
+const char* oracle_last_error(const oracle_ctx* ctx);
+
+/* Level L = 1..8.  q0 may be NULL (zeros); else [patch][3][my][mx]. */
+int oracle_set_level(oracle_ctx* ctx, int level, int npatch,
+                     const oracle_patch_desc* descs, const double* q0);
+
+/* Fill every ghost cell (corners included) of every patch of `level` at time t
+ * by the composite rule.  t only matters for level > 1 (time
+ * interpolation of the coarser level). */
+int oracle_fill_ghost(oracle_ctx* ctx, int level, double t);
+
+/* One step of eq. (W) on every patch of `level` with the ghost frames as they
+ * stand; returns the level's max Courant number. */
+int oracle_advance_level(oracle_ctx* ctx, int level, double dt, double* cfl_max);
+
+int oracle_read(const oracle_ctx* ctx, int level, int patch, double* q_out);
+int oracle_write(oracle_ctx* ctx, int level, int patch, const double* q_in);
+int oracle_read_padded(const oracle_ctx* ctx, int level, int patch, double* q_out);
+int oracle_patch_cfl(const oracle_ctx* ctx, int level, int patch, double* cfl);
+int oracle_level_time(const oracle_ctx* ctx, int level, double* t_old, double* t_new);
+
+/* The single-patch step itself, exposed for the pins: qpad is [3][my+4][mx+4]
+ * with ghosts already set; qout_pad receives the same shape with the interior
+ * replaced by q^{n+1} (ghost entries copied through). */
+int oracle_step_patch(int mx, int my, const double* qpad, double dx, double dy,
+                      double dt, double rho, double K, int limiter,
+                      int order_trans, double* qout_pad, double* cfl);
+
+/* Riemann solvers and limiter function exposed for the pins.
+ * ixy = 1 (x) or 2 (y).  ql, qr: 3-vectors.  wave: [2][3], s: [2]. */
+void oracle_rpn2(int ixy, const double* ql, const double* qr, double rho,
+                 double K, double* wave, double* s, double* amdq, double* apdq);
+void oracle_rpt2(int ixy, const double* asdq, double rho, double K,
+                 double* bmasdq, double* bpasdq);
+double oracle_philim(int limiter, double r);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

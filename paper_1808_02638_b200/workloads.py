@@ -1,0 +1,187 @@
+"""Seeded synthetic workloads (patch layouts + initial conditions).
+
+This module is the ONLY code shared by the CUDA path's tests/bench and the CPU
+oracle: it builds patch descriptor lists and initial data and holds none of
+the method's arithmetic (no Riemann solver, limiter, update or ghost rule).
+It imports nothing from the rest of the package.
+
+Shapes follow BASELINE.json's configs and the paper's benchmark (P:445-504:
+radial acoustics, ring-shaped pressure perturbation, outflow boundaries,
+fp64).  The ring itself is not printed in the paper; we use Clawpack's
+public acoustics_2d_radial qinit (reading R11):
+    p = 1 + cos(pi (r - 0.5) / 0.2)   if |r - 0.5| <= 0.2,   else 0;  u = v = 0.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+# C layout of claw_patch_desc / oracle_patch_desc (natural alignment, 64 B).
+PATCH_DTYPE = np.dtype(
+    [("mx", "<i4"), ("my", "<i4"), ("dx", "<f8"), ("dy", "<f8"),
+     ("xlower", "<f8"), ("ylower", "<f8"), ("mbc", "<i4"),
+     ("rho", "<f8"), ("K", "<f8")], align=True)
+assert PATCH_DTYPE.itemsize == 64
+
+DOMAIN = (-1.0, 1.0, -1.0, 1.0)
+EXTRAP = (1, 1, 1, 1)
+PERIODIC = (2, 2, 2, 2)
+
+
+@dataclass
+class Level:
+    descs: np.ndarray            # PATCH_DTYPE records
+    ratio: int | None = None     # refinement ratio to the coarser level
+
+    @property
+    def cells(self) -> int:
+        return int((self.descs["mx"].astype(np.int64) * self.descs["my"]).sum())
+
+
+@dataclass
+class Workload:
+    name: str
+    levels: list
+    domain: tuple = DOMAIN
+    bc: tuple = EXTRAP
+    limiter: int = 4
+    order_trans: int = 2
+    cfl: float = 0.9
+    steps: int = 20
+    note: str = ""
+    extra: dict = field(default_factory=dict)
+
+    def dt0(self) -> float:
+        """dt = nu * min(dx, dy) / c on the coarsest level (eq:cfl)."""
+        d = self.levels[0].descs
+        c = math.sqrt(float(d["K"][0]) / float(d["rho"][0]))
+        return self.cfl * min(float(d["dx"][0]), float(d["dy"][0])) / c
+
+
+def make_descs(i0, j0, mx, my, dx, dy, domain=DOMAIN, rho=1.0, K=1.0) -> np.ndarray:
+    """Descriptors from integer boxes (lower-left global index i0, j0)."""
+    i0 = np.asarray(i0, dtype=np.int64)
+    n = i0.size
+    d = np.zeros(n, dtype=PATCH_DTYPE)
+    d["mx"] = mx
+    d["my"] = my
+    d["dx"] = dx
+    d["dy"] = dy
+    d["xlower"] = domain[0] + i0 * dx
+    d["ylower"] = domain[2] + np.asarray(j0, dtype=np.int64) * dy
+    d["mbc"] = 2
+    d["rho"] = rho
+    d["K"] = K
+    return d
+
+
+def uniform_level(npx: int, npy: int, mx: int, my: int, domain=DOMAIN,
+                  rho=1.0, K=1.0) -> np.ndarray:
+    """npx x npy patches of mx x my tiling the domain, row-major order."""
+    nx, ny = npx * mx, npy * my
+    dx = (domain[1] - domain[0]) / nx
+    dy = (domain[3] - domain[2]) / ny
+    jj, ii = np.meshgrid(np.arange(npy), np.arange(npx), indexing="ij")
+    return make_descs(ii.ravel() * mx, jj.ravel() * my, mx, my, dx, dy, domain, rho, K)
+
+
+def ring_pressure(x, y):
+    r = np.sqrt(x * x + y * y)
+    return np.where(np.abs(r - 0.5) <= 0.2, 1.0 + np.cos(np.pi * (r - 0.5) / 0.2), 0.0)
+
+
+def ring_ic(descs: np.ndarray, out: np.ndarray | None = None, chunk: int = 4096) -> np.ndarray:
+    """Ring pressure, u = v = 0, point-sampled at cell centres.
+    Returns the flat [patch][3][my][mx] array (optionally into `out`)."""
+    sizes = 3 * descs["mx"].astype(np.int64) * descs["my"]
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    if out is None:
+        out = np.zeros(int(offs[-1]))
+    else:
+        out[...] = 0.0
+    uniform = (descs["mx"] == descs["mx"][0]).all() and (descs["my"] == descs["my"][0]).all()
+    if uniform:
+        mx, my = int(descs["mx"][0]), int(descs["my"][0])
+        view = out.reshape(len(descs), 3, my, mx)
+        ii = np.arange(mx) + 0.5
+        jj = np.arange(my) + 0.5
+        for s in range(0, len(descs), chunk):
+            d = descs[s:s + chunk]
+            x = d["xlower"][:, None, None] + ii[None, None, :] * d["dx"][:, None, None]
+            y = d["ylower"][:, None, None] + jj[None, :, None] * d["dy"][:, None, None]
+            view[s:s + chunk, 0] = ring_pressure(x, y)
+    else:
+        for p, d in enumerate(descs):
+            mx, my = int(d["mx"]), int(d["my"])
+            x = d["xlower"] + (np.arange(mx) + 0.5) * d["dx"]
+            y = d["ylower"] + (np.arange(my) + 0.5) * d["dy"]
+            X, Y = np.meshgrid(x, y)
+            out[offs[p]:offs[p] + mx * my] = ring_pressure(X, Y).ravel()
+    return out
+
+
+def random_ic(descs: np.ndarray, seed: int) -> np.ndarray:
+    """i.i.d. uniform[-1, 1] for every component (numpy default_rng(seed))."""
+    n = 3 * int((descs["mx"].astype(np.int64) * descs["my"]).sum())
+    return np.random.default_rng(seed).uniform(-1.0, 1.0, n)
+
+
+def level_offsets(descs: np.ndarray) -> np.ndarray:
+    sizes = 3 * descs["mx"].astype(np.int64) * descs["my"]
+    return np.concatenate([[0], np.cumsum(sizes)])
+
+
+# ---------------------------------------------------------------------------
+# BASELINE.json configs
+# ---------------------------------------------------------------------------
+
+def c1() -> Workload:
+    """configs[0]: single 64x64 patch, ring, rho=K=1, MC, 20 steps, CFL 0.9."""
+    return Workload("c1_single_64", [Level(uniform_level(1, 1, 64, 64))], steps=20,
+                    note="single 64x64 uniform patch, ring pulse, MC, extrapolation BCs")
+
+
+def c4(patches_per_side: int = 256, mx: int = 32) -> Workload:
+    """configs[3]: 256x256 patches of 32x32 (8192^2 = 67,108,864 cells)."""
+    n = patches_per_side
+    return Workload(f"c4_{n}x{n}_patches_{mx}x{mx}",
+                    [Level(uniform_level(n, n, mx, mx))], steps=100,
+                    note=f"{n*n} patches of {mx}x{mx} on one level ({n*mx}^2 cells)")
+
+
+def c5(patches_per_side: int = 256, mx: int = 64) -> Workload:
+    """configs[4]: 16,384^2 cells as 256x256 patches of 64x64."""
+    n = patches_per_side
+    return Workload(f"c5_{n*mx}sq_patches_{mx}x{mx}",
+                    [Level(uniform_level(n, n, mx, mx))], steps=100,
+                    note=f"{n*mx}^2 cells as {n}x{n} patches of {mx}x{mx}")
+
+
+def ragged_level(seed: int, nx: int = 40, ny: int = 36, max_w: int = 13) -> np.ndarray:
+    """A level of irregular rectangles tiling an nx x ny index space (guillotine
+    cuts), exercising ragged sizes, T-junction neighbours and corners."""
+    rng = np.random.default_rng(seed)
+    boxes = []
+
+    def cut(i0, j0, w, h):
+        if w <= max_w and h <= max_w and (w * h <= 60 or rng.random() < 0.3):
+            boxes.append((i0, j0, w, h))
+            return
+        if (w >= h and w > 1) or h == 1:
+            k = int(rng.integers(1, w))
+            cut(i0, j0, k, h)
+            cut(i0 + k, j0, w - k, h)
+        else:
+            k = int(rng.integers(1, h))
+            cut(i0, j0, w, k)
+            cut(i0, j0 + k, w, h - k)
+
+    cut(0, 0, nx, ny)
+    dx = (DOMAIN[1] - DOMAIN[0]) / nx
+    dy = (DOMAIN[3] - DOMAIN[2]) / ny
+    d = np.zeros(len(boxes), dtype=PATCH_DTYPE)
+    for k, (i0, j0, w, h) in enumerate(boxes):
+        d[k] = make_descs([i0], [j0], w, h, dx, dy)[0]
+    return d
