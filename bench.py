@@ -1,0 +1,423 @@
+#!/usr/bin/env python
+"""Benchmark of the batched AMR-level advance (arXiv 1808.02638 hot path) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5|c4|c3|c2|c1]
+                    [--impl reference] [--no-cpu-baseline]
+
+One "step" = one level step of the whole hot path over the workload:
+claw_fill_ghost (same-level/BC ghosts are pulled inside the step kernel; for
+N > 1 this is the NCCL halo exchange) + claw_advance_level (the fused sm_100a
+step kernel, the device block->grid CFL max, the NCCL max all-reduce for N > 1
+and the 8-byte CFL read-back).  Metric: fp64 cell-updates/s of the whole job
+(all ranks), BASELINE.json's metric.  Default workload: configs[4] (C5,
+16,384^2 cells as 65,536 patches of 64^2; fits one B200), partitioned over N
+ranks (strong scaling).  Multi-level configs (c2, c3) count one coarse step
+(1 + R1 + R1 R2 level advances) as a step.
+
+Rank 0 prints ONE JSON line.  --impl reference times the CPU oracle (the only
+"reference" this paper-only build has) on a bounded sample of the same
+workload, on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1808_02638_b200 import workloads as W  # noqa: E402
+
+BYTES_PER_CELL = 48  # algorithmic: read q^n (3 x fp64) + write q^{n+1} (3 x fp64)
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j.get("hbm_gbs", 6650.0)), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def workload(name: str) -> W.Workload:
+    return {"c1": W.c1, "c2": W.c2, "c3": W.c3, "c4": W.c4, "c5": W.c5}[name]()
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md clocks line)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[5 + k].lower() == "active"})
+        pw = [float(r[3]) for r in self.rows if r[3].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows),
+                "power_w_max": max(pw) if pw else None}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle on a bounded sample (cpu_baseline / --impl reference)
+# ---------------------------------------------------------------------------
+def oracle_sample(wl: W.Workload, budget_s: float = 12.0, steps_cap: int | None = None):
+    """Time the oracle as it stands on a sub-level of the same workload shape
+    (same patch size, same scheme) for ~budget_s of CPU work.  Returns
+    (cell-updates/s, cores, description)."""
+    import oracle
+    d0 = wl.levels[0].descs
+    mx, my = int(d0["mx"][0]), int(d0["my"][0])
+    uniform = len(wl.levels) == 1 and (d0["mx"] == mx).all() and (d0["my"] == my).all()
+    cores = host_cores()
+    if uniform:
+        side = max(1, min(int(math.sqrt(len(d0))), max(1, 1024 // mx)))  # ~1024^2 cells max
+        dx = float(d0["dx"][0])
+        dom = (-1.0, -1.0 + side * mx * dx, -1.0, -1.0 + side * my * dx)
+        descs = W.uniform_level(side, side, mx, my, dom)
+        q0 = W.ring_ic(descs)
+        levels = [descs]
+        desc = f"{side}x{side} patches of {mx}x{my} ({side*mx}x{side*my} cells) cut from {wl.name}"
+    else:
+        levels = [L.descs for L in wl.levels]
+        desc = f"full {wl.name} hierarchy"
+        q0 = None
+    o = oracle.Oracle(wl.domain if not uniform else dom, wl.bc, wl.limiter, wl.order_trans, nthreads=cores)
+    if uniform:
+        o.set_level(1, levels[0], q0)
+        cells = int((levels[0]["mx"].astype(np.int64) * levels[0]["my"]).sum())
+        dt = wl.cfl * float(d0["dx"][0])
+        n, t0 = 0, time.perf_counter()
+        while True:
+            o.fill_ghost(1, n * dt)
+            o.advance_level(1, dt)
+            n += 1
+            el = time.perf_counter() - t0
+            if el >= budget_s or (steps_cap and n >= steps_cap):
+                break
+        return cells * n / el, cores, f"{desc}, {n} steps, {el:.1f} s"
+    for L, (lv, q) in enumerate(zip(wl.levels, W.hierarchy_ic(wl)), start=1):
+        o.set_level(L, lv.descs, q)
+    ratios = {L + 1: wl.levels[L + 1].ratio for L in range(len(wl.levels) - 1)}
+    nlev = len(wl.levels)
+    per_coarse = sum(wl.levels[L].cells * int(np.prod([wl.levels[k].ratio for k in range(1, L + 1)]))
+                     for L in range(nlev))
+
+    def bo(level, t, dt):
+        o.fill_ghost(level, t)
+        o.advance_level(level, dt)
+        if level < nlev:
+            for k in range(ratios[level]):
+                bo(level + 1, t + k * dt / ratios[level], dt / ratios[level])
+
+    dt = wl.dt0()
+    n, t0 = 0, time.perf_counter()
+    while True:
+        bo(1, n * dt, dt)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or (steps_cap and n >= steps_cap):
+            break
+    return per_coarse * n / el, cores, f"{desc}, {n} coarse steps, {el:.1f} s"
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.build()
+    wl = workload(args.config)
+    vals = []
+    desc = ""
+    cores = host_cores()
+    for _ in range(args.warmup):
+        oracle_sample(wl, budget_s=2.0, steps_cap=1)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, cores, desc = oracle_sample(wl, budget_s=max(1.0, 60.0 / max(args.steps, 1)), steps_cap=None)
+        vals.append(v)
+    el = time.perf_counter() - t0
+    value = statistics.median(vals)
+    line = {"impl": "reference", "metric": "fp64 cell-updates/s", "value": value, "unit": "cell-updates/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * el / max(args.steps, 1), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wl.name, "note": wl.note},
+            "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": cores, "kind": "oracle",
+                             "sample": desc, "cpu": cpu_model()},
+            "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# the GPU arm
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--tile-rows", type=int, default=0)
+    args = ap.parse_args()
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local_rank = env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        sys.exit(run_reference(args, rank))
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1808_02638_b200 import binding
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    wl = workload(args.config)
+    nlev = len(wl.levels)
+    if world > 1 and nlev > 1:
+        raise SystemExit("multi-level configs are single-GPU in this version")
+
+    # NCCL unique id for the library's own communicator (plumbing via torch)
+    nccl_id = None
+    if world > 1:
+        obj = [binding.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
+    stream = torch.cuda.current_stream()
+    g = binding.Claw(wl.domain, wl.bc, wl.limiter, wl.order_trans, device=local_rank, rank=rank,
+                     world=world, nccl_id=nccl_id, stream=stream.cuda_stream, tile_rows=args.tile_rows)
+
+    # inputs: host-side synthetic data of the workload's shape, uploaded once
+    # through the API; pinned so the e2e leg measures the real H2D path
+    host_q = []
+    for L, lv in enumerate(wl.levels, start=1):
+        owner = binding.partition(lv.descs, world)
+        mine = lv.descs[owner == rank]
+        n = 3 * int((mine["mx"].astype(np.int64) * mine["my"]).sum())
+        buf = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        W.ring_ic(mine, out=buf.numpy())
+        g.set_level(L, lv.descs, buf)
+        host_q.append(buf)
+    ratios = {L + 1: wl.levels[L + 1].ratio for L in range(nlev - 1)}
+    cells_owned = [g.level_owned(L)[1] for L in range(1, nlev + 1)]
+    mult = [int(np.prod([wl.levels[k].ratio for k in range(1, L + 1)])) for L in range(nlev)]
+    cells_per_step_rank = sum(c * m for c, m in zip(cells_owned, mult))
+    total_cells_per_step = sum(lv.cells * m for lv, m in zip(wl.levels, mult))
+    dt = wl.dt0()
+    t_sim = [0.0]
+
+    def step():
+        t = t_sim[0]
+        if nlev == 1:
+            g.fill_ghost(1, t)
+            g.advance_level(1, dt)
+        else:
+            binding.berger_oliger(g, 1, t, dt, ratios, nlev)
+        t_sim[0] = t + dt
+
+    for _ in range(max(args.warmup, 3) if args.warmup > 0 else 0):
+        step()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-resident timed region
+    g.reset_stats()
+    g.set_profiling(True)
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    barrier()
+    clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    st = g.stats()
+    g.set_profiling(False)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = total_cells_per_step * args.steps / (ms / 1000.0)
+
+    # ---- roofline of the dominant kernel (the fused step kernel)
+    peak, peak_src = measured_peaks()
+    launches = max(st["step_launches"], 1)
+    avg_ms = st["step_ms"] / launches
+    bytes_per_launch = BYTES_PER_CELL * cells_per_step_rank / max(1, sum(mult))  # per level-launch mean
+    if nlev == 1:
+        bytes_per_launch = BYTES_PER_CELL * cells_owned[0]
+    achieved = bytes_per_launch / (avg_ms / 1000.0) / 1e9 if avg_ms > 0 else None
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_step_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                pj = json.load(f)
+            ent = pj.get(wl.name)
+            if ent and world == 1:
+                traffic = float(ent["dram_bytes_per_launch"])
+        except (OSError, ValueError, KeyError):
+            traffic = None
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+            "kernel": "step_kernel<MC,2>", "bytes_per_cell": BYTES_PER_CELL,
+            "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,
+            "kernel_share_of_step": (st["step_ms"] / ms) if ms > 0 else None,
+            "peak_source": peak_src,
+            "nominal_8tbs_frac": (achieved / 8000.0) if achieved else None}
+
+    # ---- e2e through the public API with host buffers (H2D + steps + D2H)
+    e2e = None
+    if not args.no_e2e:
+        out_host = [torch.empty_like(b, pin_memory=True) for b in host_q]
+        barrier()
+        t0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for L, b in enumerate(host_q, start=1):
+            g.write_level(L, b)
+        for _ in range(args.steps):
+            step()
+        for L, b in enumerate(out_host, start=1):
+            g.read_level(L, b)
+        e1.record(stream)
+        barrier()
+        ems = e0.elapsed_time(e1)
+        wall = (time.perf_counter() - t0) * 1000.0
+        if world > 1:
+            t = torch.tensor([ems], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        state_bytes = sum(8 * b.numel() for b in host_q)
+        e2e = {"value": total_cells_per_step * args.steps / (ems / 1000.0), "unit": "cell-updates/s",
+               "h2d_bytes_per_step": state_bytes / args.steps + 8 * sum(mult),
+               "d2h_bytes_per_step": state_bytes / args.steps + 8 * sum(mult),
+               "ms": ems, "wall_ms": wall,
+               "what": "write_level (pinned host->device) + K x (fill_ghost + advance_level -> 8-byte cfl) "
+                       "+ read_level (device->pinned host), per rank, max over ranks"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        oracle.build()
+        v, cores, desc = oracle_sample(wl, budget_s=12.0)
+        cpu = {"value": v, "unit": "cell-updates/s", "cores": cores, "kind": "oracle", "sample": desc,
+               "cpu": cpu_model()}
+
+    clk = clocks.summary()
+    gpu_launches = st["step_launches"] + st["ghost_launches"]
+    if rank == 0:
+        line = {"metric": "fp64 cell-updates/s", "value": value, "unit": "cell-updates/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": wl.name, "note": wl.note, "levels": nlev,
+                           "patches": int(sum(len(lv.descs) for lv in wl.levels)),
+                           "cells_per_step": total_cells_per_step, "limiter": "MC", "order_trans": 2,
+                           "cfl": wl.cfl, "ic": "ring (Clawpack acoustics_2d_radial qinit)",
+                           "parallelism": f"patch-partitioned over {world} rank(s), NCCL halo + max all-reduce"
+                           if world > 1 else "single GPU",
+                           "l2": "state per buffer exceeds L2 (126 MB); no flush needed"
+                           if total_cells_per_step * 24 > 126e6 else "state fits L2 (latency-bound config)"},
+                "roofline": roof, "clocks": clk, "e2e": e2e, "gpu_launches": gpu_launches,
+                "per_gpu_value": value / world}
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    g.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,185 @@
+/*
+ * claw.h -- C ABI of libclaw.so, the B200 (sm_100a) batched AMR-level advance
+ * for 2D linear acoustics with Clawpack's wave-propagation method
+ * (arXiv 1808.02638, Qin, LeVeque & Motley).
+ *
+ * Citations: P:a-b = /root/reference/PAPER.md lines a-b (section / equation
+ * named), S:a-b = SPEC.md lines (interfaces only).  DESIGN.md lists every
+ * reading of the paper these calls implement.
+ *
+ * Conventions for every entry point
+ *   - Return value: CLAW_OK (0) or a negative CLAW_E* code; nothing aborts or
+ *     throws.  claw_last_error() names the offending field / patch.
+ *   - Host arrays passed in are copied during the call; the library keeps no
+ *     caller pointer.  Device memory, tables, events and the NCCL communicator
+ *     are owned by the context (a caller-supplied stream is borrowed).
+ *   - One context per device and process; a context is not thread-safe.
+ *   - CLAW_ECUDA / CLAW_ENCCL are sticky: the context is unusable afterwards.
+ *   - Patch data on the host is [3][my][mx] per patch: components (p, u, v),
+ *     x fastest, fp64.  "Level arrays" concatenate the patches a rank OWNS in
+ *     ascending global patch index (claw_owner tells which rank owns what).
+ *
+ * Call order: claw_create; claw_set_level(1), then 2.. (each nested in the
+ * previous); per level step claw_fill_ghost(L, t) then claw_advance_level(L,
+ * dt); claw_read* at any time.
+ */
+#ifndef CLAW_H
+#define CLAW_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CLAW_OK 0
+#define CLAW_EINVAL (-1)     /* bad argument / descriptor field */
+#define CLAW_ESTATE (-2)     /* call order violated */
+#define CLAW_ENOMEM (-3)     /* device or host allocation failed */
+#define CLAW_ECUDA (-4)      /* CUDA error (sticky) */
+#define CLAW_ENCCL (-5)      /* NCCL error or NCCL unavailable (sticky) */
+#define CLAW_ENEST (-6)      /* ghost cell with no same-level or coarse donor */
+#define CLAW_ENODEV (-8)     /* compute requested from a host-only (device = -1) context */
+
+#define CLAW_BC_EXTRAP 1     /* zero-order extrapolation, the paper's outflow BC */
+#define CLAW_BC_PERIODIC 2
+
+/* One grid patch (uniform rectangular patch of a level; P:125-126:
+ * mbc ghost cells around it).  Same field list as north_star's descriptor. */
+typedef struct {
+  int32_t mx, my;          /* interior cells, >= 1 */
+  double dx, dy;           /* > 0, identical for every patch of a level */
+  double xlower, ylower;   /* physical lower-left corner of the interior; must
+                              sit on the level's index grid */
+  int32_t mbc;             /* ghost width; must be 2 (the stencil is 5x5 minus corners) */
+  double rho, K;           /* density rho_0 and bulk modulus K_0 of P:457-466, > 0;
+                              c = sqrt(K/rho), Z = rho c */
+} claw_patch_desc;
+
+typedef struct {
+  double xlo, xhi, ylo, yhi;   /* physical domain; level-1 patches must tile it */
+  int32_t bc[4];               /* left, right, bottom, top: CLAW_BC_*; periodic pairs */
+  int32_t limiter;             /* wave limiter phi: 0 none (Lax-Wendroff), 1 minmod,
+                                  2 superbee, 3 van Leer, 4 MC */
+  int32_t order_trans;         /* transverse propagation ("corner transport"):
+                                  0 none, 1 fluctuations, 2 fluctuations + corrections */
+  int32_t device;              /* CUDA device ordinal; -1 = host-only context that
+                                  builds every table but never touches CUDA (tests) */
+  int32_t rank, world;         /* this process's rank among `world` (1 = no NCCL) */
+  const void* nccl_unique_id;  /* world > 1: 128-byte ncclUniqueId, identical on
+                                  every rank (distributed by the caller) */
+  void* stream;                /* cudaStream_t to launch on, or NULL: the library
+                                  creates a non-blocking stream */
+  int32_t tile_rows;           /* rows per tile of the fused step kernel (0 = default
+                                  64); results are bitwise independent of it */
+  int32_t reserved[7];
+} claw_config;
+
+/* Kernel-level statistics, accumulated while profiling is on. */
+typedef struct {
+  int64_t step_launches;        /* fused step kernel launches */
+  double step_ms;               /* summed CUDA-event time of those launches */
+  int64_t ghost_launches;       /* ghost-fill (coarse interp / pack) launches */
+  double ghost_ms;
+  int64_t cells_advanced;       /* interior cell-updates performed */
+  int64_t halo_bytes_sent;      /* NCCL halo bytes sent by this rank */
+} claw_stats;
+
+typedef struct claw_ctx claw_ctx;
+
+/* Create a context: validates cfg (EINVAL), selects the device, creates or
+ * adopts the stream, and for world > 1 joins the NCCL communicator (ENCCL). */
+int claw_create(const claw_config* cfg, claw_ctx** out);
+int claw_destroy(claw_ctx* ctx);
+const char* claw_last_error(const claw_ctx* ctx);
+
+/* Deterministic owner map used by claw_set_level for `world` ranks: patches in
+ * Morton order of their lower-left index, split contiguously into chunks of
+ * ~equal cell count.  owner[npatch] receives ranks.  Host-only. */
+int claw_partition(int32_t npatch, const claw_patch_desc* descs, int32_t world,
+                   int32_t* owner);
+
+/* Define level `level` (1..8) from the FULL descriptor list (identical on every
+ * rank).  Validates (EINVAL: mx,my < 1, mbc != 2, rho/K <= 0, dx/dy differing
+ * within the level, patch off the level grid or outside the domain, same-level
+ * overlap, level 1 not tiling the domain; ENEST: a ghost cell without donor),
+ * builds the ghost-source, tile and exchange tables, allocates the level's
+ * device pool (two ping-pong buffers) and uploads q0 (NULL = zeros): the
+ * owned patches' level array.  Replaces any previous definition of the level;
+ * finer levels must be set again afterwards.  world > 1 requires a single
+ * level. */
+int claw_set_level(claw_ctx* ctx, int32_t level, int32_t npatch,
+                   const claw_patch_desc* descs, const double* q0);
+
+/* Ghost fill at time t: same-level and physical-BC ghosts are read
+ * by the step kernel straight from their donors' interiors; this call fills
+ * the ghost cells that need work: space-time interpolation from level-1's two
+ * time levels (t must lie in level-1's [t_old, t_new], else ESTATE), and for
+ * world > 1 the NCCL halo exchange with neighbouring ranks. */
+int claw_fill_ghost(claw_ctx* ctx, int32_t level, double t);
+
+/* One step of eq. (W) on every owned patch of `level` with time step
+ * dt (>= 0): x/y Riemann solves, wave limiter, second-order corrections,
+ * transverse propagation and flux-difference update in ONE fused kernel
+ * launch, plus the per-patch max Courant number nu = |s| dt/dx (P:230-232,
+ * P:417-420) reduced on the device to the level max (and across ranks with an
+ * NCCL max all-reduce).  *cfl_max receives it (8-byte device-to-host copy;
+ * the only per-step host synchronisation).  cfl_max > 1 is returned, not
+ * rejected.  dt = 0 leaves q unchanged and gives cfl_max = 0. */
+int claw_advance_level(claw_ctx* ctx, int32_t level, double dt, double* cfl_max);
+
+/* Same as claw_advance_level without the host synchronisation; the result is
+ * fetched later with claw_wait_cfl (for CUDA-graph / pipelined drivers). */
+int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt);
+int claw_wait_cfl(claw_ctx* ctx, int32_t level, double* cfl_max);
+
+/* Interior of one owned patch, [3][my][mx] (EINVAL if not owned here). */
+int claw_read(claw_ctx* ctx, int32_t level, int32_t patch, double* q_out);
+int claw_write(claw_ctx* ctx, int32_t level, int32_t patch, const double* q_in);
+/* The owned patches' level array (see conventions above). */
+int claw_read_level(claw_ctx* ctx, int32_t level, double* q_out);
+int claw_write_level(claw_ctx* ctx, int32_t level, const double* q_in);
+/* [3][my+4][mx+4]: the patch with its ghost frame exactly as the step kernel
+ * sees it after claw_fill_ghost (ghost-fill parity checks). */
+int claw_read_padded(claw_ctx* ctx, int32_t level, int32_t patch, double* q_out);
+/* Per-patch max Courant number of the last step (owned patches). */
+int claw_patch_cfl(claw_ctx* ctx, int32_t level, int32_t patch, double* cfl);
+
+int claw_owner(const claw_ctx* ctx, int32_t level, int32_t patch, int32_t* rank);
+int claw_level_owned(const claw_ctx* ctx, int32_t level, int32_t* npatch_owned,
+                     int64_t* cells_owned, int64_t* device_bytes);
+
+/* Host-only introspection of the ghost-source tables (works with device=-1):
+ * for every cell of the padded frame of `patch`, out[(j+2)*(mx+4)+(i+2)]
+ * receives the global patch index whose interior supplies the value
+ * (patch*2^32 + local_j*2^16 + local_i), or -1 for coarse-interpolated cells,
+ * or -2 for cells received from another rank (their donor is then in
+ * out2, may be NULL). */
+int claw_debug_ghost_sources(const claw_ctx* ctx, int32_t level, int32_t patch,
+                             int64_t* out, int64_t* out2);
+/* Halo exchange plan: number of cells this rank sends to / receives from
+ * `peer` for `level`. */
+int claw_debug_halo_counts(const claw_ctx* ctx, int32_t level, int32_t peer,
+                           int64_t* nsend, int64_t* nrecv);
+/* The k-th cell sent to `peer`: global donor patch and local (i, j). */
+int claw_debug_halo_send(const claw_ctx* ctx, int32_t level, int32_t peer,
+                         int64_t k, int32_t* patch, int32_t* i, int32_t* j);
+
+int claw_set_profiling(claw_ctx* ctx, int32_t on);
+int claw_get_stats(claw_ctx* ctx, claw_stats* out);   /* synchronises */
+int claw_reset_stats(claw_ctx* ctx);
+int claw_synchronize(claw_ctx* ctx);
+
+/* Create an NCCL unique id (128 bytes) on one rank, to be broadcast to all
+ * ranks by the caller (e.g. torch.distributed) before claw_create.  ENCCL if
+ * NCCL cannot be loaded. */
+int claw_nccl_unique_id(void* out128);
+
+/* Library version / build string (host-only). */
+const char* claw_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

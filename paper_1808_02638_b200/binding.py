@@ -1,0 +1,307 @@
+"""Thin ctypes binding of libclaw.so (include/claw.h) -- argument marshalling only.
+
+Every step of the hot path runs in the library's sm_100a kernels; this module
+never computes anything of the method.  It fails loudly (ClawError) when the
+shared library is missing: there is no CPU fallback.
+
+PyTorch enters only as plumbing: the binding can adopt torch's current CUDA
+stream (`stream=torch.cuda.current_stream().cuda_stream`) and torch.distributed
+broadcasts the NCCL unique id (see `parallel_context`).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+
+import numpy as np
+
+from .workloads import PATCH_DTYPE
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("CLAW_LIB") or os.path.join(_PKG, "libclaw.so")
+
+CLAW_OK, CLAW_EINVAL, CLAW_ESTATE, CLAW_ENOMEM = 0, -1, -2, -3
+CLAW_ECUDA, CLAW_ENCCL, CLAW_ENEST, CLAW_ENODEV = -4, -5, -6, -8
+ERR_NAMES = {-1: "EINVAL", -2: "ESTATE", -3: "ENOMEM", -4: "ECUDA", -5: "ENCCL", -6: "ENEST", -8: "ENODEV"}
+
+EXPORTS = [
+    "claw_create", "claw_destroy", "claw_last_error", "claw_partition", "claw_set_level",
+    "claw_fill_ghost", "claw_advance_level", "claw_advance_level_async", "claw_wait_cfl",
+    "claw_read", "claw_write", "claw_read_level", "claw_write_level", "claw_read_padded",
+    "claw_patch_cfl", "claw_owner", "claw_level_owned", "claw_debug_ghost_sources",
+    "claw_debug_halo_counts", "claw_debug_halo_send", "claw_set_profiling", "claw_get_stats",
+    "claw_reset_stats", "claw_synchronize", "claw_nccl_unique_id", "claw_version",
+]
+
+
+class ClawError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{ERR_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class ClawConfig(ctypes.Structure):
+    _fields_ = [("xlo", ctypes.c_double), ("xhi", ctypes.c_double),
+                ("ylo", ctypes.c_double), ("yhi", ctypes.c_double),
+                ("bc", ctypes.c_int32 * 4), ("limiter", ctypes.c_int32),
+                ("order_trans", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+                ("nccl_unique_id", ctypes.c_void_p), ("stream", ctypes.c_void_p),
+                ("tile_rows", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+
+
+class ClawStats(ctypes.Structure):
+    _fields_ = [("step_launches", ctypes.c_int64), ("step_ms", ctypes.c_double),
+                ("ghost_launches", ctypes.c_int64), ("ghost_ms", ctypes.c_double),
+                ("cells_advanced", ctypes.c_int64), ("halo_bytes_sent", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libclaw.so from the package directory (raises if absent)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ClawError(CLAW_ENODEV, f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                                     "(no CPU fallback exists)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, dp, i32, i64, d = ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int32, \
+        ctypes.POINTER(ctypes.c_int64), ctypes.c_double
+    L.claw_create.argtypes = [ctypes.POINTER(ClawConfig), ctypes.POINTER(vp)]
+    L.claw_destroy.argtypes = [vp]
+    L.claw_last_error.argtypes = [vp]
+    L.claw_last_error.restype = ctypes.c_char_p
+    L.claw_version.restype = ctypes.c_char_p
+    L.claw_partition.argtypes = [i32, vp, i32, ctypes.POINTER(ctypes.c_int32)]
+    L.claw_set_level.argtypes = [vp, i32, i32, vp, dp]
+    L.claw_fill_ghost.argtypes = [vp, i32, d]
+    L.claw_advance_level.argtypes = [vp, i32, d, dp]
+    L.claw_advance_level_async.argtypes = [vp, i32, d]
+    L.claw_wait_cfl.argtypes = [vp, i32, dp]
+    for f in ("claw_read", "claw_read_padded", "claw_patch_cfl"):
+        getattr(L, f).argtypes = [vp, i32, i32, dp]
+    L.claw_write.argtypes = [vp, i32, i32, dp]
+    L.claw_read_level.argtypes = [vp, i32, dp]
+    L.claw_write_level.argtypes = [vp, i32, dp]
+    L.claw_owner.argtypes = [vp, i32, i32, ctypes.POINTER(ctypes.c_int32)]
+    L.claw_level_owned.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_int32), i64, i64]
+    L.claw_debug_ghost_sources.argtypes = [vp, i32, i32, i64, i64]
+    L.claw_debug_halo_counts.argtypes = [vp, i32, i32, i64, i64]
+    L.claw_debug_halo_send.argtypes = [vp, i32, i32, ctypes.c_int64, ctypes.POINTER(ctypes.c_int32),
+                                       ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
+    L.claw_set_profiling.argtypes = [vp, i32]
+    L.claw_get_stats.argtypes = [vp, ctypes.POINTER(ClawStats)]
+    L.claw_reset_stats.argtypes = [vp]
+    L.claw_synchronize.argtypes = [vp]
+    L.claw_nccl_unique_id.argtypes = [vp]
+    _lib = L
+    return L
+
+
+def _dptr(a):
+    if hasattr(a, "data_ptr"):  # torch tensor (pinned host or device)
+        return ctypes.cast(ctypes.c_void_p(a.data_ptr()), ctypes.POINTER(ctypes.c_double))
+    assert a.dtype == np.float64 and a.flags["C_CONTIGUOUS"], "need C-contiguous float64"
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _descs(descs) -> np.ndarray:
+    d = np.ascontiguousarray(np.asarray(descs).astype(PATCH_DTYPE))
+    return d
+
+
+def partition(descs, world: int) -> np.ndarray:
+    d = _descs(descs)
+    out = np.zeros(len(d), dtype=np.int32)
+    rc = load().claw_partition(len(d), d.ctypes.data, world,
+                               out.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)))
+    if rc:
+        raise ClawError(rc, "claw_partition failed")
+    return out
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    rc = load().claw_nccl_unique_id(buf)
+    if rc:
+        raise ClawError(rc, "NCCL unique id")
+    return buf.raw
+
+
+def version() -> str:
+    return load().claw_version().decode()
+
+
+class Claw:
+    """One libclaw context (one device, one rank)."""
+
+    def __init__(self, domain=(-1.0, 1.0, -1.0, 1.0), bc=(1, 1, 1, 1), limiter=4,
+                 order_trans=2, device=0, rank=0, world=1, nccl_id: bytes | None = None,
+                 stream: int | None = None, tile_rows: int = 0):
+        L = load()
+        self._idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None
+        cfg = ClawConfig(*[float(v) for v in domain], (ctypes.c_int32 * 4)(*bc), int(limiter),
+                         int(order_trans), int(device), int(rank), int(world),
+                         ctypes.cast(self._idbuf, ctypes.c_void_p) if self._idbuf else None,
+                         stream, int(tile_rows))
+        self._h = ctypes.c_void_p()
+        rc = L.claw_create(ctypes.byref(cfg), ctypes.byref(self._h))
+        if rc:
+            msg = L.claw_last_error(self._h).decode() if self._h else ""
+            if self._h:
+                L.claw_destroy(self._h)
+                self._h = None
+            raise ClawError(rc, msg or "claw_create failed")
+        self.world, self.rank = world, rank
+        self._descs = {}
+
+    # -- lifecycle -------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None):
+            load().claw_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _check(self, rc):
+        if rc:
+            raise ClawError(rc, load().claw_last_error(self._h).decode())
+
+    # -- the five calls of north_star -----------------------------------
+    def set_level(self, level: int, descs, q0=None):
+        d = _descs(descs)
+        self._descs[level] = d
+        self._check(load().claw_set_level(self._h, level, len(d), d.ctypes.data,
+                                          None if q0 is None else _dptr(q0)))
+
+    def fill_ghost(self, level: int, t: float = 0.0):
+        self._check(load().claw_fill_ghost(self._h, level, float(t)))
+
+    def advance_level(self, level: int, dt: float) -> float:
+        c = ctypes.c_double()
+        self._check(load().claw_advance_level(self._h, level, float(dt), ctypes.byref(c)))
+        return c.value
+
+    def advance_level_async(self, level: int, dt: float):
+        self._check(load().claw_advance_level_async(self._h, level, float(dt)))
+
+    def wait_cfl(self, level: int) -> float:
+        c = ctypes.c_double()
+        self._check(load().claw_wait_cfl(self._h, level, ctypes.byref(c)))
+        return c.value
+
+    def read(self, level: int, patch: int) -> np.ndarray:
+        d = self._descs[level][patch]
+        out = np.empty((3, int(d["my"]), int(d["mx"])))
+        self._check(load().claw_read(self._h, level, patch, _dptr(out)))
+        return out
+
+    def write(self, level: int, patch: int, q):
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        self._check(load().claw_write(self._h, level, patch, _dptr(q)))
+
+    # -- level-wide I/O --------------------------------------------------
+    def owned_patches(self, level: int) -> np.ndarray:
+        return np.array([p for p in range(len(self._descs[level])) if self.owner(level, p) == self.rank],
+                        dtype=np.int64)
+
+    def level_size(self, level: int) -> int:
+        n, cells, b = self.level_owned(level)
+        return 3 * cells
+
+    def read_level(self, level: int, out=None):
+        if out is None:
+            out = np.empty(self.level_size(level))
+        self._check(load().claw_read_level(self._h, level, _dptr(out)))
+        return out
+
+    def write_level(self, level: int, q):
+        if not hasattr(q, "data_ptr"):
+            q = np.ascontiguousarray(q, dtype=np.float64)
+        self._check(load().claw_write_level(self._h, level, _dptr(q)))
+
+    def read_padded(self, level: int, patch: int) -> np.ndarray:
+        d = self._descs[level][patch]
+        out = np.empty((3, int(d["my"]) + 4, int(d["mx"]) + 4))
+        self._check(load().claw_read_padded(self._h, level, patch, _dptr(out)))
+        return out
+
+    def patch_cfl(self, level: int, patch: int) -> float:
+        c = ctypes.c_double()
+        self._check(load().claw_patch_cfl(self._h, level, patch, ctypes.byref(c)))
+        return c.value
+
+    def owner(self, level: int, patch: int) -> int:
+        r = ctypes.c_int32()
+        self._check(load().claw_owner(self._h, level, patch, ctypes.byref(r)))
+        return r.value
+
+    def level_owned(self, level: int):
+        n, c, b = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()
+        self._check(load().claw_level_owned(self._h, level, ctypes.byref(n), ctypes.byref(c), ctypes.byref(b)))
+        return n.value, c.value, b.value
+
+    # -- introspection ---------------------------------------------------
+    def debug_ghost_sources(self, level: int, patch: int):
+        d = self._descs[level][patch]
+        n = (int(d["mx"]) + 4) * (int(d["my"]) + 4)
+        a = np.zeros(n, dtype=np.int64)
+        b = np.zeros(n, dtype=np.int64)
+        self._check(load().claw_debug_ghost_sources(
+            self._h, level, patch, a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+            b.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))))
+        shape = (int(d["my"]) + 4, int(d["mx"]) + 4)
+        return a.reshape(shape), b.reshape(shape)
+
+    def debug_halo_counts(self, level: int, peer: int):
+        s, r = ctypes.c_int64(), ctypes.c_int64()
+        self._check(load().claw_debug_halo_counts(self._h, level, peer, ctypes.byref(s), ctypes.byref(r)))
+        return s.value, r.value
+
+    def debug_halo_send(self, level: int, peer: int, k: int):
+        p, i, j = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        self._check(load().claw_debug_halo_send(self._h, level, peer, k, ctypes.byref(p),
+                                                ctypes.byref(i), ctypes.byref(j)))
+        return p.value, i.value, j.value
+
+    def set_profiling(self, on: bool = True):
+        self._check(load().claw_set_profiling(self._h, int(on)))
+
+    def stats(self) -> dict:
+        s = ClawStats()
+        self._check(load().claw_get_stats(self._h, ctypes.byref(s)))
+        return {k: getattr(s, k) for k, _ in ClawStats._fields_}
+
+    def reset_stats(self):
+        self._check(load().claw_reset_stats(self._h))
+
+    def synchronize(self):
+        self._check(load().claw_synchronize(self._h))
+
+
+def berger_oliger(claw: Claw, level: int, t: float, dt: float, ratios: dict, nlevels: int) -> float:
+    """Advance `level` from t by dt, then recursively the finer level R_L times
+    with dt / R_L, coarse level first.  ratios[L] = R_L between
+    levels L and L+1.  Returns the max CFL number seen."""
+    claw.fill_ghost(level, t)
+    cfl = claw.advance_level(level, dt)
+    if level < nlevels:
+        R = ratios[level]
+        dtf = dt / R
+        for k in range(R):
+            cfl = max(cfl, berger_oliger(claw, level + 1, t + k * dtf, dtf, ratios, nlevels))
+    return cfl

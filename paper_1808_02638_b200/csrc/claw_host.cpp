@@ -1,0 +1,1196 @@
+// claw_host.cpp -- C ABI of libclaw.so (include/claw.h): validation, level
+// planning (owner map, ghost-source tables, tiles, halo plan), the device
+// patch pool and the per-step driver around the sm_100a kernels.
+//
+// Paper map: patch hierarchy P:97-106; ghost cells and their three
+// sources P:125-132; level-by-level advance P:113-118; CFL P:227-233,
+// P:282-288; GPU memory pool P:422-426; one merged launch per level instead of
+// per-patch kernels P:296-299; per-patch max-speed array reduced to
+// a level max P:417-420.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/claw.h"
+#include "claw_internal.h"
+
+using claw::DevInterp;
+using claw::DevPatch;
+using claw::DevRect;
+
+namespace {
+
+constexpr int kMaxLevel = 8;
+constexpr int kBucket = 16;
+
+// ---------------------------------------------------------------------------
+// NCCL through dlopen: the library loads without NCCL; world > 1 needs it.
+// ---------------------------------------------------------------------------
+struct Nccl {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool load(std::string& err) {
+    if (h) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) {
+      err = "NCCL (libnccl.so.2) could not be loaded";
+      return false;
+    }
+#define SYM(f)                                                   \
+  f = reinterpret_cast<decltype(f)>(dlsym(h, "nccl" #f));        \
+  if (!f) {                                                      \
+    err = "NCCL symbol nccl" #f " missing";                      \
+    return false;                                                \
+  }
+    SYM(GetUniqueId) SYM(CommInitRank) SYM(CommDestroy) SYM(AllReduce) SYM(Send) SYM(Recv)
+    SYM(GroupStart) SYM(GroupEnd) SYM(GetErrorString)
+#undef SYM
+    return true;
+  }
+};
+Nccl g_nccl;
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  ~DevBuf() { reset(); }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  cudaError_t alloc(size_t count) {
+    reset();
+    if (count == 0) return cudaSuccess;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T));
+    if (e == cudaSuccess) n = count;
+    else p = nullptr;
+    return e;
+  }
+};
+
+// Per-cell ghost source (host side of the planner).
+struct Src {
+  int kind;        // 0 local same-level interior, 1 frame (coarse / remote), -1 unset
+  int64_t base;    // element offset (p component) in the level buffer / frame
+  int64_t cs;      // component stride
+};
+
+struct Level {
+  bool set = false;
+  int npatch = 0;
+  std::vector<claw_patch_desc> desc;
+  std::vector<int64_t> i0, j0;
+  int64_t nx = 0, ny = 0;
+  int ratio = 0;  // to the coarser level
+  double dx = 0, dy = 0;
+  std::vector<int32_t> owner;
+  std::vector<int32_t> local;       // global patch -> owned index or -1
+  std::vector<int32_t> owned;       // owned index -> global patch
+  std::vector<int64_t> off;         // owned index -> element offset
+  int64_t buf_elems = 0;
+  bool gapless = true;
+  int64_t cells_owned = 0;
+  // bucket grid
+  int64_t nbx = 0, nby = 0;
+  std::vector<int64_t> bstart;
+  std::vector<int32_t> blist;
+  // host tables
+  std::vector<DevPatch> hpatch;
+  std::vector<DevRect> hrect;
+  std::vector<int4> htile;
+  std::vector<DevInterp> hinterp;
+  // debug: per owned patch, per padded cell, donor code
+  std::vector<std::vector<int64_t>> dbg_src, dbg_remote;
+  // halo plan (per peer)
+  std::vector<std::vector<int64_t>> send_off, send_cs;
+  std::vector<std::vector<int64_t>> send_dbg;  // patch<<32 | j<<16 | i
+  std::vector<int64_t> nrecv, recv_frame_off;
+  int64_t frame_elems = 0;
+  int64_t coarse_frame_off = 0, ncoarse = 0;
+  // device
+  DevBuf<double> q[2];
+  int cur = 0;
+  DevBuf<double> frame;
+  DevBuf<DevPatch> dpatch;
+  DevBuf<DevRect> drect;
+  DevBuf<int4> dtile;
+  DevBuf<DevInterp> dinterp;
+  DevBuf<unsigned long long> pcfl;  // per owned patch
+  DevBuf<unsigned long long> lcfl;  // level slot
+  std::vector<std::unique_ptr<DevBuf<int64_t>>> dsend_off, dsend_cs;
+  std::vector<std::unique_ptr<DevBuf<double>>> dsend_buf;
+  double t_old = 0, t_new = 0;
+  bool stepped_once = false;
+  int64_t device_bytes = 0;
+  bool uniform = false;  // every patch shares (c, Z): step constants as kernel params
+
+  int find(int64_t I, int64_t J) const {
+    if (I < 0 || J < 0 || I >= nx || J >= ny) return -1;
+    const int64_t b = (J / kBucket) * nbx + (I / kBucket);
+    for (int64_t k = bstart[b]; k < bstart[b + 1]; ++k) {
+      const int p = blist[k];
+      if (I >= i0[p] && I < i0[p] + desc[p].mx && J >= j0[p] && J < j0[p] + desc[p].my) return p;
+    }
+    return -1;
+  }
+};
+
+}  // namespace
+
+struct claw_ctx {
+  claw_config cfg{};
+  bool host_only = false;
+  bool dead = false;       // sticky CUDA / NCCL failure
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  ncclComm_t comm = nullptr;
+  Level lev[kMaxLevel + 1];
+  double* h_cfl = nullptr;  // pinned 8 bytes
+  std::string err;
+  bool profiling = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_step, ev_ghost, ev_pool;
+  claw_stats stats{};
+  int tile_rows = 64;
+};
+
+namespace {
+
+int fail(claw_ctx* c, int code, const char* fmt, ...) {
+  if (c) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    c->err = buf;
+  }
+  return code;
+}
+
+int cuda_fail(claw_ctx* c, cudaError_t e, const char* where) {
+  c->dead = true;
+  return fail(c, CLAW_ECUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define CUDA_TRY(expr)                                 \
+  do {                                                 \
+    cudaError_t e_ = (expr);                           \
+    if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #expr); \
+  } while (0)
+
+int nccl_fail(claw_ctx* c, ncclResult_t r, const char* where) {
+  c->dead = true;
+  return fail(c, CLAW_ENCCL, "%s: %s", where,
+              g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "nccl error");
+}
+
+int64_t map_axis(int64_t I, int64_t n, int bc_lo, int bc_hi) {
+  if (I < 0) return (bc_lo == CLAW_BC_PERIODIC) ? ((I % n) + n) % n : 0;
+  if (I >= n) return (bc_hi == CLAW_BC_PERIODIC) ? I % n : n - 1;
+  return I;
+}
+
+uint64_t morton(uint32_t x, uint32_t y) {
+  auto spread = [](uint64_t v) {
+    v &= 0xffffffffull;
+    v = (v | (v << 16)) & 0x0000ffff0000ffffull;
+    v = (v | (v << 8)) & 0x00ff00ff00ff00ffull;
+    v = (v | (v << 4)) & 0x0f0f0f0f0f0f0f0full;
+    v = (v | (v << 2)) & 0x3333333333333333ull;
+    v = (v | (v << 1)) & 0x5555555555555555ull;
+    return v;
+  };
+  return spread(x) | (spread(y) << 1);
+}
+
+void partition_impl(int npatch, const claw_patch_desc* d, const std::vector<int64_t>& i0,
+                    const std::vector<int64_t>& j0, int world, int32_t* owner) {
+  if (world <= 1) {
+    for (int p = 0; p < npatch; ++p) owner[p] = 0;
+    return;
+  }
+  std::vector<int> order(npatch);
+  for (int p = 0; p < npatch; ++p) order[p] = p;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    return morton(static_cast<uint32_t>(i0[a]), static_cast<uint32_t>(j0[a])) <
+           morton(static_cast<uint32_t>(i0[b]), static_cast<uint32_t>(j0[b]));
+  });
+  int64_t total = 0;
+  for (int p = 0; p < npatch; ++p) total += static_cast<int64_t>(d[p].mx) * d[p].my;
+  // greedy contiguous split: rank r takes patches until its running total
+  // reaches the (r+1)/world quantile (closest boundary)
+  int r = 0;
+  int64_t acc = 0;
+  for (int k = 0; k < npatch; ++k) {
+    const int p = order[k];
+    const int64_t w = static_cast<int64_t>(d[p].mx) * d[p].my;
+    const double target = static_cast<double>(total) * (r + 1) / world;
+    if (r < world - 1 && acc > 0 &&
+        std::fabs(static_cast<double>(acc + w) - target) > std::fabs(static_cast<double>(acc) - target))
+      ++r;
+    owner[p] = r;
+    acc += w;
+  }
+}
+
+int validate_config(claw_ctx* c, const claw_config* cfg) {
+  if (!(cfg->xhi > cfg->xlo) || !(cfg->yhi > cfg->ylo)) return fail(c, CLAW_EINVAL, "domain: xhi>xlo, yhi>ylo required");
+  for (int k = 0; k < 4; ++k)
+    if (cfg->bc[k] != CLAW_BC_EXTRAP && cfg->bc[k] != CLAW_BC_PERIODIC)
+      return fail(c, CLAW_EINVAL, "bc[%d]=%d: must be 1 (extrapolation) or 2 (periodic)", k, cfg->bc[k]);
+  if ((cfg->bc[0] == CLAW_BC_PERIODIC) != (cfg->bc[1] == CLAW_BC_PERIODIC) ||
+      (cfg->bc[2] == CLAW_BC_PERIODIC) != (cfg->bc[3] == CLAW_BC_PERIODIC))
+    return fail(c, CLAW_EINVAL, "bc: periodic boundaries must come in pairs");
+  if (cfg->limiter < 0 || cfg->limiter > 4) return fail(c, CLAW_EINVAL, "limiter=%d: must be 0..4", cfg->limiter);
+  if (cfg->order_trans < 0 || cfg->order_trans > 2)
+    return fail(c, CLAW_EINVAL, "order_trans=%d: must be 0..2", cfg->order_trans);
+  if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world)
+    return fail(c, CLAW_EINVAL, "rank=%d world=%d", cfg->rank, cfg->world);
+  if (cfg->world > 1 && !cfg->nccl_unique_id && cfg->device >= 0)
+    return fail(c, CLAW_EINVAL, "world>1 needs nccl_unique_id");
+  if (cfg->tile_rows < 0 || cfg->tile_rows > claw::max_tile_rows())
+    return fail(c, CLAW_EINVAL, "tile_rows=%d: must be 0..%d", cfg->tile_rows, claw::max_tile_rows());
+  return CLAW_OK;
+}
+
+// Validate descriptors and integer boxes of a level (S:51-style messages).
+int build_geometry(claw_ctx* c, int level, int npatch, const claw_patch_desc* d, Level& L) {
+  const claw_config& cfg = c->cfg;
+  L.npatch = npatch;
+  L.desc.assign(d, d + npatch);
+  L.dx = d[0].dx;
+  L.dy = d[0].dy;
+  if (!(L.dx > 0) || !(L.dy > 0)) return fail(c, CLAW_EINVAL, "patch 0: dx, dy must be > 0");
+  L.nx = std::llround((cfg.xhi - cfg.xlo) / L.dx);
+  L.ny = std::llround((cfg.yhi - cfg.ylo) / L.dy);
+  if (std::fabs((cfg.xhi - cfg.xlo) / L.dx - L.nx) > 1e-6 || std::fabs((cfg.yhi - cfg.ylo) / L.dy - L.ny) > 1e-6)
+    return fail(c, CLAW_EINVAL, "level %d: dx/dy do not divide the domain", level);
+  if (level > 1) {
+    const Level& C = c->lev[level - 1];
+    const double rx = C.dx / L.dx, ry = C.dy / L.dy;
+    L.ratio = static_cast<int>(std::llround(rx));
+    if (L.ratio < 1 || std::fabs(rx - L.ratio) > 1e-9 || std::fabs(ry - L.ratio) > 1e-9)
+      return fail(c, CLAW_EINVAL, "level %d: refinement ratio must be an integer, equal in x and y", level);
+  }
+  L.i0.resize(npatch);
+  L.j0.resize(npatch);
+  int64_t cells = 0;
+  for (int p = 0; p < npatch; ++p) {
+    const claw_patch_desc& q = d[p];
+    if (q.mx < 1 || q.my < 1) return fail(c, CLAW_EINVAL, "patch %d: mx=%d my=%d must be >= 1", p, q.mx, q.my);
+    if (q.mx > 65535 || q.my > 65535) return fail(c, CLAW_EINVAL, "patch %d: mx, my must be < 65536", p);
+    if (q.mbc != 2) return fail(c, CLAW_EINVAL, "patch %d: mbc=%d must be 2", p, q.mbc);
+    if (!(q.rho > 0) || !(q.K > 0)) return fail(c, CLAW_EINVAL, "patch %d: rho and K must be > 0", p);
+    if (q.dx != L.dx || q.dy != L.dy) return fail(c, CLAW_EINVAL, "patch %d: dx/dy differ within level %d", p, level);
+    const double fi = (q.xlower - cfg.xlo) / L.dx, fj = (q.ylower - cfg.ylo) / L.dy;
+    L.i0[p] = std::llround(fi);
+    L.j0[p] = std::llround(fj);
+    if (std::fabs(fi - L.i0[p]) > 1e-6 || std::fabs(fj - L.j0[p]) > 1e-6)
+      return fail(c, CLAW_EINVAL, "patch %d: xlower/ylower not on the level grid", p);
+    if (L.i0[p] < 0 || L.j0[p] < 0 || L.i0[p] + q.mx > L.nx || L.j0[p] + q.my > L.ny)
+      return fail(c, CLAW_EINVAL, "patch %d: outside the domain", p);
+    cells += static_cast<int64_t>(q.mx) * q.my;
+  }
+  // bucket grid
+  L.nbx = (L.nx + kBucket - 1) / kBucket;
+  L.nby = (L.ny + kBucket - 1) / kBucket;
+  const int64_t nb = L.nbx * L.nby;
+  L.bstart.assign(nb + 1, 0);
+  for (int pass = 0; pass < 2; ++pass) {
+    std::vector<int64_t> fill;
+    if (pass == 1) {
+      for (int64_t b = 0; b < nb; ++b) L.bstart[b + 1] += L.bstart[b];
+      L.blist.assign(L.bstart[nb], 0);
+      fill.assign(L.bstart.begin(), L.bstart.end() - 1);
+    }
+    for (int p = 0; p < npatch; ++p) {
+      const int64_t bx0 = L.i0[p] / kBucket, bx1 = (L.i0[p] + d[p].mx - 1) / kBucket;
+      const int64_t by0 = L.j0[p] / kBucket, by1 = (L.j0[p] + d[p].my - 1) / kBucket;
+      for (int64_t by = by0; by <= by1; ++by)
+        for (int64_t bx = bx0; bx <= bx1; ++bx) {
+          const int64_t b = by * L.nbx + bx;
+          if (pass == 0) L.bstart[b + 1]++;
+          else L.blist[fill[b]++] = p;
+        }
+    }
+  }
+  for (int64_t b = 0; b < nb; ++b)
+    for (int64_t k = L.bstart[b]; k < L.bstart[b + 1]; ++k)
+      for (int64_t k2 = k + 1; k2 < L.bstart[b + 1]; ++k2) {
+        const int p = L.blist[k], q = L.blist[k2];
+        if (L.i0[p] < L.i0[q] + d[q].mx && L.i0[q] < L.i0[p] + d[p].mx && L.j0[p] < L.j0[q] + d[q].my &&
+            L.j0[q] < L.j0[p] + d[p].my)
+          return fail(c, CLAW_EINVAL, "patches %d and %d overlap on level %d", p, q, level);
+      }
+  if (level == 1 && cells != L.nx * L.ny) return fail(c, CLAW_EINVAL, "level 1 does not tile the domain");
+  return CLAW_OK;
+}
+
+// Compress per-cell sources of a patch's padded frame into rectangles.
+void compress_rects(const std::vector<Src>& cell, int mx, int my, std::vector<DevRect>& out) {
+  const int PX = mx + 4;
+  auto at = [&](int i, int j) -> const Src& { return cell[(j + 2) * PX + (i + 2)]; };
+  struct Run {
+    int i0, i1, j0, j1;  // [i0, i1) x [j0, j1)
+    int kind;
+    int64_t base, sx, sy, cs;
+    bool open;
+  };
+  std::vector<Run> runs;
+  std::vector<Run> prev;  // runs of the previous row that can still grow
+  for (int j = -2; j <= my + 1; ++j) {
+    std::vector<Run> row;
+    auto emit_segment = [&](int a, int b) {  // ghost cells [a, b) of row j
+      int i = a;
+      while (i < b) {
+        const Src& s = at(i, j);
+        Run r{i, i + 1, j, j + 1, s.kind, s.base, 0, 0, s.cs, true};
+        int k = i + 1;
+        if (k < b) {
+          const Src& t = at(k, j);
+          if (t.kind == s.kind && t.cs == s.cs) {
+            r.sx = t.base - s.base;
+            while (k < b) {
+              const Src& u = at(k, j);
+              if (u.kind != s.kind || u.cs != s.cs || u.base != s.base + (k - i) * r.sx) break;
+              ++k;
+            }
+          }
+        }
+        r.i1 = k;
+        row.push_back(r);
+        i = k;
+      }
+    };
+    if (j < 0 || j >= my) {
+      emit_segment(-2, mx + 2);
+    } else {
+      emit_segment(-2, 0);
+      emit_segment(mx, mx + 2);
+    }
+    // vertical merge with runs ending at row j
+    std::vector<Run> next;
+    for (Run& r : row) {
+      bool merged = false;
+      for (Run& p : prev) {
+        if (!p.open || p.i0 != r.i0 || p.i1 != r.i1 || p.kind != r.kind || p.cs != r.cs) continue;
+        if (p.i1 - p.i0 > 1 && p.sx != r.sx) continue;
+        const int64_t step = r.base - (p.base + (int64_t)(p.j1 - 1 - p.j0) * p.sy);
+        if (p.j1 - p.j0 > 1 && step != p.sy) continue;
+        // compatible: also need x steps equal when width 1 is ambiguous (both 0)
+        if (p.j1 - p.j0 == 1) p.sy = step;
+        p.j1 = j + 1;
+        next.push_back(p);
+        p.open = false;
+        merged = true;
+        break;
+      }
+      if (!merged) next.push_back(r);
+    }
+    for (Run& p : prev)
+      if (p.open) runs.push_back(p);
+    prev = next;
+    for (Run& p : prev) p.open = true;
+  }
+  for (Run& p : prev) runs.push_back(p);
+  for (const Run& r : runs) {
+    DevRect d{};
+    d.i0 = r.i0;
+    d.j0 = r.j0;
+    d.w = r.i1 - r.i0;
+    d.h = r.j1 - r.j0;
+    d.kind = r.kind;
+    d.base = r.base;
+    d.sx = r.sx;
+    d.sy = r.sy;
+    d.cs = r.cs;
+    out.push_back(d);
+  }
+}
+
+// The composite ghost rule (R1, R8-R10) for every padded
+// cell of every owned patch, the halo plan, coarse-interpolation specs, and
+// device tables.
+int plan_level(claw_ctx* c, int level, Level& L) {
+  const claw_config& cfg = c->cfg;
+  const int me = cfg.rank, world = cfg.world;
+  const int np = L.npatch;
+  L.owner.assign(np, 0);
+  partition_impl(np, L.desc.data(), L.i0, L.j0, world, L.owner.data());
+  L.local.assign(np, -1);
+  L.owned.clear();
+  L.off.clear();
+  int64_t off = 0;
+  L.gapless = true;
+  L.cells_owned = 0;
+  for (int p = 0; p < np; ++p) {
+    if (L.owner[p] != me) continue;
+    L.local[p] = static_cast<int32_t>(L.owned.size());
+    L.owned.push_back(p);
+    const int64_t n = 3ll * L.desc[p].mx * L.desc[p].my;
+    const int64_t aligned = (off + 31) / 32 * 32;  // 256-byte aligned patch start
+    if (aligned != off) L.gapless = false;
+    off = aligned;
+    L.off.push_back(off);
+    off += n;
+    L.cells_owned += n / 3;
+  }
+  L.buf_elems = off;
+
+  const Level* C = (level > 1) ? &c->lev[level - 1] : nullptr;
+  // which patches need resolving: owned ones (receive side) and, for world>1,
+  // patches of other ranks whose ghost frame may read my cells (send side)
+  std::vector<char> need(np, 0);
+  int64_t bx0 = INT64_MAX, by0 = INT64_MAX, bx1 = INT64_MIN, by1 = INT64_MIN;
+  for (int p : L.owned) {
+    need[p] = 1;
+    bx0 = std::min(bx0, L.i0[p]);
+    by0 = std::min(by0, L.j0[p]);
+    bx1 = std::max(bx1, L.i0[p] + L.desc[p].mx);
+    by1 = std::max(by1, L.j0[p] + L.desc[p].my);
+  }
+  const bool periodic = cfg.bc[0] == CLAW_BC_PERIODIC || cfg.bc[2] == CLAW_BC_PERIODIC;
+  if (world > 1)
+    for (int p = 0; p < np; ++p) {
+      if (need[p]) continue;
+      const int64_t a0 = L.i0[p] - 2, a1 = L.i0[p] + L.desc[p].mx + 2;
+      const int64_t b0 = L.j0[p] - 2, b1 = L.j0[p] + L.desc[p].my + 2;
+      bool touch = a0 < bx1 && bx0 < a1 && b0 < by1 && by0 < b1;
+      if (periodic && (a0 < 0 || b0 < 0 || a1 > L.nx || b1 > L.ny)) touch = true;
+      need[p] = touch;
+    }
+
+  L.send_off.assign(world, {});
+  L.send_cs.assign(world, {});
+  L.send_dbg.assign(world, {});
+  L.nrecv.assign(world, 0);
+  L.recv_frame_off.assign(world, 0);
+  L.hinterp.clear();
+  L.dbg_src.assign(L.owned.size(), {});
+  L.dbg_remote.assign(L.owned.size(), {});
+
+  struct Pending {  // frame cells of owned patches before slot assignment
+    int lp;         // owned index
+    int cellidx;
+    int kind;       // 1 remote, 2 coarse
+    int src_rank;
+    int64_t Ic, Jc, I, J;  // coarse spec inputs (kind 2)
+  };
+  std::vector<std::vector<Src>> cells(L.owned.size());
+  std::vector<Pending> pend;
+
+  for (int p = 0; p < np; ++p) {
+    if (!need[p]) continue;
+    const int dst_owner = L.owner[p];
+    const bool mine = dst_owner == me;
+    const int mx = L.desc[p].mx, my = L.desc[p].my, PX = mx + 4;
+    const int lp = mine ? L.local[p] : -1;
+    if (mine) {
+      cells[lp].assign(static_cast<size_t>(PX) * (my + 4), Src{-1, 0, 0});
+      L.dbg_src[lp].assign(static_cast<size_t>(PX) * (my + 4), 0);
+      L.dbg_remote[lp].assign(static_cast<size_t>(PX) * (my + 4), 0);
+    }
+    for (int j = -2; j <= my + 1; ++j)
+      for (int i = -2; i <= mx + 1; ++i) {
+        const bool interior = i >= 0 && i < mx && j >= 0 && j < my;
+        const int idx = (j + 2) * PX + (i + 2);
+        if (interior) {
+          if (mine) {
+            L.dbg_src[lp][idx] = (static_cast<int64_t>(p) << 32) | (static_cast<int64_t>(j) << 16) | i;
+            cells[lp][idx] = Src{0, L.off[lp] + static_cast<int64_t>(j) * mx + i, static_cast<int64_t>(mx) * my};
+          }
+          continue;
+        }
+        const int64_t I = map_axis(L.i0[p] + i, L.nx, cfg.bc[0], cfg.bc[1]);
+        const int64_t J = map_axis(L.j0[p] + j, L.ny, cfg.bc[2], cfg.bc[3]);
+        const int q = L.find(I, J);
+        if (q >= 0) {
+          const int li = static_cast<int>(I - L.i0[q]), lj = static_cast<int>(J - L.j0[q]);
+          const int src_owner = L.owner[q];
+          const int64_t code = (static_cast<int64_t>(q) << 32) | (static_cast<int64_t>(lj) << 16) | li;
+          if (mine) {
+            if (src_owner == me) {
+              const int lq = L.local[q];
+              cells[lp][idx] = Src{0, L.off[lq] + static_cast<int64_t>(lj) * L.desc[q].mx + li,
+                                   static_cast<int64_t>(L.desc[q].mx) * L.desc[q].my};
+              L.dbg_src[lp][idx] = code;
+            } else {
+              pend.push_back(Pending{lp, idx, 1, src_owner, 0, 0, 0, 0});
+              L.dbg_src[lp][idx] = -2;
+              L.dbg_remote[lp][idx] = code;
+            }
+          } else if (src_owner == me) {
+            // p belongs to dst_owner; I supply this cell (send list order =
+            // dst patch ascending, cell row-major: identical on both sides)
+            const int lq = L.local[q];
+            L.send_off[dst_owner].push_back(L.off[lq] + static_cast<int64_t>(lj) * L.desc[q].mx + li);
+            L.send_cs[dst_owner].push_back(static_cast<int64_t>(L.desc[q].mx) * L.desc[q].my);
+            L.send_dbg[dst_owner].push_back(code);
+          }
+          continue;
+        }
+        if (!mine) continue;
+        if (!C) return fail(c, CLAW_ENEST, "level %d patch %d: ghost cell (%d,%d) has no donor", level, p, i, j);
+        const int R = L.ratio;
+        const int64_t Ic = I / R, Jc = J / R;
+        pend.push_back(Pending{lp, idx, 2, -1, Ic, Jc, I, J});
+        L.dbg_src[lp][idx] = -1;
+      }
+  }
+
+  // frame layout: [peer 0 segment][peer 1 segment]...[coarse segment], each [3][n]
+  for (const Pending& pd : pend)
+    if (pd.kind == 1) L.nrecv[pd.src_rank]++;
+  int64_t fo = 0;
+  for (int r = 0; r < world; ++r) {
+    L.recv_frame_off[r] = fo;
+    fo += 3 * L.nrecv[r];
+  }
+  L.coarse_frame_off = fo;
+  L.ncoarse = 0;
+  for (const Pending& pd : pend)
+    if (pd.kind == 2) L.ncoarse++;
+  L.frame_elems = fo + 3 * L.ncoarse;
+  std::vector<int64_t> rk(world, 0);
+  int64_t ck = 0;
+  for (const Pending& pd : pend) {
+    if (pd.kind == 1) {
+      const int64_t k = rk[pd.src_rank]++;
+      cells[pd.lp][pd.cellidx] = Src{1, L.recv_frame_off[pd.src_rank] + k, L.nrecv[pd.src_rank]};
+    } else {
+      const int64_t k = ck++;
+      cells[pd.lp][pd.cellidx] = Src{1, L.coarse_frame_off + k, L.ncoarse};
+      // coarse donors: centre, x-, x+, y-, y+ (coarse composite via clamp/wrap)
+      DevInterp sp{};
+      const int64_t cI[5] = {pd.Ic, map_axis(pd.Ic - 1, C->nx, cfg.bc[0], cfg.bc[1]),
+                             map_axis(pd.Ic + 1, C->nx, cfg.bc[0], cfg.bc[1]), pd.Ic, pd.Ic};
+      const int64_t cJ[5] = {pd.Jc, pd.Jc, pd.Jc, map_axis(pd.Jc - 1, C->ny, cfg.bc[2], cfg.bc[3]),
+                             map_axis(pd.Jc + 1, C->ny, cfg.bc[2], cfg.bc[3])};
+      for (int d = 0; d < 5; ++d) {
+        const int q = C->find(cI[d], cJ[d]);
+        if (q < 0 || C->local[q] < 0)
+          return fail(c, CLAW_ENEST, "level %d: coarse cell (%lld,%lld) needed for interpolation is not on level %d",
+                      level, (long long)cI[d], (long long)cJ[d], level - 1);
+        const int lq = C->local[q];
+        sp.off[d] = C->off[lq] + (cJ[d] - C->j0[q]) * C->desc[q].mx + (cI[d] - C->i0[q]);
+        sp.cs[d] = static_cast<int64_t>(C->desc[q].mx) * C->desc[q].my;
+      }
+      const int R = L.ratio;
+      sp.xi = (static_cast<double>(pd.I % R) + 0.5) / static_cast<double>(R) - 0.5;
+      sp.eta = (static_cast<double>(pd.J % R) + 0.5) / static_cast<double>(R) - 0.5;
+      sp.dst = L.coarse_frame_off + k;
+      L.hinterp.push_back(sp);
+    }
+  }
+
+  // rectangles and device patch records
+  L.hpatch.clear();
+  L.hrect.clear();
+  for (size_t lp = 0; lp < L.owned.size(); ++lp) {
+    const int p = L.owned[lp];
+    DevPatch d{};
+    d.off = L.off[lp];
+    d.cs = static_cast<int64_t>(L.desc[p].mx) * L.desc[p].my;
+    d.mx = L.desc[p].mx;
+    d.my = L.desc[p].my;
+    d.rect_begin = static_cast<int32_t>(L.hrect.size());
+    compress_rects(cells[lp], d.mx, d.my, L.hrect);
+    d.rect_end = static_cast<int32_t>(L.hrect.size());
+    // regions: strips W (i in [-2,0), j in [0,my)), E, S, N and 2x2 corners
+    // SW, SE, NW, NE, each covered by one rectangle (or -1)
+    const int X0 = -2, X1 = 0, X2 = d.mx, X3 = d.mx + 2, Y0 = -2, Y1 = 0, Y2 = d.my, Y3 = d.my + 2;
+    const int sb[8][4] = {{X0, X1, Y1, Y2}, {X2, X3, Y1, Y2}, {X1, X2, Y0, Y1}, {X1, X2, Y2, Y3},
+                          {X0, X1, Y0, Y1}, {X2, X3, Y0, Y1}, {X0, X1, Y2, Y3}, {X2, X3, Y2, Y3}};
+    for (int e = 0; e < 8; ++e) {
+      d.region[e] = -1;
+      for (int k = d.rect_begin; k < d.rect_end; ++k) {
+        const DevRect& r = L.hrect[k];
+        if (r.i0 <= sb[e][0] && r.i0 + r.w >= sb[e][1] && r.j0 <= sb[e][2] && r.j0 + r.h >= sb[e][3]) {
+          d.region[e] = k;
+          break;
+        }
+      }
+    }
+    d.dx = L.desc[p].dx;
+    d.dy = L.desc[p].dy;
+    d.c = std::sqrt(L.desc[p].K / L.desc[p].rho);
+    d.Z = L.desc[p].rho * d.c;
+    L.hpatch.push_back(d);
+  }
+  // tiles: strips of <= 32 columns x <= tile_rows rows, largest first
+  L.uniform = true;
+  for (size_t lp = 1; lp < L.hpatch.size(); ++lp)
+    if (L.hpatch[lp].c != L.hpatch[0].c || L.hpatch[lp].Z != L.hpatch[0].Z) L.uniform = false;
+  L.htile.clear();
+  for (size_t lp = 0; lp < L.owned.size(); ++lp) {
+    const int mx = L.hpatch[lp].mx, my = L.hpatch[lp].my;
+    for (int j0 = 0; j0 < my; j0 += c->tile_rows)
+      for (int i0 = 0; i0 < mx; i0 += 32) {
+        const int tw = std::min(32, mx - i0), th = std::min(c->tile_rows, my - j0);
+        L.htile.push_back(make_int4(static_cast<int>(lp), i0, j0, tw | (th << 16)));
+      }
+  }
+  std::stable_sort(L.htile.begin(), L.htile.end(), [](const int4& a, const int4& b) {
+    return (a.w & 0xffff) * (a.w >> 16) > (b.w & 0xffff) * (b.w >> 16);
+  });
+  return CLAW_OK;
+}
+
+// Host twin of the kernel's make_consts (same operations, same order; x86-64
+// without FMA contraction, so every result is the same IEEE double).
+void fill_step_consts(const DevPatch& pt, double dt, double LS, int ot, claw::StepConsts& k) {
+  volatile double c = pt.c, Z = pt.Z;  // volatile: keep each operation separately rounded
+  k.Z = Z;
+  k.r = dt / pt.dx;
+  k.s = dt / pt.dy;
+  k.h = 0.5 * c;
+  k.hz = k.h / Z;
+  volatile double cr = c * k.r, cs = c * k.s;
+  volatile double omx = 1.0 - cr, omy = 1.0 - cs;
+  const double kx = c * omx, ky = c * omy;
+  k.kx4 = kx / (4.0 * LS);
+  k.ky4 = ky / (4.0 * LS);
+  k.kx2 = (ot == 2) ? kx / (2.0 * LS) : 0.0;
+  k.ky2 = (ot == 2) ? ky / (2.0 * LS) : 0.0;
+  k.kx4z = k.kx4 / Z;
+  k.ky4z = k.ky4 / Z;
+  volatile double rs = k.r * k.s;
+  volatile double rsc = rs * c;
+  k.T = (ot != 0) ? 0.25 * rsc : 0.0;
+  k.TZ = (ot != 0) ? k.T / Z : 0.0;
+  const double a = k.r * c, b = k.s * c;
+  k.cfl = a > b ? a : b;
+}
+
+template <class T>
+int upload(claw_ctx* ctx, DevBuf<T>& b, const std::vector<T>& v) {
+  CUDA_TRY(b.alloc(v.size()));
+  if (!v.empty()) CUDA_TRY(cudaMemcpy(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return CLAW_OK;
+}
+
+int check_ctx(claw_ctx* c) {
+  if (!c) return CLAW_EINVAL;
+  if (c->dead) return fail(c, CLAW_ECUDA, "context unusable after an earlier CUDA/NCCL error");
+  return CLAW_OK;
+}
+
+int check_level(claw_ctx* c, int level) {
+  if (level < 1 || level > kMaxLevel || !c->lev[level].set)
+    return fail(c, CLAW_ESTATE, "level %d is not set", level);
+  return CLAW_OK;
+}
+
+void record(claw_ctx* c, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v, bool start) {
+  if (!c->profiling) return;
+  if (start) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    v.emplace_back(a, b);
+    cudaEventRecord(a, c->stream);
+  } else {
+    cudaEventRecord(v.back().second, c->stream);
+  }
+}
+
+double drain(std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
+  double ms = 0;
+  for (auto& e : v) {
+    float t = 0;
+    cudaEventSynchronize(e.second);
+    cudaEventElapsedTime(&t, e.first, e.second);
+    ms += t;
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  v.clear();
+  return ms;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* claw_version(void) { return "libclaw 0.1 (sm_100a, fp64, acoustics 2D)"; }
+
+int claw_partition(int32_t npatch, const claw_patch_desc* d, int32_t world, int32_t* owner) {
+  if (npatch < 1 || !d || !owner || world < 1) return CLAW_EINVAL;
+  // integer boxes relative to the minimum corner (no domain needed)
+  double xmin = d[0].xlower, ymin = d[0].ylower;
+  for (int p = 1; p < npatch; ++p) {
+    xmin = std::min(xmin, d[p].xlower);
+    ymin = std::min(ymin, d[p].ylower);
+  }
+  std::vector<int64_t> i0(npatch), j0(npatch);
+  for (int p = 0; p < npatch; ++p) {
+    if (!(d[p].dx > 0) || !(d[p].dy > 0)) return CLAW_EINVAL;
+    i0[p] = std::llround((d[p].xlower - xmin) / d[p].dx);
+    j0[p] = std::llround((d[p].ylower - ymin) / d[p].dy);
+  }
+  partition_impl(npatch, d, i0, j0, world, owner);
+  return CLAW_OK;
+}
+
+int claw_create(const claw_config* cfg, claw_ctx** out) {
+  if (!cfg || !out) return CLAW_EINVAL;
+  *out = nullptr;
+  auto* ctx = new claw_ctx();
+  ctx->cfg = *cfg;
+  int rc = validate_config(ctx, cfg);
+  if (rc) {
+    // keep the context so the caller can read the message
+    *out = ctx;
+    ctx->dead = true;
+    return rc;
+  }
+  ctx->tile_rows = cfg->tile_rows > 0 ? cfg->tile_rows : claw::max_tile_rows();
+  ctx->host_only = cfg->device < 0;
+  *out = ctx;
+  if (ctx->host_only) return CLAW_OK;
+  CUDA_TRY(cudaSetDevice(cfg->device));
+  if (cfg->stream) {
+    ctx->stream = static_cast<cudaStream_t>(cfg->stream);
+  } else {
+    CUDA_TRY(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    ctx->own_stream = true;
+  }
+  CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_cfl), sizeof(double)));
+  if (cfg->world > 1) {
+    if (!g_nccl.load(ctx->err)) {
+      ctx->dead = true;
+      return CLAW_ENCCL;
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, cfg->nccl_unique_id, sizeof id);
+    ncclResult_t r = g_nccl.CommInitRank(&ctx->comm, cfg->world, id, cfg->rank);
+    if (r != ncclSuccess) return nccl_fail(ctx, r, "ncclCommInitRank");
+  }
+  return CLAW_OK;
+}
+
+int claw_nccl_unique_id(void* out128) {
+  std::string err;
+  if (!out128 || !g_nccl.load(err)) return CLAW_ENCCL;
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != ncclSuccess) return CLAW_ENCCL;
+  std::memcpy(out128, &id, sizeof id);
+  return CLAW_OK;
+}
+
+int claw_destroy(claw_ctx* ctx) {
+  if (!ctx) return CLAW_EINVAL;
+  if (!ctx->host_only && !ctx->dead) cudaStreamSynchronize(ctx->stream);
+  drain(ctx->ev_step);
+  drain(ctx->ev_ghost);
+  for (auto& L : ctx->lev) L = Level();
+  if (ctx->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(ctx->comm);
+  if (ctx->h_cfl) cudaFreeHost(ctx->h_cfl);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return CLAW_OK;
+}
+
+const char* claw_last_error(const claw_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int claw_set_level(claw_ctx* ctx, int32_t level, int32_t npatch, const claw_patch_desc* descs,
+                   const double* q0) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (level < 1 || level > kMaxLevel) return fail(ctx, CLAW_EINVAL, "level=%d: must be 1..%d", level, kMaxLevel);
+  if (npatch < 1 || !descs) return fail(ctx, CLAW_EINVAL, "npatch=%d: need >= 1 patch descriptors", npatch);
+  if (level > 1 && !ctx->lev[level - 1].set) return fail(ctx, CLAW_ESTATE, "level %d set before level %d", level, level - 1);
+  if (level > 1 && ctx->cfg.world > 1)
+    return fail(ctx, CLAW_EINVAL, "multi-level hierarchies are single-rank in this version (world=%d)", ctx->cfg.world);
+  if (!ctx->host_only) CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  for (int l = level; l <= kMaxLevel; ++l) ctx->lev[l] = Level();
+  Level& L = ctx->lev[level];
+  int rc = build_geometry(ctx, level, npatch, descs, L);
+  if (!rc) rc = plan_level(ctx, level, L);
+  if (rc) {
+    L = Level();
+    return rc;
+  }
+  L.t_old = L.t_new = (level > 1) ? ctx->lev[level - 1].t_old : 0.0;
+  if (ctx->host_only) {
+    L.set = true;
+    return CLAW_OK;
+  }
+  // device pool: two ping-pong buffers + frame + tables (allocated once; no
+  // per-step allocation, cf. the paper's memory pool P:422-426)
+  for (int b = 0; b < 2; ++b) {
+    cudaError_t e = L.q[b].alloc(std::max<int64_t>(L.buf_elems, 1));
+    if (e != cudaSuccess) {
+      L = Level();
+      cudaGetLastError();
+      return fail(ctx, CLAW_ENOMEM, "level %d: cannot allocate %lld bytes of device pool", level,
+                  (long long)(2 * L.buf_elems * 8));
+    }
+  }
+  CUDA_TRY(L.frame.alloc(std::max<int64_t>(L.frame_elems, 1)));
+  if (int r2 = upload(ctx, L.dpatch, L.hpatch)) return r2;
+  if (int r2 = upload(ctx, L.drect, L.hrect)) return r2;
+  if (int r2 = upload(ctx, L.dtile, L.htile)) return r2;
+  if (int r2 = upload(ctx, L.dinterp, L.hinterp)) return r2;
+  CUDA_TRY(L.pcfl.alloc(std::max<size_t>(L.owned.size(), 1)));
+  CUDA_TRY(L.lcfl.alloc(1));
+  CUDA_TRY(cudaMemset(L.pcfl.p, 0, L.pcfl.n * 8));
+  CUDA_TRY(cudaMemset(L.lcfl.p, 0, 8));
+  const int world = ctx->cfg.world;
+  L.dsend_off.clear();
+  L.dsend_cs.clear();
+  L.dsend_buf.clear();
+  for (int r = 0; r < world; ++r) {
+    L.dsend_off.emplace_back(new DevBuf<int64_t>());
+    L.dsend_cs.emplace_back(new DevBuf<int64_t>());
+    L.dsend_buf.emplace_back(new DevBuf<double>());
+    if (int r2 = upload(ctx, *L.dsend_off[r], L.send_off[r])) return r2;
+    if (int r2 = upload(ctx, *L.dsend_cs[r], L.send_cs[r])) return r2;
+    CUDA_TRY(L.dsend_buf[r]->alloc(3 * L.send_off[r].size()));
+  }
+  L.device_bytes = 2 * L.buf_elems * 8 + L.frame_elems * 8 +
+                   static_cast<int64_t>(L.hpatch.size() * sizeof(DevPatch) + L.hrect.size() * sizeof(DevRect) +
+                                        L.htile.size() * sizeof(int4) + L.hinterp.size() * sizeof(DevInterp));
+  L.cur = 0;
+  if (q0) {
+    if (L.gapless) {
+      CUDA_TRY(cudaMemcpy(L.q[0].p, q0, L.buf_elems * 8, cudaMemcpyHostToDevice));
+    } else {
+      int64_t src = 0;
+      for (size_t lp = 0; lp < L.owned.size(); ++lp) {
+        const int64_t n = 3ll * L.hpatch[lp].mx * L.hpatch[lp].my;
+        CUDA_TRY(cudaMemcpy(L.q[0].p + L.off[lp], q0 + src, n * 8, cudaMemcpyHostToDevice));
+        src += n;
+      }
+    }
+  } else {
+    CUDA_TRY(cudaMemset(L.q[0].p, 0, L.buf_elems * 8));
+  }
+  CUDA_TRY(cudaMemcpy(L.q[1].p, L.q[0].p, L.buf_elems * 8, cudaMemcpyDeviceToDevice));
+  CUDA_TRY(cudaMemset(L.frame.p, 0, L.frame.n * 8));
+  L.set = true;
+  return CLAW_OK;
+}
+
+int claw_fill_ghost(claw_ctx* ctx, int32_t level, double t) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = check_level(ctx, level)) return rc;
+  if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
+  Level& L = ctx->lev[level];
+  record(ctx, ctx->ev_ghost, true);
+  if (level > 1 && L.ncoarse > 0) {
+    const Level& C = ctx->lev[level - 1];
+    const double span = C.t_new - C.t_old;
+    const double tol = 1e-12 * std::max(1.0, std::fabs(C.t_new));
+    if (t < C.t_old - tol || t > C.t_new + tol)
+      return fail(ctx, CLAW_ESTATE, "fill_ghost(level %d, t=%.17g): outside level %d's [%.17g, %.17g]", level, t,
+                  level - 1, C.t_old, C.t_new);
+    const double alpha = (span > 0) ? (t - C.t_old) / span : 0.0;
+    // C.q[C.cur] holds t_new, the other buffer t_old
+    // DevInterp.dst is an absolute frame offset; components are ncoarse apart
+    CUDA_TRY(static_cast<cudaError_t>(claw::launch_interp(C.q[1 - C.cur].p, C.q[C.cur].p, alpha, L.dinterp.p,
+                                                          L.ncoarse, L.frame.p, L.ncoarse, ctx->stream)));
+    ctx->stats.ghost_launches++;
+  }
+  if (ctx->cfg.world > 1) {
+    const int world = ctx->cfg.world;
+    for (int r = 0; r < world; ++r) {
+      const int64_t n = static_cast<int64_t>(L.send_off[r].size());
+      if (n == 0) continue;
+      CUDA_TRY(static_cast<cudaError_t>(claw::launch_pack(L.q[L.cur].p, L.dsend_off[r]->p, L.dsend_cs[r]->p, n,
+                                                          L.dsend_buf[r]->p, ctx->stream)));
+      ctx->stats.ghost_launches++;
+    }
+    ncclResult_t nr = g_nccl.GroupStart();
+    if (nr != ncclSuccess) return nccl_fail(ctx, nr, "ncclGroupStart");
+    for (int r = 0; r < world; ++r) {
+      const size_t ns = L.send_off[r].size();
+      if (ns) {
+        nr = g_nccl.Send(L.dsend_buf[r]->p, 3 * ns, ncclFloat64, r, ctx->comm, ctx->stream);
+        if (nr != ncclSuccess) return nccl_fail(ctx, nr, "ncclSend");
+        ctx->stats.halo_bytes_sent += static_cast<int64_t>(24 * ns);
+      }
+      if (L.nrecv[r]) {
+        nr = g_nccl.Recv(L.frame.p + L.recv_frame_off[r], 3 * L.nrecv[r], ncclFloat64, r, ctx->comm, ctx->stream);
+        if (nr != ncclSuccess) return nccl_fail(ctx, nr, "ncclRecv");
+      }
+    }
+    nr = g_nccl.GroupEnd();
+    if (nr != ncclSuccess) return nccl_fail(ctx, nr, "ncclGroupEnd");
+  }
+  record(ctx, ctx->ev_ghost, false);
+  return CLAW_OK;
+}
+
+int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = check_level(ctx, level)) return rc;
+  if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
+  if (!(dt >= 0) || !std::isfinite(dt)) return fail(ctx, CLAW_EINVAL, "dt=%g: must be finite and >= 0", dt);
+  Level& L = ctx->lev[level];
+  CUDA_TRY(cudaMemsetAsync(L.pcfl.p, 0, L.pcfl.n * 8, ctx->stream));
+  CUDA_TRY(cudaMemsetAsync(L.lcfl.p, 0, 8, ctx->stream));
+  claw::StepParams P{};
+  P.q = L.q[L.cur].p;
+  P.qn = L.q[1 - L.cur].p;
+  P.frame = L.frame.p;
+  P.patches = L.dpatch.p;
+  P.rects = L.drect.p;
+  P.tiles = L.dtile.p;
+  P.ntiles = static_cast<int32_t>(L.htile.size());
+  P.limiter = ctx->cfg.limiter;
+  P.order_trans = ctx->cfg.order_trans;
+  P.dt = dt;
+  P.patch_cfl = L.pcfl.p;
+  P.level_cfl = L.lcfl.p;
+  P.uniform = (L.uniform && !L.hpatch.empty()) ? 1 : 0;
+  if (P.uniform) fill_step_consts(L.hpatch[0], dt, ctx->cfg.limiter == 4 ? 2.0 : 1.0, ctx->cfg.order_trans, P.k);
+  record(ctx, ctx->ev_step, true);
+  CUDA_TRY(static_cast<cudaError_t>(claw::launch_step(P, ctx->stream)));
+  record(ctx, ctx->ev_step, false);
+  ctx->stats.step_launches++;
+  ctx->stats.cells_advanced += L.cells_owned;
+  if (ctx->cfg.world > 1) {
+    ncclResult_t nr = g_nccl.AllReduce(L.lcfl.p, L.lcfl.p, 1, ncclFloat64, ncclMax, ctx->comm, ctx->stream);
+    if (nr != ncclSuccess) return nccl_fail(ctx, nr, "ncclAllReduce(cfl, max)");
+  }
+  L.cur = 1 - L.cur;
+  L.t_old = L.t_new;
+  L.t_new = L.t_new + dt;
+  return CLAW_OK;
+}
+
+int claw_wait_cfl(claw_ctx* ctx, int32_t level, double* cfl_max) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = check_level(ctx, level)) return rc;
+  if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
+  if (!cfl_max) return fail(ctx, CLAW_EINVAL, "cfl_max is NULL");
+  Level& L = ctx->lev[level];
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_cfl, L.lcfl.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  *cfl_max = *ctx->h_cfl;
+  return CLAW_OK;
+}
+
+int claw_advance_level(claw_ctx* ctx, int32_t level, double dt, double* cfl_max) {
+  if (!cfl_max) return fail(ctx, CLAW_EINVAL, "cfl_max is NULL");
+  if (int rc = claw_advance_level_async(ctx, level, dt)) return rc;
+  return claw_wait_cfl(ctx, level, cfl_max);
+}
+
+static int owned_index(claw_ctx* ctx, int level, int patch, int* lp) {
+  if (int rc = check_level(ctx, level)) return rc;
+  const Level& L = ctx->lev[level];
+  if (patch < 0 || patch >= L.npatch) return fail(ctx, CLAW_EINVAL, "patch %d out of range", patch);
+  if (L.local[patch] < 0) return fail(ctx, CLAW_EINVAL, "patch %d is owned by rank %d", patch, L.owner[patch]);
+  *lp = L.local[patch];
+  return CLAW_OK;
+}
+
+int claw_read(claw_ctx* ctx, int32_t level, int32_t patch, double* q_out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
+  int lp;
+  if (int rc = owned_index(ctx, level, patch, &lp)) return rc;
+  if (!q_out) return fail(ctx, CLAW_EINVAL, "q_out is NULL");
+  Level& L = ctx->lev[level];
+  const int64_t n = 3ll * L.hpatch[lp].mx * L.hpatch[lp].my;
+  CUDA_TRY(cudaMemcpyAsync(q_out, L.q[L.cur].p + L.off[lp], n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return CLAW_OK;
+}
+
+int claw_write(claw_ctx* ctx, int32_t level, int32_t patch, const double* q_in) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
+  int lp;
+  if (int rc = owned_index(ctx, level, patch, &lp)) return rc;
+  if (!q_in) return fail(ctx, CLAW_EINVAL, "q_in is NULL");
+  Level& L = ctx->lev[level];
+  const int64_t n = 3ll * L.hpatch[lp].mx * L.hpatch[lp].my;
+  CUDA_TRY(cudaMemcpyAsync(L.q[L.cur].p + L.off[lp], q_in, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return CLAW_OK;
+}
+
+int claw_read_level(claw_ctx* ctx, int32_t level, double* q_out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = check_level(ctx, level)) return rc;
+  if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
+  if (!q_out) return fail(ctx, CLAW_EINVAL, "q_out is NULL");
+  Level& L = ctx->lev[level];
+  if (L.gapless) {
+    CUDA_TRY(cudaMemcpyAsync(q_out, L.q[L.cur].p, L.buf_elems * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  } else {
+    int64_t dst = 0;
+    for (size_t lp = 0; lp < L.owned.size(); ++lp) {
+      const int64_t n = 3ll * L.hpatch[lp].mx * L.hpatch[lp].my;
+      CUDA_TRY(cudaMemcpyAsync(q_out + dst, L.q[L.cur].p + L.off[lp], n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+      dst += n;
+    }
+  }
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return CLAW_OK;
+}
+
+int claw_write_level(claw_ctx* ctx, int32_t level, const double* q_in) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = check_level(ctx, level)) return rc;
+  if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
+  if (!q_in) return fail(ctx, CLAW_EINVAL, "q_in is NULL");
+  Level& L = ctx->lev[level];
+  if (L.gapless) {
+    CUDA_TRY(cudaMemcpyAsync(L.q[L.cur].p, q_in, L.buf_elems * 8, cudaMemcpyHostToDevice, ctx->stream));
+  } else {
+    int64_t src = 0;
+    for (size_t lp = 0; lp < L.owned.size(); ++lp) {
+      const int64_t n = 3ll * L.hpatch[lp].mx * L.hpatch[lp].my;
+      CUDA_TRY(cudaMemcpyAsync(L.q[L.cur].p + L.off[lp], q_in + src, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+      src += n;
+    }
+  }
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return CLAW_OK;
+}
+
+int claw_read_padded(claw_ctx* ctx, int32_t level, int32_t patch, double* q_out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
+  int lp;
+  if (int rc = owned_index(ctx, level, patch, &lp)) return rc;
+  if (!q_out) return fail(ctx, CLAW_EINVAL, "q_out is NULL");
+  Level& L = ctx->lev[level];
+  const int64_t n = 3ll * (L.hpatch[lp].mx + 4) * (L.hpatch[lp].my + 4);
+  DevBuf<double> tmp;
+  CUDA_TRY(tmp.alloc(n));
+  CUDA_TRY(static_cast<cudaError_t>(claw::launch_gather_padded(L.q[L.cur].p, L.frame.p, L.dpatch.p, L.drect.p, lp,
+                                                               tmp.p, ctx->stream)));
+  CUDA_TRY(cudaMemcpyAsync(q_out, tmp.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return CLAW_OK;
+}
+
+int claw_patch_cfl(claw_ctx* ctx, int32_t level, int32_t patch, double* cfl) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
+  int lp;
+  if (int rc = owned_index(ctx, level, patch, &lp)) return rc;
+  if (!cfl) return fail(ctx, CLAW_EINVAL, "cfl is NULL");
+  unsigned long long bits = 0;
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_cfl, ctx->lev[level].pcfl.p + lp, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(&bits, ctx->h_cfl, 8);
+  std::memcpy(cfl, &bits, 8);
+  return CLAW_OK;
+}
+
+int claw_owner(const claw_ctx* ctx, int32_t level, int32_t patch, int32_t* rank) {
+  if (!ctx || !rank || level < 1 || level > kMaxLevel || !ctx->lev[level].set) return CLAW_EINVAL;
+  const Level& L = ctx->lev[level];
+  if (patch < 0 || patch >= L.npatch) return CLAW_EINVAL;
+  *rank = L.owner[patch];
+  return CLAW_OK;
+}
+
+int claw_level_owned(const claw_ctx* ctx, int32_t level, int32_t* npatch_owned, int64_t* cells_owned,
+                     int64_t* device_bytes) {
+  if (!ctx || level < 1 || level > kMaxLevel || !ctx->lev[level].set) return CLAW_EINVAL;
+  const Level& L = ctx->lev[level];
+  if (npatch_owned) *npatch_owned = static_cast<int32_t>(L.owned.size());
+  if (cells_owned) *cells_owned = L.cells_owned;
+  if (device_bytes) *device_bytes = L.device_bytes;
+  return CLAW_OK;
+}
+
+int claw_debug_ghost_sources(const claw_ctx* ctx, int32_t level, int32_t patch, int64_t* out, int64_t* out2) {
+  if (!ctx || !out || level < 1 || level > kMaxLevel || !ctx->lev[level].set) return CLAW_EINVAL;
+  const Level& L = ctx->lev[level];
+  if (patch < 0 || patch >= L.npatch || L.local[patch] < 0) return CLAW_EINVAL;
+  const auto& v = L.dbg_src[L.local[patch]];
+  std::memcpy(out, v.data(), v.size() * sizeof(int64_t));
+  if (out2) {
+    const auto& w = L.dbg_remote[L.local[patch]];
+    std::memcpy(out2, w.data(), w.size() * sizeof(int64_t));
+  }
+  return CLAW_OK;
+}
+
+int claw_debug_halo_counts(const claw_ctx* ctx, int32_t level, int32_t peer, int64_t* nsend, int64_t* nrecv) {
+  if (!ctx || level < 1 || level > kMaxLevel || !ctx->lev[level].set) return CLAW_EINVAL;
+  const Level& L = ctx->lev[level];
+  if (peer < 0 || peer >= ctx->cfg.world) return CLAW_EINVAL;
+  if (nsend) *nsend = static_cast<int64_t>(L.send_off[peer].size());
+  if (nrecv) *nrecv = L.nrecv[peer];
+  return CLAW_OK;
+}
+
+int claw_debug_halo_send(const claw_ctx* ctx, int32_t level, int32_t peer, int64_t k, int32_t* patch, int32_t* i,
+                         int32_t* j) {
+  if (!ctx || level < 1 || level > kMaxLevel || !ctx->lev[level].set) return CLAW_EINVAL;
+  const Level& L = ctx->lev[level];
+  if (peer < 0 || peer >= ctx->cfg.world || k < 0 || k >= static_cast<int64_t>(L.send_dbg[peer].size()))
+    return CLAW_EINVAL;
+  const int64_t code = L.send_dbg[peer][k];
+  if (patch) *patch = static_cast<int32_t>(code >> 32);
+  if (j) *j = static_cast<int32_t>((code >> 16) & 0xffff);
+  if (i) *i = static_cast<int32_t>(code & 0xffff);
+  return CLAW_OK;
+}
+
+int claw_set_profiling(claw_ctx* ctx, int32_t on) {
+  if (int rc = check_ctx(ctx)) return rc;
+  ctx->profiling = on != 0;
+  return CLAW_OK;
+}
+
+int claw_get_stats(claw_ctx* ctx, claw_stats* out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (!out) return CLAW_EINVAL;
+  ctx->stats.step_ms += drain(ctx->ev_step);
+  ctx->stats.ghost_ms += drain(ctx->ev_ghost);
+  *out = ctx->stats;
+  return CLAW_OK;
+}
+
+int claw_reset_stats(claw_ctx* ctx) {
+  if (int rc = check_ctx(ctx)) return rc;
+  drain(ctx->ev_step);
+  drain(ctx->ev_ghost);
+  ctx->stats = claw_stats{};
+  return CLAW_OK;
+}
+
+int claw_synchronize(claw_ctx* ctx) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (ctx->host_only) return CLAW_OK;
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return CLAW_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,94 @@
+// claw_internal.h -- device-table layouts shared by the host planner
+// (claw_host.cpp) and the sm_100a kernels (claw_kernels.cu).  Not part of the
+// public ABI (include/claw.h).
+#pragma once
+#include <cstdint>
+
+namespace claw {
+
+// One owned patch of a level.  The level buffer stores owned patches back to
+// back as [3][my][mx] fp64 (components p, u, v; x fastest), each patch's
+// component planes starting on a 256-byte boundary when mx*my allows.
+struct DevPatch {
+  int64_t off;        // element offset of (m=0, j=0, i=0) in the level buffer
+  int64_t cs;         // component stride (elements)
+  int32_t mx, my;
+  int32_t rect_begin; // ghost-source rectangles [rect_begin, rect_end)
+  int32_t rect_end;
+  int32_t region[8];  // rectangle covering the whole W, E, S, N ghost strip or
+                      // SW, SE, NW, NE 2x2 corner block, or -1 (search the list)
+  double dx, dy;
+  double c, Z;        // sound speed sqrt(K/rho), impedance rho*c
+};
+static_assert(sizeof(DevPatch) == 96, "DevPatch layout");
+
+// Ghost-source rectangle: patch-local cells (i, j) with i0 <= i < i0+w,
+// j0 <= j < j0+h (0-based, ghosts are -2..-1 and mx..mx+1) take their value
+// from  buffer[base + (i-i0)*sx + (j-j0)*sy + m*cs].
+//   kind 0: the level's current ping-pong buffer (same-level donor interior,
+//           physical BC mapped onto an interior cell);
+//   kind 1: the level's frame buffer (coarse-interpolated or remote cells).
+struct DevRect {
+  int32_t i0, j0, w, h;
+  int32_t kind, pad;
+  int64_t base, sx, sy, cs;
+};
+static_assert(sizeof(DevRect) == 56, "DevRect layout");
+
+// Work unit of the fused step kernel: a strip of <= 32 columns of one patch
+// (tile columns [i0, i0+tw), rows [j0, j0+th)); packed as int4 {patch, i0, j0,
+// tw | th << 16}.
+
+// Coarse-interpolation spec for one frame slot (P:131 case 3; R10):
+// 5 coarse donors (centre, x-, x+, y-, y+) given as element offsets of their
+// p component in the coarse level buffer and component strides.
+struct DevInterp {
+  int64_t off[5];
+  int64_t cs[5];
+  double xi, eta;     // fine-cell offset inside the coarse cell, in coarse cells
+  int64_t dst;        // frame slot (p component); components at dst + m*fcs
+};
+
+// Per-patch step constants (dt, dx, dy, c, Z and the limiter scale LS folded
+// in).  For a level whose patches share one medium they are computed once on
+// the host and passed as kernel parameters (no registers); otherwise every
+// tile derives them on the device with the same operation order.
+struct StepConsts {
+  double Z, h, hz;        // Z, c/2, c/(2Z)
+  double r, s;            // dt/dx, dt/dy
+  double kx4, kx2, kx4z;  // kx/(4 LS), kx/(2 LS) (order_trans 2 else 0), kx/(4 LS Z); kx = c(1 - c r)
+  double ky4, ky2, ky4z;
+  double T, TZ;           // r s c / 4, r s c / (4 Z)   (0 when order_trans = 0)
+  double cfl;             // max(c dt/dx, c dt/dy)
+};
+
+struct StepParams {
+  const double* q;        // current buffer (read)
+  double* qn;             // next buffer (write)
+  const double* frame;    // frame buffer
+  const DevPatch* patches;
+  const DevRect* rects;
+  const int4* tiles;
+  int32_t ntiles;
+  int32_t limiter, order_trans;
+  int32_t pad;
+  double dt;
+  unsigned long long* patch_cfl;  // per owned patch, bits of a non-negative double
+  unsigned long long* level_cfl;  // 1 slot
+  int32_t uniform;                // 1: every patch uses `k` below
+  int32_t pad2;
+  StepConsts k;
+};
+
+// Launchers (claw_kernels.cu).  All return cudaError_t as int.
+int launch_step(const StepParams& p, void* stream);
+int launch_interp(const double* q_old, const double* q_new, double alpha,
+                  const DevInterp* spec, int64_t n, double* frame, int64_t fcs,
+                  void* stream);
+int launch_pack(const double* q, const int64_t* off, const int64_t* cs, int64_t n,
+                double* out, void* stream);
+int launch_gather_padded(const double* q, const double* frame, const DevPatch* patches,
+                         const DevRect* rects, int32_t patch, double* out, void* stream);
+int max_tile_rows();
+
+}  // namespace claw

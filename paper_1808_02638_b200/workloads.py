@@ -185,3 +185,124 @@ def ragged_level(seed: int, nx: int = 40, ny: int = 36, max_w: int = 13) -> np.n
     for k, (i0, j0, w, h) in enumerate(boxes):
         d[k] = make_descs([i0], [j0], w, h, dx, dy)[0]
     return d
+
+
+# ---------------------------------------------------------------------------
+# Multi-level fixed hierarchies (configs[1], configs[2]); SURVEY 8(d)
+# ---------------------------------------------------------------------------
+
+def _annulus_test(x0, x1, y0, y1, w, r0=0.5):
+    """(misses, fully_inside) of the box against |r - r0| <= w."""
+    # exact min/max distance from the origin over the box
+    dxmin = 0.0 if x0 <= 0.0 <= x1 else min(abs(x0), abs(x1))
+    dymin = 0.0 if y0 <= 0.0 <= y1 else min(abs(y0), abs(y1))
+    rmin = math.hypot(dxmin, dymin)
+    rmax = math.hypot(max(abs(x0), abs(x1)), max(abs(y0), abs(y1)))
+    misses = not (rmin <= r0 + w and rmax >= r0 - w)
+    inside = rmin >= r0 - w and rmax <= r0 + w
+    return misses, inside
+
+
+def _cover_map(nx, ny, boxes):
+    m = np.zeros((ny, nx), dtype=bool)
+    for i0, j0, w, h in boxes:
+        m[j0:j0 + h, i0:i0 + w] = True
+    return m
+
+
+def _nest_ok(box, fine_cover, coarse_cover, R):
+    """Every ghost cell of `box` is covered on its own level or has its coarse
+    parent's 5-point cross covered on the coarser level (clamped indices)."""
+    i0, j0, w, h = box
+    ny, nx = fine_cover.shape
+    cny, cnx = coarse_cover.shape
+    for j in range(j0 - 2, j0 + h + 2):
+        for i in range(i0 - 2, i0 + w + 2):
+            if i0 <= i < i0 + w and j0 <= j < j0 + h:
+                continue
+            I, J = min(max(i, 0), nx - 1), min(max(j, 0), ny - 1)
+            if fine_cover[J, I]:
+                continue
+            Ic, Jc = I // R, J // R
+            for a, b in ((0, 0), (-1, 0), (1, 0), (0, -1), (0, 1)):
+                ci, cj = min(max(Ic + a, 0), cnx - 1), min(max(Jc + b, 0), cny - 1)
+                if not coarse_cover[cj, ci]:
+                    return False
+    return True
+
+
+def _descs_from_boxes(boxes, dx, dy, domain=DOMAIN):
+    return np.concatenate([make_descs([a], [b], w, h, dx, dy, domain) for a, b, w, h in boxes])
+
+
+def c2() -> Workload:
+    """configs[1]: 2 levels, R = 4; L1 128^2 as 2x2 patches of 64^2; L2 a
+    quadtree of 16..64-wide blocks following the ring in the first quadrant."""
+    l1 = uniform_level(2, 2, 64, 64)
+    R = 4
+    nf = 128 * R
+    dxf = 2.0 / nf
+    w = 0.25
+    boxes = []
+
+    def rec(i0, j0, s):
+        x0, x1 = -1 + i0 * dxf, -1 + (i0 + s) * dxf
+        y0, y1 = -1 + j0 * dxf, -1 + (j0 + s) * dxf
+        miss, inside = _annulus_test(x0, x1, y0, y1, w)
+        if miss:
+            return
+        if inside or s == 16:
+            boxes.append((i0, j0, s, s))
+            return
+        h = s // 2
+        for dj in (0, h):
+            for di in (0, h):
+                rec(i0 + di, j0 + dj, h)
+
+    for bj in range(nf // 2, nf, 64):
+        for bi in range(nf // 2, nf, 64):
+            rec(bi, bj, 64)
+    l2 = _descs_from_boxes(boxes, dxf, dxf)
+    return Workload("c2_2level_r4", [Level(l1), Level(l2, ratio=R)], steps=200,
+                    note=f"2 levels R=4: 4 + {len(boxes)} patches (16..64 wide)")
+
+
+def c3(w2: float = 0.45, w3: float = 0.40) -> Workload:
+    """configs[2]: 3 levels R = (2, 4); L1 200^2 as 7x7 patches (29/28 wide),
+    L2 32^2 tiles near the ring, L3 aligned 32^2 tiles near the ring."""
+    n1 = 200
+    cuts = [0, 29, 58, 87, 115, 143, 171, 200]   # 3 x 29 + 4 x 28
+    b1 = [(cuts[a], cuts[b], cuts[a + 1] - cuts[a], cuts[b + 1] - cuts[b])
+          for b in range(7) for a in range(7)]
+    l1 = _descs_from_boxes(b1, 2.0 / n1, 2.0 / n1)
+    n2, n3 = 2 * n1, 8 * n1
+    dx2, dx3 = 2.0 / n2, 2.0 / n3
+    b2 = []
+    for j in range(0, n2, 32):
+        for i in range(0, n2, 32):
+            w_, h_ = min(32, n2 - i), min(32, n2 - j)
+            miss, _ = _annulus_test(-1 + i * dx2, -1 + (i + w_) * dx2, -1 + j * dx2, -1 + (j + h_) * dx2, w2)
+            if not miss:
+                b2.append((i, j, w_, h_))
+    cover2 = _cover_map(n2, n2, b2)
+    b3 = []
+    for j in range(0, n3, 32):
+        for i in range(0, n3, 32):
+            miss, _ = _annulus_test(-1 + i * dx3, -1 + (i + 32) * dx3, -1 + j * dx3, -1 + (j + 32) * dx3, w3)
+            if not miss:
+                b3.append((i, j, 32, 32))
+    while True:  # drop L3 tiles that violate nesting, to a fixed point
+        cover3 = _cover_map(n3, n3, b3)
+        keep = [b for b in b3 if _nest_ok(b, cover3, cover2, 4)]
+        if len(keep) == len(b3):
+            break
+        b3 = keep
+    l2 = _descs_from_boxes(b2, dx2, dx2)
+    l3 = _descs_from_boxes(b3, dx3, dx3)
+    return Workload("c3_3level_r2_r4", [Level(l1), Level(l2, ratio=2), Level(l3, ratio=4)], steps=100,
+                    note=f"3 levels R=(2,4): {len(b1)} + {len(b2)} + {len(b3)} patches")
+
+
+def hierarchy_ic(wl: Workload) -> list:
+    """Ring initial data point-sampled on every level."""
+    return [ring_ic(L.descs) for L in wl.levels]

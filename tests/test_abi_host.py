@@ -1,0 +1,138 @@
+"""CPU tests of libclaw.so: it loads without a GPU, exports every symbol
+include/claw.h declares, validates inputs, and its host planner resolves every
+ghost cell exactly as the oracle's composite ghost rule does."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1808_02638_b200 import binding, workloads as W
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "claw.h")).read()
+    return sorted(set(re.findall(r"^(?:int|const char\*)\s+(claw_\w+)\s*\(", txt, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = binding.load()
+    syms = header_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(binding.EXPORTS)
+    assert "sm_100a" in binding.version()
+
+
+def test_library_is_built_for_sm100a():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", binding.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def host_ctx(bc=W.EXTRAP, world=1, rank=0, limiter=4, domain=W.DOMAIN):
+    return binding.Claw(domain, bc, limiter, 2, device=-1, rank=rank, world=world)
+
+
+def code_field(descs):
+    """Interior value = the cell's own donor code patch<<32 | lj<<16 | li
+    (exact in fp64), so a ghost copy reveals its donor."""
+    out = []
+    for p, d in enumerate(descs):
+        J, I = np.meshgrid(np.arange(d["my"]), np.arange(d["mx"]), indexing="ij")
+        code = (p * 2.0 ** 32 + J * 2.0 ** 16 + I).astype(np.float64)
+        out.append(np.stack([code, code, code]).ravel())
+    return np.concatenate(out)
+
+
+@pytest.mark.parametrize("bc", [W.EXTRAP, W.PERIODIC, (2, 2, 1, 1)])
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_planner_ghost_sources_equal_oracle_composite_rule(bc, seed):
+    d = W.ragged_level(seed, 26 + seed, 22, 8)
+    g = host_ctx(bc)
+    g.set_level(1, d)
+    o = oracle.Oracle(W.DOMAIN, bc, 4, 2, nthreads=2)
+    o.set_level(1, d, code_field(d))
+    o.fill_ghost(1)
+    for p in range(len(d)):
+        src, _ = g.debug_ghost_sources(1, p)
+        ref = o.read_padded(1, p)[0].astype(np.int64)
+        assert np.array_equal(src, ref), p
+
+
+def test_uniform_level_uses_few_rectangles_and_tiles():
+    d = W.uniform_level(4, 4, 32, 32)
+    g = host_ctx()
+    g.set_level(1, d)
+    n, cells, _ = g.level_owned(1)
+    assert n == 16 and cells == 16 * 1024
+
+
+@pytest.mark.parametrize("field,value", [("mx", 0), ("my", -1), ("mbc", 3), ("rho", 0.0), ("K", -1.0)])
+def test_descriptor_validation(field, value):
+    d = W.uniform_level(2, 2, 8, 8)
+    d[field][1] = value
+    g = host_ctx()
+    with pytest.raises(binding.ClawError) as e:
+        g.set_level(1, d)
+    assert e.value.code == binding.CLAW_EINVAL
+    assert "patch 1" in str(e.value)
+
+
+def test_level_validation():
+    g = host_ctx()
+    d = W.uniform_level(2, 2, 8, 8)
+    bad = d.copy(); bad["dx"][2] *= 2                    # dx differs within the level
+    with pytest.raises(binding.ClawError):
+        g.set_level(1, bad)
+    bad = d.copy(); bad["xlower"][1] += 0.3 * d["dx"][1]   # off the grid
+    with pytest.raises(binding.ClawError):
+        g.set_level(1, bad)
+    with pytest.raises(binding.ClawError):                 # does not tile
+        g.set_level(1, d[:3])
+    bad = d.copy(); bad["xlower"][1] = bad["xlower"][0]    # overlap
+    with pytest.raises(binding.ClawError):
+        g.set_level(1, bad)
+    with pytest.raises(binding.ClawError) as e:            # level 2 before 1 on a fresh ctx
+        host_ctx().set_level(2, d)
+    assert e.value.code == binding.CLAW_ESTATE
+    g.set_level(1, d)
+    with pytest.raises(binding.ClawError) as e:
+        g.fill_ghost(1, 0.0)
+    assert e.value.code == binding.CLAW_ENODEV
+
+
+def test_config_validation():
+    for kw in (dict(limiter=7), dict(bc=(1, 2, 1, 1)), dict(bc=(3, 3, 1, 1))):
+        args = dict(domain=W.DOMAIN, bc=W.EXTRAP, limiter=4)
+        args.update(kw)
+        with pytest.raises(binding.ClawError) as e:
+            binding.Claw(args["domain"], args["bc"], args["limiter"], 2, device=-1)
+        assert e.value.code == binding.CLAW_EINVAL
+
+
+def test_fine_level_without_donor_is_enest():
+    g = host_ctx()
+    g.set_level(1, W.uniform_level(1, 1, 8, 8))
+    # a fine patch (R=2) hugging the domain corner: every ghost has a donor
+    fine = W.make_descs([0], [0], 4, 4, 2 / 16, 2 / 16)
+    g.set_level(2, fine)
+    src, _ = g.debug_ghost_sources(2, 0)
+    assert (src == -1).sum() > 0          # coarse-interpolated ghosts exist
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_partition_balanced_and_contiguous_in_morton_order(world):
+    d = W.uniform_level(16, 16, 16, 16)
+    own = binding.partition(d, world)
+    counts = np.bincount(own, minlength=world)
+    assert counts.min() >= len(d) // world - 1 and counts.max() <= len(d) // world + 1
+    assert np.array_equal(own, binding.partition(d, world))
+    d2 = W.ragged_level(5, 40, 36, 9)
+    own2 = binding.partition(d2, world)
+    cells = np.bincount(own2, weights=d2["mx"] * d2["my"], minlength=world)
+    assert cells.max() <= cells.sum() / world + (d2["mx"] * d2["my"]).max()
