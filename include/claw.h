@@ -73,7 +73,11 @@ typedef struct {
                                   creates a non-blocking stream */
   int32_t tile_rows;           /* rows per tile of the fused step kernel (0 = default
                                   64); results are bitwise independent of it */
-  int32_t reserved[7];
+  int32_t path;                /* 0 auto: a level that is one uniform grid of equal
+                                  patches (row-major, whole domain, one medium, one
+                                  rank) uses the table-free grid kernel; 1 always the
+                                  generic ghost-table kernel.  Bitwise identical. */
+  int32_t reserved[6];
 } claw_config;
 
 /* Kernel-level statistics, accumulated while profiling is on. */

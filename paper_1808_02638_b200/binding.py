@@ -48,7 +48,8 @@ class ClawConfig(ctypes.Structure):
                 ("order_trans", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
                 ("nccl_unique_id", ctypes.c_void_p), ("stream", ctypes.c_void_p),
-                ("tile_rows", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+                ("tile_rows", ctypes.c_int32), ("path", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 6)]
 
 
 class ClawStats(ctypes.Structure):
@@ -141,13 +142,13 @@ class Claw:
 
     def __init__(self, domain=(-1.0, 1.0, -1.0, 1.0), bc=(1, 1, 1, 1), limiter=4,
                  order_trans=2, device=0, rank=0, world=1, nccl_id: bytes | None = None,
-                 stream: int | None = None, tile_rows: int = 0):
+                 stream: int | None = None, tile_rows: int = 0, path: int = 0):
         L = load()
         self._idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None
         cfg = ClawConfig(*[float(v) for v in domain], (ctypes.c_int32 * 4)(*bc), int(limiter),
                          int(order_trans), int(device), int(rank), int(world),
                          ctypes.cast(self._idbuf, ctypes.c_void_p) if self._idbuf else None,
-                         stream, int(tile_rows))
+                         stream, int(tile_rows), int(path))
         self._h = ctypes.c_void_p()
         rc = L.claw_create(ctypes.byref(cfg), ctypes.byref(self._h))
         if rc:

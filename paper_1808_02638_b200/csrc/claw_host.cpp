@@ -147,6 +147,9 @@ struct Level {
   bool stepped_once = false;
   int64_t device_bytes = 0;
   bool uniform = false;  // every patch shares (c, Z): step constants as kernel params
+  bool grid = false;     // one uniform grid of equal patches: table-free grid kernel
+  int npx = 0;
+  int64_t ngrid_tiles = 0;
 
   int find(int64_t I, int64_t J) const {
     if (I < 0 || J < 0 || I >= nx || J >= ny) return -1;
@@ -645,6 +648,24 @@ int plan_level(claw_ctx* c, int level, Level& L) {
   L.uniform = true;
   for (size_t lp = 1; lp < L.hpatch.size(); ++lp)
     if (L.hpatch[lp].c != L.hpatch[0].c || L.hpatch[lp].Z != L.hpatch[0].Z) L.uniform = false;
+  // grid mode: whole domain tiled by equal patches in row-major order, gapless
+  L.grid = false;
+  if (L.uniform && c->cfg.path == 0 && world == 1 && L.gapless && !L.owned.empty()) {
+    const int mx = L.desc[0].mx, my = L.desc[0].my;
+    bool ok = (L.nx % mx == 0) && (L.ny % my == 0) &&
+              static_cast<int64_t>(np) == (L.nx / mx) * (L.ny / my);
+    const int npx = ok ? static_cast<int>(L.nx / mx) : 0;
+    for (int p = 0; ok && p < np; ++p)
+      ok = L.desc[p].mx == mx && L.desc[p].my == my && L.i0[p] == static_cast<int64_t>(p % npx) * mx &&
+           L.j0[p] == static_cast<int64_t>(p / npx) * my && L.off[p] == static_cast<int64_t>(p) * 3 * mx * my;
+    if (ok && L.nx < (1ll << 30) && L.ny < (1ll << 30)) {
+      L.grid = true;
+      L.npx = npx;
+      const int th = std::min(c->tile_rows, my);
+      const int64_t nstrip = (L.nx + claw::grid_strip() - 1) / claw::grid_strip();
+      L.ngrid_tiles = nstrip * (L.ny / my) * ((my + th - 1) / th);
+    }
+  }
   L.htile.clear();
   for (size_t lp = 0; lp < L.owned.size(); ++lp) {
     const int mx = L.hpatch[lp].mx, my = L.hpatch[lp].my;
@@ -684,6 +705,9 @@ void fill_step_consts(const DevPatch& pt, double dt, double LS, int ot, claw::St
   k.TZ = (ot != 0) ? k.T / Z : 0.0;
   const double a = k.r * c, b = k.s * c;
   k.cfl = a > b ? a : b;
+  k.mr = -k.r;
+  k.ms = -k.s;
+  k.mT = -k.T;
 }
 
 template <class T>
@@ -971,6 +995,18 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
   P.level_cfl = L.lcfl.p;
   P.uniform = (L.uniform && !L.hpatch.empty()) ? 1 : 0;
   if (P.uniform) fill_step_consts(L.hpatch[0], dt, ctx->cfg.limiter == 4 ? 2.0 : 1.0, ctx->cfg.order_trans, P.k);
+  if (L.grid) {
+    P.grid = 1;
+    P.NX = static_cast<int32_t>(L.nx);
+    P.NY = static_cast<int32_t>(L.ny);
+    P.mx = L.desc[0].mx;
+    P.my = L.desc[0].my;
+    P.npx = L.npx;
+    P.th = std::min(ctx->tile_rows, P.my);
+    P.per_x = ctx->cfg.bc[0] == CLAW_BC_PERIODIC;
+    P.per_y = ctx->cfg.bc[2] == CLAW_BC_PERIODIC;
+    P.ntiles = static_cast<int32_t>(L.ngrid_tiles);
+  }
   record(ctx, ctx->ev_step, true);
   CUDA_TRY(static_cast<cudaError_t>(claw::launch_step(P, ctx->stream)));
   record(ctx, ctx->ev_step, false);
@@ -1103,7 +1139,10 @@ int claw_patch_cfl(claw_ctx* ctx, int32_t level, int32_t patch, double* cfl) {
   if (int rc = owned_index(ctx, level, patch, &lp)) return rc;
   if (!cfl) return fail(ctx, CLAW_EINVAL, "cfl is NULL");
   unsigned long long bits = 0;
-  CUDA_TRY(cudaMemcpyAsync(ctx->h_cfl, ctx->lev[level].pcfl.p + lp, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  // grid mode: every patch shares dt, dx, dy and c, so its max Courant number
+  // is the level's (the grid kernel only maintains the level slot)
+  const unsigned long long* src = ctx->lev[level].grid ? ctx->lev[level].lcfl.p : ctx->lev[level].pcfl.p + lp;
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_cfl, src, 8, cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   std::memcpy(&bits, ctx->h_cfl, 8);
   std::memcpy(cfl, &bits, 8);

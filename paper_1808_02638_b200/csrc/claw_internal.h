@@ -60,6 +60,7 @@ struct StepConsts {
   double ky4, ky2, ky4z;
   double T, TZ;           // r s c / 4, r s c / (4 Z)   (0 when order_trans = 0)
   double cfl;             // max(c dt/dx, c dt/dy)
+  double mr, ms, mT;      // -r, -s, -T (negation is exact)
 };
 
 struct StepParams {
@@ -78,6 +79,12 @@ struct StepParams {
   int32_t uniform;                // 1: every patch uses `k` below
   int32_t pad2;
   StepConsts k;
+  // grid mode (uniform tiling of the whole domain by equal patches in
+  // row-major order, gapless buffer): level-index strips, no tables
+  int32_t grid;
+  int32_t NX, NY, mx, my, npx;    // level extent, patch size, patches per row
+  int32_t th;                     // rows per tile (divides nothing; tiles stay in one patch row)
+  int32_t per_x, per_y;           // periodic in x / y
 };
 
 // Launchers (claw_kernels.cu).  All return cudaError_t as int.
@@ -90,5 +97,6 @@ int launch_pack(const double* q, const int64_t* off, const int64_t* cs, int64_t 
 int launch_gather_padded(const double* q, const double* frame, const DevPatch* patches,
                          const DevRect* rects, int32_t patch, double* out, void* stream);
 int max_tile_rows();
+int grid_strip();
 
 }  // namespace claw

@@ -322,3 +322,28 @@ def test_torch_stream_adoption():
         g.advance_level(1, 0.01)
     st = g.stats()
     assert st["step_launches"] == 3 and st["step_ms"] > 0 and st["cells_advanced"] == 3 * 16 * 1024
+
+
+@pytest.mark.parametrize("npx,npy,mx,my,bc,limiter,ot", [
+    (8, 8, 32, 32, W.EXTRAP, 4, 2), (4, 4, 64, 64, W.PERIODIC, 4, 2), (3, 5, 7, 5, W.EXTRAP, 1, 2),
+    (5, 3, 13, 70, (2, 2, 1, 1), 2, 1), (2, 2, 33, 31, (1, 1, 2, 2), 0, 0), (1, 1, 61, 3, W.EXTRAP, 3, 2)])
+def test_grid_kernel_bitwise_equals_generic_kernel(npx, npy, mx, my, bc, limiter, ot):
+    """The table-free grid kernel (uniform levels) and the generic ghost-table
+    kernel run the same cell arithmetic: results must agree bit for bit, and
+    both must match the oracle."""
+    d = W.uniform_level(npx, npy, mx, my)
+    q0 = W.random_ic(d, npx * 100 + mx)
+    dt = (0.9 if ot else 0.45) * 2 / max(npx * mx, npy * my)
+    res = []
+    for path in (0, 1):
+        g = binding.Claw(W.DOMAIN, bc, limiter, ot, device=0, path=path)
+        g.set_level(1, d, q0)
+        for n in range(6):
+            g.fill_ghost(1, n * dt)
+            c = g.advance_level(1, dt)
+        res.append((g.read_level(1), c, g.patch_cfl(1, len(d) - 1)))
+        g.close()
+    assert np.array_equal(res[0][0], res[1][0])
+    assert res[0][1] == res[1][1] and res[0][2] == res[1][2]
+    qg, qo = run_both(d, q0, 6, dt, bc=bc, limiter=limiter, order_trans=ot)
+    assert rel_err(qg, qo) <= TOL
