@@ -151,6 +151,17 @@ int claw_read_padded(claw_ctx* ctx, int32_t level, int32_t patch, double* q_out)
 int claw_patch_cfl(claw_ctx* ctx, int32_t level, int32_t patch, double* cfl);
 
 int claw_owner(const claw_ctx* ctx, int32_t level, int32_t patch, int32_t* rank);
+/* Kernel path chosen for a level: 0 generic ghost-table kernel, 1 grid kernel
+ * (see claw_config.path). */
+int claw_level_mode(const claw_ctx* ctx, int32_t level, int32_t* mode);
+
+/* One coarse step of the whole hierarchy, level by level with subcycling
+ * (P:113-118): level 1 advances by dt, then every finer level L+1 R_L times
+ * with dt / prod(R), each level step preceded by its ghost fill at its own
+ * time.  Runs entirely on the library's stream with one host synchronisation
+ * at the end; *cfl_max receives the max Courant number over all level steps.
+ * Ratios are taken from the levels' dx. */
+int claw_advance_hierarchy(claw_ctx* ctx, double t, double dt, double* cfl_max);
 int claw_level_owned(const claw_ctx* ctx, int32_t level, int32_t* npatch_owned,
                      int64_t* cells_owned, int64_t* device_bytes);
 

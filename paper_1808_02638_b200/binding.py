@@ -32,6 +32,7 @@ EXPORTS = [
     "claw_patch_cfl", "claw_owner", "claw_level_owned", "claw_debug_ghost_sources",
     "claw_debug_halo_counts", "claw_debug_halo_send", "claw_set_profiling", "claw_get_stats",
     "claw_reset_stats", "claw_synchronize", "claw_nccl_unique_id", "claw_version",
+    "claw_level_mode", "claw_advance_hierarchy",
 ]
 
 
@@ -99,6 +100,8 @@ def load() -> ctypes.CDLL:
     L.claw_reset_stats.argtypes = [vp]
     L.claw_synchronize.argtypes = [vp]
     L.claw_nccl_unique_id.argtypes = [vp]
+    L.claw_level_mode.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_int32)]
+    L.claw_advance_hierarchy.argtypes = [vp, d, d, dp]
     _lib = L
     return L
 
@@ -250,6 +253,17 @@ class Claw:
         r = ctypes.c_int32()
         self._check(load().claw_owner(self._h, level, patch, ctypes.byref(r)))
         return r.value
+
+    def level_mode(self, level: int) -> str:
+        m = ctypes.c_int32()
+        self._check(load().claw_level_mode(self._h, level, ctypes.byref(m)))
+        return "grid" if m.value == 1 else "generic"
+
+    def advance_hierarchy(self, t: float, dt: float) -> float:
+        """One coarse step of every level with subcycling, natively."""
+        c = ctypes.c_double()
+        self._check(load().claw_advance_hierarchy(self._h, float(t), float(dt), ctypes.byref(c)))
+        return c.value
 
     def level_owned(self, level: int):
         n, c, b = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()

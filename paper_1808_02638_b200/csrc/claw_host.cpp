@@ -148,6 +148,10 @@ struct Level {
   int64_t device_bytes = 0;
   bool uniform = false;  // every patch shares (c, Z): step constants as kernel params
   bool grid = false;     // one uniform grid of equal patches: table-free grid kernel
+  int th = 64;           // rows per tile for this level
+  int gen = 0;           // level CFL slot generation (lcfl[gen] is the last step's)
+  unsigned long long* hier = nullptr;  // coarse-step slot while claw_advance_hierarchy runs
+
   int npx = 0;
   int64_t ngrid_tiles = 0;
 
@@ -178,6 +182,9 @@ struct claw_ctx {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_step, ev_ghost, ev_pool;
   claw_stats stats{};
   int tile_rows = 64;
+  unsigned long long* hier_slot = nullptr;  // set while claw_advance_hierarchy runs
+  DevBuf<unsigned long long> hier_buf;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_free;  // event pool
 };
 
 namespace {
@@ -648,6 +655,18 @@ int plan_level(claw_ctx* c, int level, Level& L) {
   L.uniform = true;
   for (size_t lp = 1; lp < L.hpatch.size(); ++lp)
     if (L.hpatch[lp].c != L.hpatch[0].c || L.hpatch[lp].Z != L.hpatch[0].Z) L.uniform = false;
+  // rows per tile: the configured value, or (auto) the largest power of two
+  // <= 64 that still gives ~one tile per resident warp of the GPU (148 SMs x
+  // 16 warps); small, latency-bound levels get short tiles (>= 8) so the
+  // serial row march of each warp stays short
+  if (c->cfg.tile_rows > 0) {
+    L.th = c->tile_rows;
+  } else {
+    const int64_t want = 148 * 16;
+    int th = 64;
+    while (th > 8 && L.cells_owned / (32ll * th) < want) th /= 2;
+    L.th = th;
+  }
   // grid mode: whole domain tiled by equal patches in row-major order, gapless
   L.grid = false;
   if (L.uniform && c->cfg.path == 0 && world == 1 && L.gapless && !L.owned.empty()) {
@@ -661,7 +680,7 @@ int plan_level(claw_ctx* c, int level, Level& L) {
     if (ok && L.nx < (1ll << 30) && L.ny < (1ll << 30)) {
       L.grid = true;
       L.npx = npx;
-      const int th = std::min(c->tile_rows, my);
+      const int th = std::min(L.th, my);
       const int64_t nstrip = (L.nx + claw::grid_strip() - 1) / claw::grid_strip();
       L.ngrid_tiles = nstrip * (L.ny / my) * ((my + th - 1) / th);
     }
@@ -669,9 +688,9 @@ int plan_level(claw_ctx* c, int level, Level& L) {
   L.htile.clear();
   for (size_t lp = 0; lp < L.owned.size(); ++lp) {
     const int mx = L.hpatch[lp].mx, my = L.hpatch[lp].my;
-    for (int j0 = 0; j0 < my; j0 += c->tile_rows)
+    for (int j0 = 0; j0 < my; j0 += L.th)
       for (int i0 = 0; i0 < mx; i0 += 32) {
-        const int tw = std::min(32, mx - i0), th = std::min(c->tile_rows, my - j0);
+        const int tw = std::min(32, mx - i0), th = std::min(L.th, my - j0);
         L.htile.push_back(make_int4(static_cast<int>(lp), i0, j0, tw | (th << 16)));
       }
   }
@@ -732,25 +751,29 @@ int check_level(claw_ctx* c, int level) {
 void record(claw_ctx* c, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v, bool start) {
   if (!c->profiling) return;
   if (start) {
-    cudaEvent_t a, b;
-    cudaEventCreate(&a);
-    cudaEventCreate(&b);
-    v.emplace_back(a, b);
-    cudaEventRecord(a, c->stream);
+    std::pair<cudaEvent_t, cudaEvent_t> e;
+    if (!c->ev_free.empty()) {
+      e = c->ev_free.back();
+      c->ev_free.pop_back();
+    } else {
+      cudaEventCreate(&e.first);
+      cudaEventCreate(&e.second);
+    }
+    v.push_back(e);
+    cudaEventRecord(e.first, c->stream);
   } else {
     cudaEventRecord(v.back().second, c->stream);
   }
 }
 
-double drain(std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
+double drain(claw_ctx* c, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
   double ms = 0;
   for (auto& e : v) {
     float t = 0;
     cudaEventSynchronize(e.second);
     cudaEventElapsedTime(&t, e.first, e.second);
     ms += t;
-    cudaEventDestroy(e.first);
-    cudaEventDestroy(e.second);
+    c->ev_free.push_back(e);
   }
   v.clear();
   return ms;
@@ -832,9 +855,14 @@ int claw_nccl_unique_id(void* out128) {
 int claw_destroy(claw_ctx* ctx) {
   if (!ctx) return CLAW_EINVAL;
   if (!ctx->host_only && !ctx->dead) cudaStreamSynchronize(ctx->stream);
-  drain(ctx->ev_step);
-  drain(ctx->ev_ghost);
+  drain(ctx, ctx->ev_step);
+  drain(ctx, ctx->ev_ghost);
   for (auto& L : ctx->lev) L = Level();
+  for (auto& e : ctx->ev_free) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  ctx->hier_buf.reset();
   if (ctx->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(ctx->comm);
   if (ctx->h_cfl) cudaFreeHost(ctx->h_cfl);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -883,9 +911,10 @@ int claw_set_level(claw_ctx* ctx, int32_t level, int32_t npatch, const claw_patc
   if (int r2 = upload(ctx, L.dtile, L.htile)) return r2;
   if (int r2 = upload(ctx, L.dinterp, L.hinterp)) return r2;
   CUDA_TRY(L.pcfl.alloc(std::max<size_t>(L.owned.size(), 1)));
-  CUDA_TRY(L.lcfl.alloc(1));
+  CUDA_TRY(L.lcfl.alloc(2));
   CUDA_TRY(cudaMemset(L.pcfl.p, 0, L.pcfl.n * 8));
-  CUDA_TRY(cudaMemset(L.lcfl.p, 0, 8));
+  CUDA_TRY(cudaMemset(L.lcfl.p, 0, 16));
+  L.gen = 0;
   const int world = ctx->cfg.world;
   L.dsend_off.clear();
   L.dsend_cs.clear();
@@ -978,8 +1007,9 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
   if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
   if (!(dt >= 0) || !std::isfinite(dt)) return fail(ctx, CLAW_EINVAL, "dt=%g: must be finite and >= 0", dt);
   Level& L = ctx->lev[level];
-  CUDA_TRY(cudaMemsetAsync(L.pcfl.p, 0, L.pcfl.n * 8, ctx->stream));
-  CUDA_TRY(cudaMemsetAsync(L.lcfl.p, 0, 8, ctx->stream));
+  // CFL slots: this step accumulates into lcfl[g] (zeroed by the previous
+  // step's kernel, or at set_level) and zeroes lcfl[1-g] for the next step
+  const int g = 1 - L.gen;
   claw::StepParams P{};
   P.q = L.q[L.cur].p;
   P.qn = L.q[1 - L.cur].p;
@@ -992,7 +1022,9 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
   P.order_trans = ctx->cfg.order_trans;
   P.dt = dt;
   P.patch_cfl = L.pcfl.p;
-  P.level_cfl = L.lcfl.p;
+  P.level_cfl = L.lcfl.p + g;
+  P.level_cfl_reset = L.lcfl.p + (1 - g);
+  P.hier_cfl = ctx->hier_slot;
   P.uniform = (L.uniform && !L.hpatch.empty()) ? 1 : 0;
   if (P.uniform) fill_step_consts(L.hpatch[0], dt, ctx->cfg.limiter == 4 ? 2.0 : 1.0, ctx->cfg.order_trans, P.k);
   if (L.grid) {
@@ -1002,7 +1034,7 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
     P.mx = L.desc[0].mx;
     P.my = L.desc[0].my;
     P.npx = L.npx;
-    P.th = std::min(ctx->tile_rows, P.my);
+    P.th = std::min(L.th, P.my);
     P.per_x = ctx->cfg.bc[0] == CLAW_BC_PERIODIC;
     P.per_y = ctx->cfg.bc[2] == CLAW_BC_PERIODIC;
     P.ntiles = static_cast<int32_t>(L.ngrid_tiles);
@@ -1013,9 +1045,10 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
   ctx->stats.step_launches++;
   ctx->stats.cells_advanced += L.cells_owned;
   if (ctx->cfg.world > 1) {
-    ncclResult_t nr = g_nccl.AllReduce(L.lcfl.p, L.lcfl.p, 1, ncclFloat64, ncclMax, ctx->comm, ctx->stream);
+    ncclResult_t nr = g_nccl.AllReduce(L.lcfl.p + g, L.lcfl.p + g, 1, ncclFloat64, ncclMax, ctx->comm, ctx->stream);
     if (nr != ncclSuccess) return nccl_fail(ctx, nr, "ncclAllReduce(cfl, max)");
   }
+  L.gen = g;
   L.cur = 1 - L.cur;
   L.t_old = L.t_new;
   L.t_new = L.t_new + dt;
@@ -1028,7 +1061,7 @@ int claw_wait_cfl(claw_ctx* ctx, int32_t level, double* cfl_max) {
   if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
   if (!cfl_max) return fail(ctx, CLAW_EINVAL, "cfl_max is NULL");
   Level& L = ctx->lev[level];
-  CUDA_TRY(cudaMemcpyAsync(ctx->h_cfl, L.lcfl.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_cfl, L.lcfl.p + L.gen, 8, cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   *cfl_max = *ctx->h_cfl;
   return CLAW_OK;
@@ -1141,7 +1174,8 @@ int claw_patch_cfl(claw_ctx* ctx, int32_t level, int32_t patch, double* cfl) {
   unsigned long long bits = 0;
   // grid mode: every patch shares dt, dx, dy and c, so its max Courant number
   // is the level's (the grid kernel only maintains the level slot)
-  const unsigned long long* src = ctx->lev[level].grid ? ctx->lev[level].lcfl.p : ctx->lev[level].pcfl.p + lp;
+  const unsigned long long* src =
+      ctx->lev[level].grid ? ctx->lev[level].lcfl.p + ctx->lev[level].gen : ctx->lev[level].pcfl.p + lp;
   CUDA_TRY(cudaMemcpyAsync(ctx->h_cfl, src, 8, cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   std::memcpy(&bits, ctx->h_cfl, 8);
@@ -1154,6 +1188,50 @@ int claw_owner(const claw_ctx* ctx, int32_t level, int32_t patch, int32_t* rank)
   const Level& L = ctx->lev[level];
   if (patch < 0 || patch >= L.npatch) return CLAW_EINVAL;
   *rank = L.owner[patch];
+  return CLAW_OK;
+}
+
+int claw_level_mode(const claw_ctx* ctx, int32_t level, int32_t* mode) {
+  if (!ctx || !mode || level < 1 || level > kMaxLevel || !ctx->lev[level].set) return CLAW_EINVAL;
+  *mode = ctx->lev[level].grid ? 1 : 0;
+  return CLAW_OK;
+}
+
+// Recursive subcycled advance without host synchronisation; every
+// step kernel also folds its Courant number into the coarse-step slot.
+static int advance_rec(claw_ctx* ctx, int level, double t, double dt, int nlev) {
+  if (int rc = claw_fill_ghost(ctx, level, t)) return rc;
+  if (int rc = claw_advance_level_async(ctx, level, dt)) return rc;
+  if (level < nlev) {
+    const int R = ctx->lev[level + 1].ratio;
+    const double dtf = dt / R;
+    for (int k = 0; k < R; ++k)
+      if (int rc = advance_rec(ctx, level + 1, t + k * dtf, dtf, nlev)) return rc;
+  }
+  return CLAW_OK;
+}
+
+int claw_advance_hierarchy(claw_ctx* ctx, double t, double dt, double* cfl_max) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
+  if (!cfl_max) return fail(ctx, CLAW_EINVAL, "cfl_max is NULL");
+  int nlev = 0;
+  while (nlev < kMaxLevel && ctx->lev[nlev + 1].set) ++nlev;
+  if (nlev == 0) return fail(ctx, CLAW_ESTATE, "no level set");
+  if (!ctx->hier_buf.p) CUDA_TRY(ctx->hier_buf.alloc(1));
+  CUDA_TRY(cudaMemsetAsync(ctx->hier_buf.p, 0, 8, ctx->stream));
+  ctx->hier_slot = ctx->hier_buf.p;
+  const int rc = advance_rec(ctx, 1, t, dt, nlev);
+  ctx->hier_slot = nullptr;
+  if (rc) return rc;
+  if (ctx->cfg.world > 1) {
+    ncclResult_t nr = g_nccl.AllReduce(ctx->hier_buf.p, ctx->hier_buf.p, 1, ncclFloat64, ncclMax, ctx->comm,
+                                       ctx->stream);
+    if (nr != ncclSuccess) return nccl_fail(ctx, nr, "ncclAllReduce(cfl, max)");
+  }
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_cfl, ctx->hier_buf.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  *cfl_max = *ctx->h_cfl;
   return CLAW_OK;
 }
 
@@ -1211,16 +1289,16 @@ int claw_set_profiling(claw_ctx* ctx, int32_t on) {
 int claw_get_stats(claw_ctx* ctx, claw_stats* out) {
   if (int rc = check_ctx(ctx)) return rc;
   if (!out) return CLAW_EINVAL;
-  ctx->stats.step_ms += drain(ctx->ev_step);
-  ctx->stats.ghost_ms += drain(ctx->ev_ghost);
+  ctx->stats.step_ms += drain(ctx, ctx->ev_step);
+  ctx->stats.ghost_ms += drain(ctx, ctx->ev_ghost);
   *out = ctx->stats;
   return CLAW_OK;
 }
 
 int claw_reset_stats(claw_ctx* ctx) {
   if (int rc = check_ctx(ctx)) return rc;
-  drain(ctx->ev_step);
-  drain(ctx->ev_ghost);
+  drain(ctx, ctx->ev_step);
+  drain(ctx, ctx->ev_ghost);
   ctx->stats = claw_stats{};
   return CLAW_OK;
 }

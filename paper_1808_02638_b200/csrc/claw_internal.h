@@ -74,8 +74,10 @@ struct StepParams {
   int32_t limiter, order_trans;
   int32_t pad;
   double dt;
-  unsigned long long* patch_cfl;  // per owned patch, bits of a non-negative double
-  unsigned long long* level_cfl;  // 1 slot
+  unsigned long long* patch_cfl;  // per owned patch, bits of a non-negative double (plain stores)
+  unsigned long long* level_cfl;  // level slot of this step (atomicMax)
+  unsigned long long* level_cfl_reset;  // the other generation's slot, zeroed by the kernel
+  unsigned long long* hier_cfl;   // coarse-step slot of claw_advance_hierarchy, or null
   int32_t uniform;                // 1: every patch uses `k` below
   int32_t pad2;
   StepConsts k;

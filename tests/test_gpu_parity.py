@@ -347,3 +347,26 @@ def test_grid_kernel_bitwise_equals_generic_kernel(npx, npy, mx, my, bc, limiter
     assert res[0][1] == res[1][1] and res[0][2] == res[1][2]
     qg, qo = run_both(d, q0, 6, dt, bc=bc, limiter=limiter, order_trans=ot)
     assert rel_err(qg, qo) <= TOL
+
+
+def test_native_hierarchy_driver_equals_python_driver():
+    """claw_advance_hierarchy (native subcycling, one host sync) runs the same
+    level steps as the Python Berger-Oliger recursion: bitwise equal."""
+    wl = W.c2()
+    q0s = [W.random_ic(L.descs, 40 + k) for k, L in enumerate(wl.levels)]
+    out = []
+    for native in (True, False):
+        g = binding.Claw(wl.domain, wl.bc, wl.limiter, wl.order_trans, device=0)
+        for L, (lv, q0) in enumerate(zip(wl.levels, q0s), start=1):
+            g.set_level(L, lv.descs, q0)
+        dt = wl.dt0()
+        cfl = []
+        for n in range(3):
+            if native:
+                cfl.append(g.advance_hierarchy(n * dt, dt))
+            else:
+                cfl.append(binding.berger_oliger(g, 1, n * dt, dt, {1: 4}, 2))
+        out.append((g.read_level(1), g.read_level(2), cfl))
+        g.close()
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    assert out[0][2] == out[1][2]
