@@ -77,7 +77,13 @@ typedef struct {
                                   patches (row-major, whole domain, one medium, one
                                   rank) uses the table-free grid kernel; 1 always the
                                   generic ghost-table kernel.  Bitwise identical. */
-  int32_t reserved[6];
+  int32_t exchange;            /* world > 1 only.  0: NCCL (send/recv halo, max
+                                  all-reduce of the CFL).  1: external -- the caller
+                                  moves remote ghost cells with claw_halo_pack /
+                                  claw_halo_unpack between claw_fill_ghost and
+                                  claw_advance_level and reduces the CFL itself
+                                  (tests and custom transports; no NCCL needed) */
+  int32_t reserved[5];
 } claw_config;
 
 /* Kernel-level statistics, accumulated while profiling is on. */
@@ -173,6 +179,13 @@ int claw_level_owned(const claw_ctx* ctx, int32_t level, int32_t* npatch_owned,
  * out2, may be NULL). */
 int claw_debug_ghost_sources(const claw_ctx* ctx, int32_t level, int32_t patch,
                              int64_t* out, int64_t* out2);
+/* External halo exchange (claw_config.exchange = 1): pack the cells this rank
+ * sends to `peer` into host_out ([3][nsend], component-major, in the plan's
+ * order), or place the cells received from `peer` (host_in, [3][nrecv]) into
+ * this rank's ghost frames.  Synchronous. */
+int claw_halo_pack(claw_ctx* ctx, int32_t level, int32_t peer, double* host_out);
+int claw_halo_unpack(claw_ctx* ctx, int32_t level, int32_t peer, const double* host_in);
+
 /* Halo exchange plan: number of cells this rank sends to / receives from
  * `peer` for `level`. */
 int claw_debug_halo_counts(const claw_ctx* ctx, int32_t level, int32_t peer,

@@ -32,7 +32,7 @@ EXPORTS = [
     "claw_patch_cfl", "claw_owner", "claw_level_owned", "claw_debug_ghost_sources",
     "claw_debug_halo_counts", "claw_debug_halo_send", "claw_set_profiling", "claw_get_stats",
     "claw_reset_stats", "claw_synchronize", "claw_nccl_unique_id", "claw_version",
-    "claw_level_mode", "claw_advance_hierarchy",
+    "claw_level_mode", "claw_advance_hierarchy", "claw_halo_pack", "claw_halo_unpack",
 ]
 
 
@@ -50,7 +50,7 @@ class ClawConfig(ctypes.Structure):
                 ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
                 ("nccl_unique_id", ctypes.c_void_p), ("stream", ctypes.c_void_p),
                 ("tile_rows", ctypes.c_int32), ("path", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 6)]
+                ("exchange", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
 
 
 class ClawStats(ctypes.Structure):
@@ -102,6 +102,8 @@ def load() -> ctypes.CDLL:
     L.claw_nccl_unique_id.argtypes = [vp]
     L.claw_level_mode.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_int32)]
     L.claw_advance_hierarchy.argtypes = [vp, d, d, dp]
+    L.claw_halo_pack.argtypes = [vp, i32, i32, dp]
+    L.claw_halo_unpack.argtypes = [vp, i32, i32, dp]
     _lib = L
     return L
 
@@ -145,13 +147,13 @@ class Claw:
 
     def __init__(self, domain=(-1.0, 1.0, -1.0, 1.0), bc=(1, 1, 1, 1), limiter=4,
                  order_trans=2, device=0, rank=0, world=1, nccl_id: bytes | None = None,
-                 stream: int | None = None, tile_rows: int = 0, path: int = 0):
+                 stream: int | None = None, tile_rows: int = 0, path: int = 0, exchange: int = 0):
         L = load()
         self._idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None
         cfg = ClawConfig(*[float(v) for v in domain], (ctypes.c_int32 * 4)(*bc), int(limiter),
                          int(order_trans), int(device), int(rank), int(world),
                          ctypes.cast(self._idbuf, ctypes.c_void_p) if self._idbuf else None,
-                         stream, int(tile_rows), int(path))
+                         stream, int(tile_rows), int(path), int(exchange))
         self._h = ctypes.c_void_p()
         rc = L.claw_create(ctypes.byref(cfg), ctypes.byref(self._h))
         if rc:
@@ -281,6 +283,18 @@ class Claw:
             b.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))))
         shape = (int(d["my"]) + 4, int(d["mx"]) + 4)
         return a.reshape(shape), b.reshape(shape)
+
+    def halo_pack(self, level: int, peer: int) -> np.ndarray:
+        ns, _ = self.debug_halo_counts(level, peer)
+        out = np.empty(3 * ns)
+        if ns:
+            self._check(load().claw_halo_pack(self._h, level, peer, _dptr(out)))
+        return out
+
+    def halo_unpack(self, level: int, peer: int, buf: np.ndarray):
+        buf = np.ascontiguousarray(buf, dtype=np.float64)
+        if buf.size:
+            self._check(load().claw_halo_unpack(self._h, level, peer, _dptr(buf)))
 
     def debug_halo_counts(self, level: int, peer: int):
         s, r = ctypes.c_int64(), ctypes.c_int64()

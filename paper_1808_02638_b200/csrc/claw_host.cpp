@@ -280,7 +280,8 @@ int validate_config(claw_ctx* c, const claw_config* cfg) {
     return fail(c, CLAW_EINVAL, "order_trans=%d: must be 0..2", cfg->order_trans);
   if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world)
     return fail(c, CLAW_EINVAL, "rank=%d world=%d", cfg->rank, cfg->world);
-  if (cfg->world > 1 && !cfg->nccl_unique_id && cfg->device >= 0)
+  if (cfg->exchange != 0 && cfg->exchange != 1) return fail(c, CLAW_EINVAL, "exchange=%d: must be 0 or 1", cfg->exchange);
+  if (cfg->world > 1 && cfg->exchange == 0 && !cfg->nccl_unique_id && cfg->device >= 0)
     return fail(c, CLAW_EINVAL, "world>1 needs nccl_unique_id");
   if (cfg->tile_rows < 0 || cfg->tile_rows > claw::max_tile_rows())
     return fail(c, CLAW_EINVAL, "tile_rows=%d: must be 0..%d", cfg->tile_rows, claw::max_tile_rows());
@@ -830,7 +831,7 @@ int claw_create(const claw_config* cfg, claw_ctx** out) {
     ctx->own_stream = true;
   }
   CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_cfl), sizeof(double)));
-  if (cfg->world > 1) {
+  if (cfg->world > 1 && cfg->exchange == 0) {
     if (!g_nccl.load(ctx->err)) {
       ctx->dead = true;
       return CLAW_ENCCL;
@@ -971,7 +972,7 @@ int claw_fill_ghost(claw_ctx* ctx, int32_t level, double t) {
                                                           L.ncoarse, L.frame.p, L.ncoarse, ctx->stream)));
     ctx->stats.ghost_launches++;
   }
-  if (ctx->cfg.world > 1) {
+  if (ctx->cfg.world > 1 && ctx->cfg.exchange == 0) {
     const int world = ctx->cfg.world;
     for (int r = 0; r < world; ++r) {
       const int64_t n = static_cast<int64_t>(L.send_off[r].size());
@@ -1044,7 +1045,7 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
   record(ctx, ctx->ev_step, false);
   ctx->stats.step_launches++;
   ctx->stats.cells_advanced += L.cells_owned;
-  if (ctx->cfg.world > 1) {
+  if (ctx->cfg.world > 1 && ctx->cfg.exchange == 0) {
     ncclResult_t nr = g_nccl.AllReduce(L.lcfl.p + g, L.lcfl.p + g, 1, ncclFloat64, ncclMax, ctx->comm, ctx->stream);
     if (nr != ncclSuccess) return nccl_fail(ctx, nr, "ncclAllReduce(cfl, max)");
   }
@@ -1224,7 +1225,7 @@ int claw_advance_hierarchy(claw_ctx* ctx, double t, double dt, double* cfl_max) 
   const int rc = advance_rec(ctx, 1, t, dt, nlev);
   ctx->hier_slot = nullptr;
   if (rc) return rc;
-  if (ctx->cfg.world > 1) {
+  if (ctx->cfg.world > 1 && ctx->cfg.exchange == 0) {
     ncclResult_t nr = g_nccl.AllReduce(ctx->hier_buf.p, ctx->hier_buf.p, 1, ncclFloat64, ncclMax, ctx->comm,
                                        ctx->stream);
     if (nr != ncclSuccess) return nccl_fail(ctx, nr, "ncclAllReduce(cfl, max)");
@@ -1255,6 +1256,35 @@ int claw_debug_ghost_sources(const claw_ctx* ctx, int32_t level, int32_t patch, 
     const auto& w = L.dbg_remote[L.local[patch]];
     std::memcpy(out2, w.data(), w.size() * sizeof(int64_t));
   }
+  return CLAW_OK;
+}
+
+int claw_halo_pack(claw_ctx* ctx, int32_t level, int32_t peer, double* host_out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = check_level(ctx, level)) return rc;
+  if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
+  if (peer < 0 || peer >= ctx->cfg.world || !host_out) return fail(ctx, CLAW_EINVAL, "bad peer or buffer");
+  Level& L = ctx->lev[level];
+  const int64_t n = static_cast<int64_t>(L.send_off[peer].size());
+  if (n == 0) return CLAW_OK;
+  CUDA_TRY(static_cast<cudaError_t>(claw::launch_pack(L.q[L.cur].p, L.dsend_off[peer]->p, L.dsend_cs[peer]->p, n,
+                                                      L.dsend_buf[peer]->p, ctx->stream)));
+  CUDA_TRY(cudaMemcpyAsync(host_out, L.dsend_buf[peer]->p, 3 * n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return CLAW_OK;
+}
+
+int claw_halo_unpack(claw_ctx* ctx, int32_t level, int32_t peer, const double* host_in) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = check_level(ctx, level)) return rc;
+  if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
+  if (peer < 0 || peer >= ctx->cfg.world || !host_in) return fail(ctx, CLAW_EINVAL, "bad peer or buffer");
+  Level& L = ctx->lev[level];
+  const int64_t n = L.nrecv[peer];
+  if (n == 0) return CLAW_OK;
+  CUDA_TRY(cudaMemcpyAsync(L.frame.p + L.recv_frame_off[peer], host_in, 3 * n * 8, cudaMemcpyHostToDevice,
+                           ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   return CLAW_OK;
 }
 

@@ -1,0 +1,74 @@
+"""Multi-rank path on ONE GPU: N contexts (world = N, one per virtual rank) in
+one process, remote ghost cells moved through host memory with the external
+exchange mode (claw_halo_pack / claw_halo_unpack) instead of NCCL.  Everything
+the NCCL path runs on each rank -- Morton partition, send/receive plans, the
+pack kernel, frame-buffer ghosts read by the generic step kernel, per-rank
+CFL -- runs here, and the N-rank result must be bitwise equal to the 1-rank
+result (halo values are exact copies, the max is exact)."""
+import numpy as np
+import pytest
+
+from paper_1808_02638_b200 import binding, workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def layout(name):
+    if name == "c5small":
+        return W.c5(patches_per_side=8, mx=32).levels[0].descs
+    if name == "c4small":
+        return W.c4(patches_per_side=16).levels[0].descs
+    return W.ragged_level(6, 90, 70, 30)
+
+
+@pytest.mark.parametrize("world,name,bc", [(2, "c5small", W.EXTRAP), (3, "ragged", W.PERIODIC),
+                                           (4, "c4small", W.PERIODIC), (8, "c5small", W.EXTRAP),
+                                           (5, "ragged", (1, 1, 2, 2))])
+def test_virtual_ranks_bitwise_equal_single_rank(world, name, bc):
+    d = layout(name)
+    q0 = W.random_ic(d, world)
+    offs = W.level_offsets(d)
+    owners = binding.partition(d, world)
+    ctxs = []
+    for r in range(world):
+        c = binding.Claw(W.DOMAIN, bc, 4, 2, device=0, rank=r, world=world, exchange=1)
+        mine = np.concatenate([q0[offs[p]:offs[p + 1]] for p in range(len(d)) if owners[p] == r])
+        c.set_level(1, d, mine)
+        assert [c.owner(1, p) for p in range(len(d))] == list(owners)
+        ctxs.append(c)
+    ref = binding.Claw(W.DOMAIN, bc, 4, 2, device=0)
+    ref.set_level(1, d, q0)
+    dx = float(min(d["dx"][0], d["dy"][0]))
+    dt = 0.9 * dx
+    moved = 0
+    for n in range(6):
+        for c in ctxs:
+            c.fill_ghost(1, n * dt)
+        for r in range(world):
+            for s in range(world):
+                if r != s:
+                    buf = ctxs[r].halo_pack(1, s)
+                    moved += buf.size
+                    ctxs[s].halo_unpack(1, r, buf)
+        cfl = max(c.advance_level(1, dt) for c in ctxs)
+        ref.fill_ghost(1, n * dt)
+        assert cfl == ref.advance_level(1, dt)
+    assert moved > 0
+    full = ref.read_level(1)
+    got = np.empty_like(full)
+    for r, c in enumerate(ctxs):
+        mine = c.read_level(1)
+        k = 0
+        for p in range(len(d)):
+            if owners[p] == r:
+                n = offs[p + 1] - offs[p]
+                got[offs[p]:offs[p + 1]] = mine[k:k + n]
+                k += n
+    assert np.array_equal(got, full)
