@@ -149,6 +149,11 @@ struct Level {
   bool uniform = false;  // every patch shares (c, Z): step constants as kernel params
   bool grid = false;     // one uniform grid of equal patches: table-free grid kernel
   int th = 64;           // rows per tile for this level
+  bool band = false;     // world > 1 band partition of a uniform grid (grid kernel per rank)
+  int gnpx = 0, gnpy = 0;  // grid layout of the whole level
+  int64_t Y0 = 0, Y1 = 0;  // this rank's band of level rows
+  int64_t hoff[4] = {-1, -1, -1, -1};  // frame offset (column 0) of halo rows Y0-2, Y0-1, Y1, Y1+1; -1 local
+  int64_t hcs[4] = {0, 0, 0, 0};       // their component strides
   int gen = 0;           // level CFL slot generation (lcfl[gen] is the last step's)
   unsigned long long* hier = nullptr;  // coarse-step slot while claw_advance_hierarchy runs
 
@@ -237,10 +242,50 @@ uint64_t morton(uint32_t x, uint32_t y) {
   return spread(x) | (spread(y) << 1);
 }
 
+// A uniform grid of equal patches in row-major order filling a rectangle of
+// the index space (relative to the minimum corner): returns npx, npy.
+bool grid_layout(int npatch, const claw_patch_desc* d, const std::vector<int64_t>& i0,
+                 const std::vector<int64_t>& j0, int* npx_out, int* npy_out) {
+  const int mx = d[0].mx, my = d[0].my;
+  int64_t imin = i0[0], jmin = j0[0], imax = i0[0], jmax = j0[0];
+  for (int p = 1; p < npatch; ++p) {
+    imin = std::min(imin, i0[p]);
+    jmin = std::min(jmin, j0[p]);
+    imax = std::max(imax, i0[p]);
+    jmax = std::max(jmax, j0[p]);
+  }
+  const int64_t npx = (imax - imin) / mx + 1, npy = (jmax - jmin) / my + 1;
+  if (npx * npy != npatch) return false;
+  for (int p = 0; p < npatch; ++p)
+    if (d[p].mx != mx || d[p].my != my || i0[p] - imin != (p % npx) * mx || j0[p] - jmin != (p / npx) * my)
+      return false;
+  *npx_out = static_cast<int>(npx);
+  *npy_out = static_cast<int>(npy);
+  return true;
+}
+
+// Owner map.  A uniform grid with at least `world` patch rows is cut into
+// horizontal bands of whole patch rows (rank r: rows [r npy / world, (r+1) npy
+// / world)), so every rank advances a rectangle with the table-free grid
+// kernel and exchanges only full halo rows.  Anything else: patches in Morton
+// order of their lower-left index, split contiguously by cell count.
 void partition_impl(int npatch, const claw_patch_desc* d, const std::vector<int64_t>& i0,
                     const std::vector<int64_t>& j0, int world, int32_t* owner) {
   if (world <= 1) {
     for (int p = 0; p < npatch; ++p) owner[p] = 0;
+    return;
+  }
+  int npx, npy;
+  if (grid_layout(npatch, d, i0, j0, &npx, &npy) && npy >= world &&
+      static_cast<int64_t>(d[0].my) * (npy / world) >= 4) {
+    for (int p = 0; p < npatch; ++p) {
+      const int64_t pr = p / npx;
+      // band cut r: rows [floor(r npy / world), floor((r+1) npy / world))
+      int r = static_cast<int>((pr * world) / npy);
+      while (r + 1 < world && (static_cast<int64_t>(r + 1) * npy) / world <= pr) ++r;
+      while (r > 0 && (static_cast<int64_t>(r) * npy) / world > pr) --r;
+      owner[p] = r;
+    }
     return;
   }
   std::vector<int> order(npatch);
@@ -473,6 +518,79 @@ int plan_level(claw_ctx* c, int level, Level& L) {
   L.buf_elems = off;
 
   const Level* C = (level > 1) ? &c->lev[level - 1] : nullptr;
+
+  L.send_off.assign(world, {});
+  L.send_cs.assign(world, {});
+  L.send_dbg.assign(world, {});
+  L.nrecv.assign(world, 0);
+  L.recv_frame_off.assign(world, 0);
+
+  // ---- band mode: a uniform grid over the whole domain cut into bands of
+  // patch rows by partition_impl; halo = two full rows below and above
+  L.band = false;
+  if (world > 1 && grid_layout(np, L.desc.data(), L.i0, L.j0, &L.gnpx, &L.gnpy)) {
+    const int mx = L.desc[0].mx, my = L.desc[0].my;
+    const bool whole = L.gnpx * static_cast<int64_t>(mx) == L.nx && L.gnpy * static_cast<int64_t>(my) == L.ny;
+    if (whole && L.gnpy >= world && static_cast<int64_t>(my) * (L.gnpy / world) >= 4 && !L.owned.empty()) {
+      L.band = true;
+      const int npx = L.gnpx;
+      auto band_of = [&](int r, int64_t& y0, int64_t& y1) {
+        y0 = (static_cast<int64_t>(r) * L.gnpy / world) * my;
+        y1 = (static_cast<int64_t>(r + 1) * L.gnpy / world) * my;
+      };
+      auto row_owner = [&](int64_t J) { return L.owner[static_cast<size_t>((J / my) * npx)]; };
+      auto halo_rows = [&](int r, int64_t* J) {
+        int64_t y0, y1;
+        band_of(r, y0, y1);
+        const int64_t raw[4] = {y0 - 2, y0 - 1, y1, y1 + 1};
+        for (int k = 0; k < 4; ++k) J[k] = map_axis(raw[k], L.ny, cfg.bc[2], cfg.bc[3]);
+      };
+      band_of(me, L.Y0, L.Y1);
+      if (L.owned.front() != static_cast<int>((L.Y0 / my) * npx)) return fail(c, CLAW_EINVAL, "band mismatch");
+      int64_t Jme[4];
+      halo_rows(me, Jme);
+      int64_t fo = 0;
+      for (int srank = 0; srank < world; ++srank) {
+        if (srank == me) continue;
+        int cnt = 0;
+        for (int k = 0; k < 4; ++k)
+          if (row_owner(Jme[k]) == srank && !(Jme[k] >= L.Y0 && Jme[k] < L.Y1)) ++cnt;
+        if (!cnt) continue;
+        L.recv_frame_off[srank] = fo;
+        L.nrecv[srank] = static_cast<int64_t>(cnt) * L.nx;
+        int idx = 0;
+        for (int k = 0; k < 4; ++k)
+          if (row_owner(Jme[k]) == srank && !(Jme[k] >= L.Y0 && Jme[k] < L.Y1)) {
+            L.hoff[k] = fo + static_cast<int64_t>(idx++) * L.nx;
+            L.hcs[k] = L.nrecv[srank];
+          }
+        fo += 3 * L.nrecv[srank];
+      }
+      L.coarse_frame_off = fo;
+      L.ncoarse = 0;
+      L.frame_elems = fo;
+      // send lists: for every other rank, its halo rows that I own, in its k order
+      for (int r = 0; r < world; ++r) {
+        if (r == me) continue;
+        int64_t Jr[4], y0r, y1r;
+        halo_rows(r, Jr);
+        band_of(r, y0r, y1r);
+        for (int k = 0; k < 4; ++k) {
+          if (row_owner(Jr[k]) != me || (Jr[k] >= y0r && Jr[k] < y1r)) continue;
+          const int64_t prow = Jr[k] / my, lj = Jr[k] % my;
+          for (int64_t Cc = 0; Cc < L.nx; ++Cc) {
+            const int gp = static_cast<int>(prow * npx + Cc / mx);
+            const int lq = L.local[gp];
+            const int64_t li = Cc % mx;
+            L.send_off[r].push_back(L.off[lq] + lj * mx + li);
+            L.send_cs[r].push_back(static_cast<int64_t>(mx) * my);
+            L.send_dbg[r].push_back((static_cast<int64_t>(gp) << 32) | (lj << 16) | li);
+          }
+        }
+      }
+    }
+  }
+
   // which patches need resolving: owned ones (receive side) and, for world>1,
   // patches of other ranks whose ghost frame may read my cells (send side)
   std::vector<char> need(np, 0);
@@ -485,7 +603,7 @@ int plan_level(claw_ctx* c, int level, Level& L) {
     by1 = std::max(by1, L.j0[p] + L.desc[p].my);
   }
   const bool periodic = cfg.bc[0] == CLAW_BC_PERIODIC || cfg.bc[2] == CLAW_BC_PERIODIC;
-  if (world > 1)
+  if (world > 1 && !L.band)
     for (int p = 0; p < np; ++p) {
       if (need[p]) continue;
       const int64_t a0 = L.i0[p] - 2, a1 = L.i0[p] + L.desc[p].mx + 2;
@@ -495,11 +613,6 @@ int plan_level(claw_ctx* c, int level, Level& L) {
       need[p] = touch;
     }
 
-  L.send_off.assign(world, {});
-  L.send_cs.assign(world, {});
-  L.send_dbg.assign(world, {});
-  L.nrecv.assign(world, 0);
-  L.recv_frame_off.assign(world, 0);
   L.hinterp.clear();
   L.dbg_src.assign(L.owned.size(), {});
   L.dbg_remote.assign(L.owned.size(), {});
@@ -550,7 +663,16 @@ int plan_level(claw_ctx* c, int level, Level& L) {
                                    static_cast<int64_t>(L.desc[q].mx) * L.desc[q].my};
               L.dbg_src[lp][idx] = code;
             } else {
-              pend.push_back(Pending{lp, idx, 1, src_owner, 0, 0, 0, 0});
+              if (L.band) {  // full halo rows in the band frame
+                int kk = -1;
+                const int64_t raw[4] = {L.Y0 - 2, L.Y0 - 1, L.Y1, L.Y1 + 1};
+                for (int k2 = 0; k2 < 4; ++k2)
+                  if (L.hoff[k2] >= 0 && map_axis(raw[k2], L.ny, cfg.bc[2], cfg.bc[3]) == J) kk = k2;
+                if (kk < 0) return fail(c, CLAW_EINVAL, "band halo row not planned");
+                cells[lp][idx] = Src{1, L.hoff[kk] + I, L.hcs[kk]};
+              } else {
+                pend.push_back(Pending{lp, idx, 1, src_owner, 0, 0, 0, 0});
+              }
               L.dbg_src[lp][idx] = -2;
               L.dbg_remote[lp][idx] = code;
             }
@@ -574,12 +696,15 @@ int plan_level(claw_ctx* c, int level, Level& L) {
   }
 
   // frame layout: [peer 0 segment][peer 1 segment]...[coarse segment], each [3][n]
-  for (const Pending& pd : pend)
-    if (pd.kind == 1) L.nrecv[pd.src_rank]++;
-  int64_t fo = 0;
-  for (int r = 0; r < world; ++r) {
-    L.recv_frame_off[r] = fo;
-    fo += 3 * L.nrecv[r];
+  // (band mode: planned above, full halo rows per source rank)
+  int64_t fo = L.band ? L.frame_elems : 0;
+  if (!L.band) {
+    for (const Pending& pd : pend)
+      if (pd.kind == 1) L.nrecv[pd.src_rank]++;
+    for (int r = 0; r < world; ++r) {
+      L.recv_frame_off[r] = fo;
+      fo += 3 * L.nrecv[r];
+    }
   }
   L.coarse_frame_off = fo;
   L.ncoarse = 0;
@@ -670,20 +795,29 @@ int plan_level(claw_ctx* c, int level, Level& L) {
   }
   // grid mode: whole domain tiled by equal patches in row-major order, gapless
   L.grid = false;
-  if (L.uniform && c->cfg.path == 0 && world == 1 && L.gapless && !L.owned.empty()) {
+  if (L.uniform && c->cfg.path == 0 && (world == 1 || L.band) && L.gapless && !L.owned.empty()) {
     const int mx = L.desc[0].mx, my = L.desc[0].my;
     bool ok = (L.nx % mx == 0) && (L.ny % my == 0) &&
               static_cast<int64_t>(np) == (L.nx / mx) * (L.ny / my);
     const int npx = ok ? static_cast<int>(L.nx / mx) : 0;
     for (int p = 0; ok && p < np; ++p)
       ok = L.desc[p].mx == mx && L.desc[p].my == my && L.i0[p] == static_cast<int64_t>(p % npx) * mx &&
-           L.j0[p] == static_cast<int64_t>(p / npx) * my && L.off[p] == static_cast<int64_t>(p) * 3 * mx * my;
+           L.j0[p] == static_cast<int64_t>(p / npx) * my;
+    // owned patches: whole patch rows, back to back in the buffer
+    const int p0 = L.owned.front();
+    for (size_t lp = 0; ok && lp < L.owned.size(); ++lp)
+      ok = L.owned[lp] == p0 + static_cast<int>(lp) && L.off[lp] == static_cast<int64_t>(lp) * 3 * mx * my;
+    ok = ok && (p0 % npx == 0) && (L.owned.size() % npx == 0);
     if (ok && L.nx < (1ll << 30) && L.ny < (1ll << 30)) {
       L.grid = true;
       L.npx = npx;
+      if (!L.band) {
+        L.Y0 = 0;
+        L.Y1 = L.ny;
+      }
       const int th = std::min(L.th, my);
       const int64_t nstrip = (L.nx + claw::grid_strip() - 1) / claw::grid_strip();
-      L.ngrid_tiles = nstrip * (L.ny / my) * ((my + th - 1) / th);
+      L.ngrid_tiles = nstrip * ((L.Y1 - L.Y0) / my) * ((my + th - 1) / th);
     }
   }
   L.htile.clear();
@@ -1039,6 +1173,12 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
     P.per_x = ctx->cfg.bc[0] == CLAW_BC_PERIODIC;
     P.per_y = ctx->cfg.bc[2] == CLAW_BC_PERIODIC;
     P.ntiles = static_cast<int32_t>(L.ngrid_tiles);
+    P.Y0 = static_cast<int32_t>(L.Y0);
+    P.Y1 = static_cast<int32_t>(L.Y1);
+    for (int k = 0; k < 4; ++k) {
+      P.hoff[k] = L.hoff[k];
+      P.hcs[k] = L.hcs[k];
+    }
   }
   record(ctx, ctx->ev_step, true);
   CUDA_TRY(static_cast<cudaError_t>(claw::launch_step(P, ctx->stream)));

@@ -85,8 +85,11 @@ struct StepParams {
   // row-major order, gapless buffer): level-index strips, no tables
   int32_t grid;
   int32_t NX, NY, mx, my, npx;    // level extent, patch size, patches per row
-  int32_t th;                     // rows per tile (divides nothing; tiles stay in one patch row)
+  int32_t th;                     // rows per tile (tiles stay in one patch row)
   int32_t per_x, per_y;           // periodic in x / y
+  int32_t Y0, Y1;                 // this rank's band of level rows (whole level: 0, NY)
+  int64_t hoff[4];                // band halo rows Y0-2, Y0-1, Y1, Y1+1: frame offset of
+  int64_t hcs[4];                 // column 0 (-1: the row is local) and component stride
 };
 
 // Launchers (claw_kernels.cu).  All return cudaError_t as int.

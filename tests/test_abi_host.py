@@ -126,13 +126,23 @@ def test_fine_level_without_donor_is_enest():
 
 
 @pytest.mark.parametrize("world", [2, 3, 8])
-def test_partition_balanced_and_contiguous_in_morton_order(world):
-    d = W.uniform_level(16, 16, 16, 16)
+def test_partition_uniform_grid_into_bands(world):
+    """A uniform grid is cut into bands of whole patch rows (grid kernel per
+    rank, halo = full rows); balanced to within one patch row."""
+    d = W.uniform_level(16, 13, 16, 16)
     own = binding.partition(d, world)
-    counts = np.bincount(own, minlength=world)
-    assert counts.min() >= len(d) // world - 1 and counts.max() <= len(d) // world + 1
+    rows = own.reshape(13, 16)
+    assert (rows == rows[:, :1]).all()                 # whole patch rows
+    assert (np.diff(rows[:, 0]) >= 0).all()            # contiguous bands, ascending
+    counts = np.bincount(rows[:, 0], minlength=world)
+    assert counts.min() >= 13 // world and counts.max() <= 13 // world + 1
     assert np.array_equal(own, binding.partition(d, world))
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_partition_ragged_morton_balanced(world):
     d2 = W.ragged_level(5, 40, 36, 9)
     own2 = binding.partition(d2, world)
     cells = np.bincount(own2, weights=d2["mx"] * d2["my"], minlength=world)
     assert cells.max() <= cells.sum() / world + (d2["mx"] * d2["my"]).max()
+    assert np.array_equal(own2, binding.partition(d2, world))

@@ -28,20 +28,23 @@ def layout(name):
     return W.ragged_level(6, 90, 70, 30)
 
 
-@pytest.mark.parametrize("world,name,bc", [(2, "c5small", W.EXTRAP), (3, "ragged", W.PERIODIC),
-                                           (4, "c4small", W.PERIODIC), (8, "c5small", W.EXTRAP),
-                                           (5, "ragged", (1, 1, 2, 2))])
-def test_virtual_ranks_bitwise_equal_single_rank(world, name, bc):
+@pytest.mark.parametrize("world,name,bc,path", [(2, "c5small", W.EXTRAP, 0), (3, "ragged", W.PERIODIC, 0),
+                                                (4, "c4small", W.PERIODIC, 0), (8, "c5small", W.EXTRAP, 0),
+                                                (5, "ragged", (1, 1, 2, 2), 0), (4, "c4small", W.PERIODIC, 1),
+                                                (3, "c5small", (1, 1, 2, 2), 1)])
+def test_virtual_ranks_bitwise_equal_single_rank(world, name, bc, path):
     d = layout(name)
     q0 = W.random_ic(d, world)
     offs = W.level_offsets(d)
     owners = binding.partition(d, world)
     ctxs = []
     for r in range(world):
-        c = binding.Claw(W.DOMAIN, bc, 4, 2, device=0, rank=r, world=world, exchange=1)
+        c = binding.Claw(W.DOMAIN, bc, 4, 2, device=0, rank=r, world=world, exchange=1, path=path)
         mine = np.concatenate([q0[offs[p]:offs[p + 1]] for p in range(len(d)) if owners[p] == r])
         c.set_level(1, d, mine)
         assert [c.owner(1, p) for p in range(len(d))] == list(owners)
+        # uniform grids: band partition + table-free grid kernel on every rank
+        assert c.level_mode(1) == ("generic" if name == "ragged" or path == 1 else "grid")
         ctxs.append(c)
     ref = binding.Claw(W.DOMAIN, bc, 4, 2, device=0)
     ref.set_level(1, d, q0)

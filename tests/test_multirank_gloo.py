@@ -85,11 +85,17 @@ def test_halo_plans_agree_and_reproduce_oracle_ghosts(world, layout, bc):
     total_remote = 0
     for r in range(world):
         for s in range(world):
-            # what s sends to r == what r expects from s, in the same order
             sent = [tuple(x) for x in plans[s]["send"][r]]
-            expect = plans[r]["recv_donors"].get(s, [])
-            assert plans[r]["nrecv"][s] == len(sent) == len(expect)
-            assert sent == [tuple(x) for x in expect]
+            expect = [tuple(x) for x in plans[r]["recv_donors"].get(s, [])]
+            assert plans[r]["nrecv"][s] == len(sent)
+            if layout == "uniform":
+                # band mode: whole halo rows are shipped once; every remote
+                # ghost cell of r reads one of them (corners share slots)
+                assert set(expect) <= set(sent)
+                assert len(set(sent)) == len(sent)
+            else:
+                # Morton mode: one frame slot per remote ghost cell, same order
+                assert sent == expect
             if r != s:
                 total_remote += len(sent)
             else:
