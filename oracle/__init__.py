@@ -70,6 +70,7 @@ def lib() -> ctypes.CDLL:
         L.oracle_write.argtypes = [vp, ctypes.c_int, ctypes.c_int, dp]
         L.oracle_patch_cfl.argtypes = [vp, ctypes.c_int, ctypes.c_int, dp]
         L.oracle_level_time.argtypes = [vp, ctypes.c_int, dp, dp]
+        L.oracle_update_level.argtypes = [vp, ctypes.c_int]
         L.oracle_step_patch.argtypes = [ctypes.c_int, ctypes.c_int, dp, ctypes.c_double,
                                         ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                         ctypes.c_double, ctypes.c_int, ctypes.c_int, dp, dp]
@@ -130,6 +131,10 @@ class Oracle:
         c = ctypes.c_double()
         self._check(lib().oracle_advance_level(self._h, level, float(dt), ctypes.byref(c)))
         return c.value
+
+    def update_level(self, level: int):
+        """Average `level` onto `level - 1` where fully covered."""
+        self._check(lib().oracle_update_level(self._h, level))
 
     def read(self, level: int, patch: int) -> np.ndarray:
         d = self._descs[level][patch]

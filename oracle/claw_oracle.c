@@ -644,6 +644,43 @@ int oracle_advance_level(oracle_ctx* c, int level, double dt, double* cfl_max) {
   return 0;
 }
 
+int oracle_update_level(oracle_ctx* c, int level) {
+  if (!c || level < 2 || level > MAXLEVEL || c->lev[level].npatch == 0 || c->lev[level - 1].npatch == 0)
+    return fail(c, -2, "update needs a fine level >= 2 and its coarser level");
+  olevel* F = &c->lev[level];
+  olevel* C = &c->lev[level - 1];
+  if (fabs(F->t_new - C->t_new) > 1e-12 * fmax(1.0, fabs(C->t_new)))
+    return fail(c, -2, "update: fine and coarse levels are not at the same time");
+  const int R = F->ratio_to_coarser;
+  /* For every coarse cell of every coarse patch: if all R x R children are
+   * interior cells of the fine level, replace the coarse value by their mean. */
+  for (int cp = 0; cp < C->npatch; ++cp) {
+    const oracle_patch_desc* cd = &C->desc[cp];
+    const size_t cplane = (size_t)(cd->mx + 4) * (cd->my + 4);
+    for (int lj = 0; lj < cd->my; ++lj)
+      for (int li = 0; li < cd->mx; ++li) {
+        const int64_t Ic = C->i0[cp] + li, Jc = C->j0[cp] + lj;
+        double v[MEQN] = {0.0, 0.0, 0.0};
+        int all = 1;
+        for (int b = 0; b < R && all; ++b)
+          for (int a = 0; a < R && all; ++a) {
+            const int64_t I = Ic * R + a, J = Jc * R + b;
+            const int fp = find_patch(F, I, J);
+            if (fp < 0) { all = 0; break; }
+            const oracle_patch_desc* fd = &F->desc[fp];
+            const size_t fplane = (size_t)(fd->mx + 4) * (fd->my + 4);
+            const int fi = (int)(I - F->i0[fp]), fj = (int)(J - F->j0[fp]);
+            for (int m = 0; m < MEQN; ++m)
+              v[m] = v[m] + F->qpad[fp][m * fplane + (size_t)(fj + 2) * (fd->mx + 4) + fi + 2];
+          }
+        if (!all) continue;
+        for (int m = 0; m < MEQN; ++m)
+          C->qpad[cp][m * cplane + (size_t)(lj + 2) * (cd->mx + 4) + li + 2] = v[m] / (double)(R * R);
+      }
+  }
+  return 0;
+}
+
 int oracle_read(const oracle_ctx* c, int level, int patch, double* q_out) {
   if (!c || level < 1 || level > MAXLEVEL || patch < 0 || patch >= c->lev[level].npatch) return -1;
   const olevel* L = &c->lev[level];

@@ -78,6 +78,12 @@ int oracle_fill_ghost(oracle_ctx* ctx, int level, double t);
  * stand; returns the level's max Courant number. */
 int oracle_advance_level(oracle_ctx* ctx, int level, double dt, double* cfl_max);
 
+/* Updating: every level-(level-1) cell whose R x R
+ * children are all interior cells of level `level` is overwritten by their
+ * mean (sum over children, rows then columns, divided by R*R; R16).
+ * Requires equal times (t_new) on both levels (else -2). */
+int oracle_update_level(oracle_ctx* ctx, int level);
+
 int oracle_read(const oracle_ctx* ctx, int level, int patch, double* q_out);
 int oracle_write(oracle_ctx* ctx, int level, int patch, const double* q_in);
 int oracle_read_padded(const oracle_ctx* ctx, int level, int patch, double* q_out);
