@@ -296,7 +296,8 @@ def main():
             g.fill_ghost(1, t)
             g.advance_level(1, dt)
         else:
-            g.advance_hierarchy(t, dt)   # native subcycled coarse step, one host sync
+            # native subcycled coarse step with updating, one host sync
+            g.advance_hierarchy(t, dt, update=True)
         t_sim[0] = t + dt
 
     for _ in range(max(args.warmup, 3) if args.warmup > 0 else 0):

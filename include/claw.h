@@ -161,13 +161,23 @@ int claw_owner(const claw_ctx* ctx, int32_t level, int32_t patch, int32_t* rank)
  * (see claw_config.path). */
 int claw_level_mode(const claw_ctx* ctx, int32_t level, int32_t* mode);
 
+/* Updating: every level-(level-1) cell whose R x R
+ * children are all interior cells of `level` is overwritten by their mean
+ * (children summed row by row, divided by R*R).  Both levels must be at the
+ * same time (else ESTATE).  Single rank. */
+int claw_update_level(claw_ctx* ctx, int32_t level);
+
+#define CLAW_HIER_UPDATE 1   /* claw_advance_hierarchy: average each finer level onto
+                                its coarser one when it has caught up */
+
 /* One coarse step of the whole hierarchy, level by level with subcycling
  * (P:113-118): level 1 advances by dt, then every finer level L+1 R_L times
  * with dt / prod(R), each level step preceded by its ghost fill at its own
- * time.  Runs entirely on the library's stream with one host synchronisation
- * at the end; *cfl_max receives the max Courant number over all level steps.
- * Ratios are taken from the levels' dx. */
-int claw_advance_hierarchy(claw_ctx* ctx, double t, double dt, double* cfl_max);
+ * time; with CLAW_HIER_UPDATE in flags, level L+1 is averaged onto level L
+ * after its R_L steps.  Runs entirely on the library's stream with one host
+ * synchronisation at the end; *cfl_max receives the max Courant number over
+ * all level steps.  Ratios are taken from the levels' dx. */
+int claw_advance_hierarchy(claw_ctx* ctx, double t, double dt, int32_t flags, double* cfl_max);
 int claw_level_owned(const claw_ctx* ctx, int32_t level, int32_t* npatch_owned,
                      int64_t* cells_owned, int64_t* device_bytes);
 

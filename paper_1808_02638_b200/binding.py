@@ -33,7 +33,9 @@ EXPORTS = [
     "claw_debug_halo_counts", "claw_debug_halo_send", "claw_set_profiling", "claw_get_stats",
     "claw_reset_stats", "claw_synchronize", "claw_nccl_unique_id", "claw_version",
     "claw_level_mode", "claw_advance_hierarchy", "claw_halo_pack", "claw_halo_unpack",
+    "claw_update_level",
 ]
+CLAW_HIER_UPDATE = 1
 
 
 class ClawError(RuntimeError):
@@ -101,7 +103,8 @@ def load() -> ctypes.CDLL:
     L.claw_synchronize.argtypes = [vp]
     L.claw_nccl_unique_id.argtypes = [vp]
     L.claw_level_mode.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_int32)]
-    L.claw_advance_hierarchy.argtypes = [vp, d, d, dp]
+    L.claw_advance_hierarchy.argtypes = [vp, d, d, i32, dp]
+    L.claw_update_level.argtypes = [vp, i32]
     L.claw_halo_pack.argtypes = [vp, i32, i32, dp]
     L.claw_halo_unpack.argtypes = [vp, i32, i32, dp]
     _lib = L
@@ -261,11 +264,17 @@ class Claw:
         self._check(load().claw_level_mode(self._h, level, ctypes.byref(m)))
         return "grid" if m.value == 1 else "generic"
 
-    def advance_hierarchy(self, t: float, dt: float) -> float:
-        """One coarse step of every level with subcycling, natively."""
+    def advance_hierarchy(self, t: float, dt: float, update: bool = False) -> float:
+        """One coarse step of every level with subcycling (and, with update,
+        fine->coarse averaging after each fine cycle), natively."""
         c = ctypes.c_double()
-        self._check(load().claw_advance_hierarchy(self._h, float(t), float(dt), ctypes.byref(c)))
+        self._check(load().claw_advance_hierarchy(self._h, float(t), float(dt),
+                                                  CLAW_HIER_UPDATE if update else 0, ctypes.byref(c)))
         return c.value
+
+    def update_level(self, level: int):
+        """Average `level` onto `level - 1` where fully covered."""
+        self._check(load().claw_update_level(self._h, level))
 
     def level_owned(self, level: int):
         n, c, b = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()

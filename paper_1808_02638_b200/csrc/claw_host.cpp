@@ -154,6 +154,10 @@ struct Level {
   int64_t Y0 = 0, Y1 = 0;  // this rank's band of level rows
   int64_t hoff[4] = {-1, -1, -1, -1};  // frame offset (column 0) of halo rows Y0-2, Y0-1, Y1, Y1+1; -1 local
   int64_t hcs[4] = {0, 0, 0, 0};       // their component strides
+  // updating table (this fine level onto level-1): covered coarse cells and
+  // their R*R children
+  std::vector<int64_t> hu_dst, hu_dcs, hu_src, hu_scs;
+  DevBuf<int64_t> du_dst, du_dcs, du_src, du_scs;
   int gen = 0;           // level CFL slot generation (lcfl[gen] is the last step's)
   unsigned long long* hier = nullptr;  // coarse-step slot while claw_advance_hierarchy runs
 
@@ -832,6 +836,46 @@ int plan_level(claw_ctx* c, int level, Level& L) {
   std::stable_sort(L.htile.begin(), L.htile.end(), [](const int4& a, const int4& b) {
     return (a.w & 0xffff) * (a.w >> 16) > (b.w & 0xffff) * (b.w >> 16);
   });
+  // updating table: coarse cells (level-1) whose R x R children are all
+  // interior cells of this level
+  L.hu_dst.clear();
+  L.hu_dcs.clear();
+  L.hu_src.clear();
+  L.hu_scs.clear();
+  if (C && world == 1) {
+    const int R = L.ratio;
+    std::vector<char> seen;
+    for (int fp = 0; fp < np; ++fp) {
+      const int64_t ic0 = L.i0[fp] / R, ic1 = (L.i0[fp] + L.desc[fp].mx - 1) / R;
+      const int64_t jc0 = L.j0[fp] / R, jc1 = (L.j0[fp] + L.desc[fp].my - 1) / R;
+      for (int64_t Jc = jc0; Jc <= jc1; ++Jc)
+        for (int64_t Ic = ic0; Ic <= ic1; ++Ic) {
+          const int cq = C->find(Ic, Jc);
+          if (cq < 0) continue;
+          // each coarse cell once: only from the fine patch holding its first child
+          if (L.find(Ic * R, Jc * R) != fp) continue;
+          bool all = true;
+          std::vector<int64_t> so, sc;
+          for (int b = 0; b < R && all; ++b)
+            for (int a = 0; a < R && all; ++a) {
+              const int q = L.find(Ic * R + a, Jc * R + b);
+              if (q < 0) {
+                all = false;
+                break;
+              }
+              const int lq = L.local[q];
+              so.push_back(L.off[lq] + (Jc * R + b - L.j0[q]) * L.desc[q].mx + (Ic * R + a - L.i0[q]));
+              sc.push_back(static_cast<int64_t>(L.desc[q].mx) * L.desc[q].my);
+            }
+          if (!all) continue;
+          const int lc = C->local[cq];
+          L.hu_dst.push_back(C->off[lc] + (Jc - C->j0[cq]) * C->desc[cq].mx + (Ic - C->i0[cq]));
+          L.hu_dcs.push_back(static_cast<int64_t>(C->desc[cq].mx) * C->desc[cq].my);
+          L.hu_src.insert(L.hu_src.end(), so.begin(), so.end());
+          L.hu_scs.insert(L.hu_scs.end(), sc.begin(), sc.end());
+        }
+    }
+  }
   return CLAW_OK;
 }
 
@@ -1045,6 +1089,10 @@ int claw_set_level(claw_ctx* ctx, int32_t level, int32_t npatch, const claw_patc
   if (int r2 = upload(ctx, L.drect, L.hrect)) return r2;
   if (int r2 = upload(ctx, L.dtile, L.htile)) return r2;
   if (int r2 = upload(ctx, L.dinterp, L.hinterp)) return r2;
+  if (int r2 = upload(ctx, L.du_dst, L.hu_dst)) return r2;
+  if (int r2 = upload(ctx, L.du_dcs, L.hu_dcs)) return r2;
+  if (int r2 = upload(ctx, L.du_src, L.hu_src)) return r2;
+  if (int r2 = upload(ctx, L.du_scs, L.hu_scs)) return r2;
   CUDA_TRY(L.pcfl.alloc(std::max<size_t>(L.owned.size(), 1)));
   CUDA_TRY(L.lcfl.alloc(2));
   CUDA_TRY(cudaMemset(L.pcfl.p, 0, L.pcfl.n * 8));
@@ -1338,21 +1386,42 @@ int claw_level_mode(const claw_ctx* ctx, int32_t level, int32_t* mode) {
   return CLAW_OK;
 }
 
+int claw_update_level(claw_ctx* ctx, int32_t level) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (level < 2 || level > kMaxLevel || !ctx->lev[level].set || !ctx->lev[level - 1].set)
+    return fail(ctx, CLAW_ESTATE, "update needs level %d and level %d set", level, level - 1);
+  if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
+  if (ctx->cfg.world > 1) return fail(ctx, CLAW_EINVAL, "updating is single-rank in this version");
+  Level& F = ctx->lev[level];
+  Level& C = ctx->lev[level - 1];
+  if (std::fabs(F.t_new - C.t_new) > 1e-12 * std::max(1.0, std::fabs(C.t_new)))
+    return fail(ctx, CLAW_ESTATE, "update: level %d (t=%.17g) has not caught up with level %d (t=%.17g)", level,
+                F.t_new, level - 1, C.t_new);
+  const int64_t n = static_cast<int64_t>(F.hu_dst.size());
+  CUDA_TRY(static_cast<cudaError_t>(claw::launch_update(C.q[C.cur].p, F.q[F.cur].p, F.du_dst.p, F.du_dcs.p,
+                                                        F.du_src.p, F.du_scs.p, n, F.ratio * F.ratio,
+                                                        ctx->stream)));
+  ctx->stats.ghost_launches++;
+  return CLAW_OK;
+}
+
 // Recursive subcycled advance without host synchronisation; every
 // step kernel also folds its Courant number into the coarse-step slot.
-static int advance_rec(claw_ctx* ctx, int level, double t, double dt, int nlev) {
+static int advance_rec(claw_ctx* ctx, int level, double t, double dt, int nlev, int flags) {
   if (int rc = claw_fill_ghost(ctx, level, t)) return rc;
   if (int rc = claw_advance_level_async(ctx, level, dt)) return rc;
   if (level < nlev) {
     const int R = ctx->lev[level + 1].ratio;
     const double dtf = dt / R;
     for (int k = 0; k < R; ++k)
-      if (int rc = advance_rec(ctx, level + 1, t + k * dtf, dtf, nlev)) return rc;
+      if (int rc = advance_rec(ctx, level + 1, t + k * dtf, dtf, nlev, flags)) return rc;
+    if (flags & CLAW_HIER_UPDATE)
+      if (int rc = claw_update_level(ctx, level + 1)) return rc;
   }
   return CLAW_OK;
 }
 
-int claw_advance_hierarchy(claw_ctx* ctx, double t, double dt, double* cfl_max) {
+int claw_advance_hierarchy(claw_ctx* ctx, double t, double dt, int32_t flags, double* cfl_max) {
   if (int rc = check_ctx(ctx)) return rc;
   if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
   if (!cfl_max) return fail(ctx, CLAW_EINVAL, "cfl_max is NULL");
@@ -1362,7 +1431,7 @@ int claw_advance_hierarchy(claw_ctx* ctx, double t, double dt, double* cfl_max) 
   if (!ctx->hier_buf.p) CUDA_TRY(ctx->hier_buf.alloc(1));
   CUDA_TRY(cudaMemsetAsync(ctx->hier_buf.p, 0, 8, ctx->stream));
   ctx->hier_slot = ctx->hier_buf.p;
-  const int rc = advance_rec(ctx, 1, t, dt, nlev);
+  const int rc = advance_rec(ctx, 1, t, dt, nlev, flags);
   ctx->hier_slot = nullptr;
   if (rc) return rc;
   if (ctx->cfg.world > 1 && ctx->cfg.exchange == 0) {

@@ -101,6 +101,8 @@ int launch_pack(const double* q, const int64_t* off, const int64_t* cs, int64_t 
                 double* out, void* stream);
 int launch_gather_padded(const double* q, const double* frame, const DevPatch* patches,
                          const DevRect* rects, int32_t patch, double* out, void* stream);
+int launch_update(double* q_coarse, const double* q_fine, const int64_t* dst, const int64_t* dcs,
+                  const int64_t* src, const int64_t* scs, int64_t n, int rr, void* stream);
 int max_tile_rows();
 int grid_strip();
 

@@ -247,7 +247,7 @@ def test_sampled_patches_at_full_c4_size_one_step():
         assert rel_err(q1[pj * 256 + pi], ref) <= TOL, (pi, pj)
 
 
-def run_hierarchy(wl, n_coarse, q0s, use_gpu):
+def run_hierarchy(wl, n_coarse, q0s, use_gpu, update=False):
     ratios = {L + 1: wl.levels[L + 1].ratio for L in range(len(wl.levels) - 1)}
     nlev = len(wl.levels)
     if use_gpu:
@@ -264,6 +264,8 @@ def run_hierarchy(wl, n_coarse, q0s, use_gpu):
             R = ratios[level]
             for k in range(R):
                 c = max(c, bo(level + 1, t + k * dt / R, dt / R))
+            if update:          # fine level caught up -> average onto coarse
+                h.update_level(level + 1)
         return c
 
     dt = wl.dt0()
@@ -370,3 +372,42 @@ def test_native_hierarchy_driver_equals_python_driver():
         g.close()
     assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
     assert out[0][2] == out[1][2]
+
+
+@pytest.mark.parametrize("name,steps", [("c2", 6), ("c3", 2)])
+def test_multilevel_with_updating(name, steps):
+    """Berger-Oliger with updating (NEXT-1): Python recursion on the GPU and
+    the native claw_advance_hierarchy(update) both match the oracle."""
+    wl = getattr(W, name)()
+    q0s = W.hierarchy_ic(wl)
+    qg, cg = run_hierarchy(wl, steps, q0s, True, update=True)
+    qo, co = run_hierarchy(wl, steps, q0s, False, update=True)
+    assert cg == co
+    for a, b in zip(qg, qo):
+        assert rel_err(a, b) <= TOL
+    g = binding.Claw(wl.domain, wl.bc, wl.limiter, wl.order_trans, device=0)
+    for L, (lv, q0) in enumerate(zip(wl.levels, q0s), start=1):
+        g.set_level(L, lv.descs, q0)
+    dt = wl.dt0()
+    cn = [g.advance_hierarchy(n * dt, dt, update=True) for n in range(steps)]
+    assert cn == cg
+    for L in range(1, len(wl.levels) + 1):
+        assert np.array_equal(g.read_level(L), qg[L - 1])
+
+
+def test_update_level_bitwise_and_state_checks():
+    wl = W.c2()
+    q0s = [W.random_ic(L.descs, 70 + k) for k, L in enumerate(wl.levels)]
+    g = binding.Claw(wl.domain, wl.bc, 4, 2, device=0)
+    o = oracle.Oracle(wl.domain, wl.bc, 4, 2)
+    for L, (lv, q0) in enumerate(zip(wl.levels, q0s), start=1):
+        g.set_level(L, lv.descs, q0)
+        o.set_level(L, lv.descs, q0)
+    g.update_level(2)
+    o.update_level(2)
+    assert np.array_equal(g.read_level(1), o.read_level(1))
+    g.fill_ghost(1, 0.0)
+    g.advance_level(1, wl.dt0())
+    with pytest.raises(binding.ClawError) as e:
+        g.update_level(2)             # level 2 has not caught up
+    assert e.value.code == binding.CLAW_ESTATE
