@@ -156,8 +156,10 @@ struct Level {
   int64_t hcs[4] = {0, 0, 0, 0};       // their component strides
   // updating table (this fine level onto level-1): covered coarse cells and
   // their R*R children
-  std::vector<int64_t> hu_dst, hu_dcs, hu_src, hu_scs;
-  DevBuf<int64_t> du_dst, du_dcs, du_src, du_scs;
+  std::vector<claw::DevUpdate> hu;
+  std::vector<int64_t> hu_src, hu_scs;   // slow entries: R*R (offset, cs) each
+  DevBuf<claw::DevUpdate> du;
+  DevBuf<int64_t> du_src, du_scs;
   int gen = 0;           // level CFL slot generation (lcfl[gen] is the last step's)
   unsigned long long* hier = nullptr;  // coarse-step slot while claw_advance_hierarchy runs
 
@@ -838,13 +840,11 @@ int plan_level(claw_ctx* c, int level, Level& L) {
   });
   // updating table: coarse cells (level-1) whose R x R children are all
   // interior cells of this level
-  L.hu_dst.clear();
-  L.hu_dcs.clear();
+  L.hu.clear();
   L.hu_src.clear();
   L.hu_scs.clear();
   if (C && world == 1) {
     const int R = L.ratio;
-    std::vector<char> seen;
     for (int fp = 0; fp < np; ++fp) {
       const int64_t ic0 = L.i0[fp] / R, ic1 = (L.i0[fp] + L.desc[fp].mx - 1) / R;
       const int64_t jc0 = L.j0[fp] / R, jc1 = (L.j0[fp] + L.desc[fp].my - 1) / R;
@@ -854,7 +854,7 @@ int plan_level(claw_ctx* c, int level, Level& L) {
           if (cq < 0) continue;
           // each coarse cell once: only from the fine patch holding its first child
           if (L.find(Ic * R, Jc * R) != fp) continue;
-          bool all = true;
+          bool all = true, one = true;
           std::vector<int64_t> so, sc;
           for (int b = 0; b < R && all; ++b)
             for (int a = 0; a < R && all; ++a) {
@@ -863,16 +863,28 @@ int plan_level(claw_ctx* c, int level, Level& L) {
                 all = false;
                 break;
               }
+              if (q != fp) one = false;
               const int lq = L.local[q];
               so.push_back(L.off[lq] + (Jc * R + b - L.j0[q]) * L.desc[q].mx + (Ic * R + a - L.i0[q]));
               sc.push_back(static_cast<int64_t>(L.desc[q].mx) * L.desc[q].my);
             }
           if (!all) continue;
           const int lc = C->local[cq];
-          L.hu_dst.push_back(C->off[lc] + (Jc - C->j0[cq]) * C->desc[cq].mx + (Ic - C->i0[cq]));
-          L.hu_dcs.push_back(static_cast<int64_t>(C->desc[cq].mx) * C->desc[cq].my);
-          L.hu_src.insert(L.hu_src.end(), so.begin(), so.end());
-          L.hu_scs.insert(L.hu_scs.end(), sc.begin(), sc.end());
+          claw::DevUpdate u{};
+          u.dst = C->off[lc] + (Jc - C->j0[cq]) * C->desc[cq].mx + (Ic - C->i0[cq]);
+          u.dcs = C->desc[cq].mx * C->desc[cq].my;
+          if (one) {
+            u.src = so[0];
+            u.fcs = L.desc[fp].mx * L.desc[fp].my;
+            u.fmx = L.desc[fp].mx;
+            u.slow = 0;
+          } else {
+            u.src = static_cast<int64_t>(L.hu_src.size()) / (R * R);
+            u.slow = 1;
+            L.hu_src.insert(L.hu_src.end(), so.begin(), so.end());
+            L.hu_scs.insert(L.hu_scs.end(), sc.begin(), sc.end());
+          }
+          L.hu.push_back(u);
         }
     }
   }
@@ -1089,8 +1101,7 @@ int claw_set_level(claw_ctx* ctx, int32_t level, int32_t npatch, const claw_patc
   if (int r2 = upload(ctx, L.drect, L.hrect)) return r2;
   if (int r2 = upload(ctx, L.dtile, L.htile)) return r2;
   if (int r2 = upload(ctx, L.dinterp, L.hinterp)) return r2;
-  if (int r2 = upload(ctx, L.du_dst, L.hu_dst)) return r2;
-  if (int r2 = upload(ctx, L.du_dcs, L.hu_dcs)) return r2;
+  if (int r2 = upload(ctx, L.du, L.hu)) return r2;
   if (int r2 = upload(ctx, L.du_src, L.hu_src)) return r2;
   if (int r2 = upload(ctx, L.du_scs, L.hu_scs)) return r2;
   CUDA_TRY(L.pcfl.alloc(std::max<size_t>(L.owned.size(), 1)));
@@ -1397,10 +1408,9 @@ int claw_update_level(claw_ctx* ctx, int32_t level) {
   if (std::fabs(F.t_new - C.t_new) > 1e-12 * std::max(1.0, std::fabs(C.t_new)))
     return fail(ctx, CLAW_ESTATE, "update: level %d (t=%.17g) has not caught up with level %d (t=%.17g)", level,
                 F.t_new, level - 1, C.t_new);
-  const int64_t n = static_cast<int64_t>(F.hu_dst.size());
-  CUDA_TRY(static_cast<cudaError_t>(claw::launch_update(C.q[C.cur].p, F.q[F.cur].p, F.du_dst.p, F.du_dcs.p,
-                                                        F.du_src.p, F.du_scs.p, n, F.ratio * F.ratio,
-                                                        ctx->stream)));
+  const int64_t n = static_cast<int64_t>(F.hu.size());
+  CUDA_TRY(static_cast<cudaError_t>(claw::launch_update(C.q[C.cur].p, F.q[F.cur].p, F.du.p, n, F.ratio,
+                                                        F.du_src.p, F.du_scs.p, ctx->stream)));
   ctx->stats.ghost_launches++;
   return CLAW_OK;
 }

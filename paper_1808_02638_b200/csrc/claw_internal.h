@@ -101,8 +101,18 @@ int launch_pack(const double* q, const int64_t* off, const int64_t* cs, int64_t 
                 double* out, void* stream);
 int launch_gather_padded(const double* q, const double* frame, const DevPatch* patches,
                          const DevRect* rects, int32_t patch, double* out, void* stream);
-int launch_update(double* q_coarse, const double* q_fine, const int64_t* dst, const int64_t* dcs,
-                  const int64_t* src, const int64_t* scs, int64_t n, int rr, void* stream);
+// Updating entry (one covered coarse cell).  Usual case: its R x R children
+// lie in one fine patch, child (a, b) at src + b*fmx + a.  Otherwise (slow),
+// src indexes R*R (offset, cs) pairs in the slow lists.
+struct DevUpdate {
+  int64_t dst;      // coarse offset (p component)
+  int64_t src;
+  int32_t dcs, fcs; // component strides (coarse, fine)
+  int32_t fmx, slow;
+};
+static_assert(sizeof(DevUpdate) == 32, "DevUpdate layout");
+int launch_update(double* q_coarse, const double* q_fine, const DevUpdate* tab, int64_t n, int R,
+                  const int64_t* slow_off, const int64_t* slow_cs, void* stream);
 int max_tile_rows();
 int grid_strip();
 

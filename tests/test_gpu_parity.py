@@ -411,3 +411,22 @@ def test_update_level_bitwise_and_state_checks():
     with pytest.raises(binding.ClawError) as e:
         g.update_level(2)             # level 2 has not caught up
     assert e.value.code == binding.CLAW_ESTATE
+
+
+def test_update_level_unaligned_fine_patches_bitwise():
+    """Fine patches whose edges split coarse cells: the coarse cells whose
+    children straddle two fine patches take the general (slow) path."""
+    dom = (0.0, 1.0, 0.0, 1.0)
+    cd = W.uniform_level(1, 1, 8, 8, dom)
+    boxes = [(3, 3, 5, 4), (8, 3, 4, 4), (3, 7, 9, 3)]
+    fd = np.concatenate([W.make_descs([a], [b], w, h, 1 / 16, 1 / 16, dom) for a, b, w, h in boxes])
+    qc, qf = W.random_ic(cd, 1), W.random_ic(fd, 2)
+    g = binding.Claw(dom, W.EXTRAP, 4, 2, device=0)
+    o = oracle.Oracle(dom, W.EXTRAP, 4, 2)
+    for h in (g, o):
+        h.set_level(1, cd, qc)
+        h.set_level(2, fd, qf)
+        h.update_level(2)
+    out = g.read_level(1)
+    assert np.array_equal(out, o.read_level(1))
+    assert not np.array_equal(out, qc)
