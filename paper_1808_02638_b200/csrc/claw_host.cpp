@@ -49,10 +49,16 @@ struct Nccl {
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   bool load(std::string& err) {
     if (h) return true;
+    // prefer the NCCL already in the process (torch's), else load one locally
+    // so it cannot interpose on another library's NCCL symbols
     const char* names[] = {"libnccl.so.2", "libnccl.so"};
     for (const char* n : names) {
-      h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      h = dlopen(n, RTLD_NOW | RTLD_NOLOAD);
       if (h) break;
+    }
+    for (const char* n : names) {
+      if (h) break;
+      h = dlopen(n, RTLD_NOW | RTLD_LOCAL);
     }
     if (!h) {
       err = "NCCL (libnccl.so.2) could not be loaded";
@@ -165,6 +171,9 @@ struct Level {
 
   int npx = 0;
   int64_t ngrid_tiles = 0;
+  int64_t ngrid_blocks = 0;   // row blocks of the band (grid mode)
+  int64_t ntile_interior = 0; // generic tiles [0, n) read no remote ghost cell
+  bool halo_pending = false;  // NCCL halo in flight on the comm stream
 
   int find(int64_t I, int64_t J) const {
     if (I < 0 || J < 0 || I >= nx || J >= ny) return -1;
@@ -194,6 +203,8 @@ struct claw_ctx {
   claw_stats stats{};
   int tile_rows = 64;
   unsigned long long* hier_slot = nullptr;  // set while claw_advance_hierarchy runs
+  cudaStream_t comm_stream = nullptr;       // world > 1: halo pack + NCCL send/recv
+  cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
   DevBuf<unsigned long long> hier_buf;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_free;  // event pool
 };
@@ -823,7 +834,8 @@ int plan_level(claw_ctx* c, int level, Level& L) {
       }
       const int th = std::min(L.th, my);
       const int64_t nstrip = (L.nx + claw::grid_strip() - 1) / claw::grid_strip();
-      L.ngrid_tiles = nstrip * ((L.Y1 - L.Y0) / my) * ((my + th - 1) / th);
+      L.ngrid_blocks = ((L.Y1 - L.Y0) / my) * ((my + th - 1) / th);
+      L.ngrid_tiles = nstrip * L.ngrid_blocks;
     }
   }
   L.htile.clear();
@@ -835,9 +847,22 @@ int plan_level(claw_ctx* c, int level, Level& L) {
         L.htile.push_back(make_int4(static_cast<int>(lp), i0, j0, tw | (th << 16)));
       }
   }
-  std::stable_sort(L.htile.begin(), L.htile.end(), [](const int4& a, const int4& b) {
+  // tiles of patches that read remote (other-rank) ghost cells go last, so a
+  // step can run the others while the halo is in flight
+  std::vector<char> remote(L.owned.size(), 0);
+  for (size_t lp = 0; lp < L.owned.size(); ++lp)
+    for (const int64_t code : L.dbg_src[lp])
+      if (code == -2) {
+        remote[lp] = 1;
+        break;
+      }
+  std::stable_sort(L.htile.begin(), L.htile.end(), [&](const int4& a, const int4& b) {
+    if (remote[a.x] != remote[b.x]) return remote[a.x] < remote[b.x];
     return (a.w & 0xffff) * (a.w >> 16) > (b.w & 0xffff) * (b.w >> 16);
   });
+  L.ntile_interior = 0;
+  while (L.ntile_interior < static_cast<int64_t>(L.htile.size()) && !remote[L.htile[L.ntile_interior].x])
+    ++L.ntile_interior;
   // updating table: coarse cells (level-1) whose R x R children are all
   // interior cells of this level
   L.hu.clear();
@@ -1021,6 +1046,11 @@ int claw_create(const claw_config* cfg, claw_ctx** out) {
     ctx->own_stream = true;
   }
   CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_cfl), sizeof(double)));
+  if (cfg->world > 1) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_ready, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_halo, cudaEventDisableTiming));
+  }
   if (cfg->world > 1 && cfg->exchange == 0) {
     if (!g_nccl.load(ctx->err)) {
       ctx->dead = true;
@@ -1057,6 +1087,9 @@ int claw_destroy(claw_ctx* ctx) {
   if (ctx->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(ctx->comm);
   if (ctx->h_cfl) cudaFreeHost(ctx->h_cfl);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+  if (ctx->ev_ready) cudaEventDestroy(ctx->ev_ready);
+  if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
   delete ctx;
   return CLAW_OK;
 }
@@ -1166,12 +1199,18 @@ int claw_fill_ghost(claw_ctx* ctx, int32_t level, double t) {
     ctx->stats.ghost_launches++;
   }
   if (ctx->cfg.world > 1 && ctx->cfg.exchange == 0) {
+    // halo on the comm stream: starts when q^n is complete on the main
+    // stream; claw_advance_level runs the interior tiles meanwhile and waits
+    // for it only before the edge tiles
     const int world = ctx->cfg.world;
+    cudaStream_t cst = ctx->comm_stream;
+    CUDA_TRY(cudaEventRecord(ctx->ev_ready, ctx->stream));
+    CUDA_TRY(cudaStreamWaitEvent(cst, ctx->ev_ready, 0));
     for (int r = 0; r < world; ++r) {
       const int64_t n = static_cast<int64_t>(L.send_off[r].size());
       if (n == 0) continue;
       CUDA_TRY(static_cast<cudaError_t>(claw::launch_pack(L.q[L.cur].p, L.dsend_off[r]->p, L.dsend_cs[r]->p, n,
-                                                          L.dsend_buf[r]->p, ctx->stream)));
+                                                          L.dsend_buf[r]->p, cst)));
       ctx->stats.ghost_launches++;
     }
     ncclResult_t nr = g_nccl.GroupStart();
@@ -1179,17 +1218,19 @@ int claw_fill_ghost(claw_ctx* ctx, int32_t level, double t) {
     for (int r = 0; r < world; ++r) {
       const size_t ns = L.send_off[r].size();
       if (ns) {
-        nr = g_nccl.Send(L.dsend_buf[r]->p, 3 * ns, ncclFloat64, r, ctx->comm, ctx->stream);
+        nr = g_nccl.Send(L.dsend_buf[r]->p, 3 * ns, ncclFloat64, r, ctx->comm, cst);
         if (nr != ncclSuccess) return nccl_fail(ctx, nr, "ncclSend");
         ctx->stats.halo_bytes_sent += static_cast<int64_t>(24 * ns);
       }
       if (L.nrecv[r]) {
-        nr = g_nccl.Recv(L.frame.p + L.recv_frame_off[r], 3 * L.nrecv[r], ncclFloat64, r, ctx->comm, ctx->stream);
+        nr = g_nccl.Recv(L.frame.p + L.recv_frame_off[r], 3 * L.nrecv[r], ncclFloat64, r, ctx->comm, cst);
         if (nr != ncclSuccess) return nccl_fail(ctx, nr, "ncclRecv");
       }
     }
     nr = g_nccl.GroupEnd();
     if (nr != ncclSuccess) return nccl_fail(ctx, nr, "ncclGroupEnd");
+    CUDA_TRY(cudaEventRecord(ctx->ev_halo, cst));
+    L.halo_pending = true;
   }
   record(ctx, ctx->ev_ghost, false);
   return CLAW_OK;
@@ -1219,6 +1260,9 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
   P.level_cfl = L.lcfl.p + g;
   P.level_cfl_reset = L.lcfl.p + (1 - g);
   P.hier_cfl = ctx->hier_slot;
+  P.blk_first = 0;
+  P.blk_stride = 1;
+  P.tile_offset = 0;
   P.uniform = (L.uniform && !L.hpatch.empty()) ? 1 : 0;
   if (P.uniform) fill_step_consts(L.hpatch[0], dt, ctx->cfg.limiter == 4 ? 2.0 : 1.0, ctx->cfg.order_trans, P.k);
   if (L.grid) {
@@ -1240,7 +1284,46 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
     }
   }
   record(ctx, ctx->ev_step, true);
-  CUDA_TRY(static_cast<cudaError_t>(claw::launch_step(P, ctx->stream)));
+  if (ctx->cfg.world > 1) {
+    // interior tiles (no remote ghost) first, then -- once the halo has
+    // landed -- the edge tiles
+    claw::StepParams Pi = P, Pe = P;
+    int64_t n_int = 0, n_all = 0;
+    if (L.grid) {
+      const int64_t nstrip = (L.nx + claw::grid_strip() - 1) / claw::grid_strip();
+      const int64_t nb = L.ngrid_blocks;
+      if (nb >= 3) {
+        Pi.blk_first = 1;
+        Pi.blk_stride = 1;
+        Pi.ntiles = static_cast<int32_t>(nstrip * (nb - 2));
+        Pe.blk_first = 0;
+        Pe.blk_stride = static_cast<int32_t>(nb - 1);
+        Pe.ntiles = static_cast<int32_t>(nstrip * 2);
+        n_int = 1;
+      }
+      n_all = 1;
+    } else {
+      Pi.tile_offset = 0;
+      Pi.ntiles = static_cast<int32_t>(L.ntile_interior);
+      Pe.tile_offset = static_cast<int32_t>(L.ntile_interior);
+      Pe.ntiles = static_cast<int32_t>(L.htile.size() - L.ntile_interior);
+      n_int = L.ntile_interior;
+      n_all = 1;
+    }
+    if (n_int > 0 && Pi.ntiles > 0) {
+      Pe.level_cfl_reset = nullptr;  // reset once (by the interior launch)
+      CUDA_TRY(static_cast<cudaError_t>(claw::launch_step(Pi, ctx->stream)));
+    } else {
+      Pe = P;                        // no split: one launch after the halo
+    }
+    if (L.halo_pending) {
+      CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo, 0));
+      L.halo_pending = false;
+    }
+    if (n_all && Pe.ntiles > 0) CUDA_TRY(static_cast<cudaError_t>(claw::launch_step(Pe, ctx->stream)));
+  } else {
+    CUDA_TRY(static_cast<cudaError_t>(claw::launch_step(P, ctx->stream)));
+  }
   record(ctx, ctx->ev_step, false);
   ctx->stats.step_launches++;
   ctx->stats.cells_advanced += L.cells_owned;

@@ -88,6 +88,9 @@ struct StepParams {
   int32_t th;                     // rows per tile (tiles stay in one patch row)
   int32_t per_x, per_y;           // periodic in x / y
   int32_t Y0, Y1;                 // this rank's band of level rows (whole level: 0, NY)
+  int32_t blk_first, blk_stride;  // grid tiles: row block = blk_first + k*blk_stride,
+                                  // k < ntiles / nstrip (interior / edge launches)
+  int32_t tile_offset;            // generic tiles: first tile index of this launch
   int64_t hoff[4];                // band halo rows Y0-2, Y0-1, Y1, Y1+1: frame offset of
   int64_t hcs[4];                 // column 0 (-1: the row is local) and component stride
 };
