@@ -1313,6 +1313,7 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
     if (n_int > 0 && Pi.ntiles > 0) {
       Pe.level_cfl_reset = nullptr;  // reset once (by the interior launch)
       CUDA_TRY(static_cast<cudaError_t>(claw::launch_step(Pi, ctx->stream)));
+      ctx->stats.step_launches++;
     } else {
       Pe = P;                        // no split: one launch after the halo
     }
@@ -1320,12 +1321,15 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
       CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo, 0));
       L.halo_pending = false;
     }
-    if (n_all && Pe.ntiles > 0) CUDA_TRY(static_cast<cudaError_t>(claw::launch_step(Pe, ctx->stream)));
+    if (n_all && Pe.ntiles > 0) {
+      CUDA_TRY(static_cast<cudaError_t>(claw::launch_step(Pe, ctx->stream)));
+      ctx->stats.step_launches++;
+    }
   } else {
     CUDA_TRY(static_cast<cudaError_t>(claw::launch_step(P, ctx->stream)));
+    ctx->stats.step_launches++;
   }
   record(ctx, ctx->ev_step, false);
-  ctx->stats.step_launches++;
   ctx->stats.cells_advanced += L.cells_owned;
   if (ctx->cfg.world > 1 && ctx->cfg.exchange == 0) {
     ncclResult_t nr = g_nccl.AllReduce(L.lcfl.p + g, L.lcfl.p + g, 1, ncclFloat64, ncclMax, ctx->comm, ctx->stream);
