@@ -71,6 +71,9 @@ def lib() -> ctypes.CDLL:
         L.oracle_patch_cfl.argtypes = [vp, ctypes.c_int, ctypes.c_int, dp]
         L.oracle_level_time.argtypes = [vp, ctypes.c_int, dp, dp]
         L.oracle_update_level.argtypes = [vp, ctypes.c_int]
+        L.oracle_set_reflux.argtypes = [vp, ctypes.c_int]
+        L.oracle_reflux_count.argtypes = [vp, ctypes.c_int]
+        L.oracle_reflux_read.argtypes = [vp, ctypes.c_int, vp, vp]
         L.oracle_step_patch.argtypes = [ctypes.c_int, ctypes.c_int, dp, ctypes.c_double,
                                         ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                         ctypes.c_double, ctypes.c_int, ctypes.c_int, dp, dp]
@@ -97,7 +100,7 @@ class Oracle:
     (create / set_level / fill_ghost / advance_level / read)."""
 
     def __init__(self, domain=(-1.0, 1.0, -1.0, 1.0), bc=(1, 1, 1, 1), limiter=4,
-                 order_trans=2, nthreads=0):
+                 order_trans=2, nthreads=0, reflux=False):
         cfg = _Config(*[float(v) for v in domain], (ctypes.c_int32 * 4)(*bc),
                       int(limiter), int(order_trans), int(nthreads))
         self._h = ctypes.c_void_p()
@@ -105,6 +108,8 @@ class Oracle:
         if rc != 0:
             raise OracleError(f"oracle_create failed ({rc})")
         self._descs = {}
+        if reflux:
+            self._check(lib().oracle_set_reflux(self._h, 1))
 
     def __del__(self):
         if getattr(self, "_h", None):
@@ -135,6 +140,17 @@ class Oracle:
     def update_level(self, level: int):
         """Average `level` onto `level - 1` where fully covered."""
         self._check(lib().oracle_update_level(self._h, level))
+
+    def reflux_registers(self, level: int):
+        """(edges [n, 8] int32, acc [n, 3]) of level `level`'s conservation-fix
+        registers (see oracle_reflux_read)."""
+        n = lib().oracle_reflux_count(self._h, level)
+        if n < 0:
+            raise OracleError("bad level")
+        e = np.zeros((n, 8), np.int32)
+        a = np.zeros((n, 3))
+        self._check(lib().oracle_reflux_read(self._h, level, e.ctypes.data, a.ctypes.data))
+        return e, a
 
     def read(self, level: int, patch: int) -> np.ndarray:
         d = self._descs[level][patch]

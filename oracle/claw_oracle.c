@@ -61,10 +61,21 @@ typedef struct {
   int64_t nbx, nby;
   int64_t* bstart; /* CSR offsets, nbx*nby+1 */
   int* blist;
+  /* conservation-fix registers of this (fine) level against level-1: one per
+   * coarse-fine edge E, i.e. a level-1 cell C not covered by this level whose
+   * edge neighbour (through periodic wrap) is covered.  E's fine side is the
+   * R cells of this level adjacent to E, starting at (rfi, rfj) in patch rfp
+   * and running along E. */
+  int nreg;
+  int *rcp, *rli, *rlj;   /* coarse patch, local cell of C */
+  int *rdir, *rside;      /* 0: x-edge, 1: y-edge; side 0: C left/below E, 1: C right/above */
+  int *rfp, *rfi, *rfj;   /* fine patch and local index of the first fine cell */
+  double* racc;           /* [nreg][3] accumulated modification of C */
 } olevel;
 
 struct oracle_ctx {
   oracle_config cfg;
+  int reflux;             /* conservation fix on (oracle_set_reflux) */
   olevel lev[MAXLEVEL + 1];
   char err[512];
 };
@@ -293,9 +304,13 @@ static void flux2(int ixy, int n, const double* q1d, double dtdx, double rho,
 /* ------------------------------------------------------------------------ */
 /* step2: one step of eq. (W) on one padded patch.                           */
 /* ------------------------------------------------------------------------ */
-int oracle_step_patch(int mx, int my, const double* qpad, double dx, double dy,
-                      double dt, double rho, double K, int limiter,
-                      int order_trans, double* qout_pad, double* cfl_out) {
+/* step2 proper.  If flux_out is not NULL it receives the four accumulated
+ * edge arrays fm, fp, gm, gp (each [3][my+4][mx+4], padded index = Clawpack
+ * index + 1; the caller frees them) -- the conservation fix reads the ones on
+ * coarse-fine interfaces ("can be saved ... for later use"). */
+static int step2(int mx, int my, const double* qpad, double dx, double dy,
+                 double dt, double rho, double K, int limiter, int order_trans,
+                 double* qout_pad, double* cfl_out, double** flux_out) {
   if (mx < 1 || my < 1 || !(dx > 0.0) || !(dy > 0.0) || !(rho > 0.0) || !(K > 0.0))
     return -1;
   const int PX = mx + 4, PY = my + 4;
@@ -364,7 +379,11 @@ int oracle_step_patch(int mx, int my, const double* qpad, double dx, double dy,
                       - dtdy * (GMA_(m, i, j + 1) - GPA_(m, i, j));
 
   *cfl_out = cfl;
-  free(fm); free(fp); free(gm); free(gp);
+  if (flux_out) {
+    flux_out[0] = fm; flux_out[1] = fp; flux_out[2] = gm; flux_out[3] = gp;
+  } else {
+    free(fm); free(fp); free(gm); free(gp);
+  }
   free(q1d); free(faddm); free(faddp); free(gadd);
   return 0;
 #undef QP
@@ -373,6 +392,12 @@ int oracle_step_patch(int mx, int my, const double* qpad, double dx, double dy,
 #undef FPA_
 #undef GMA_
 #undef GPA_
+}
+
+int oracle_step_patch(int mx, int my, const double* qpad, double dx, double dy,
+                      double dt, double rho, double K, int limiter,
+                      int order_trans, double* qout_pad, double* cfl_out) {
+  return step2(mx, my, qpad, dx, dy, dt, rho, K, limiter, order_trans, qout_pad, cfl_out, NULL);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -386,6 +411,8 @@ static void free_level(olevel* L) {
     for (int p = 0; p < L->npatch; ++p) free(L->qold[p]);
   free(L->qpad); free(L->qold); free(L->desc); free(L->i0); free(L->j0);
   free(L->pcfl); free(L->bstart); free(L->blist);
+  free(L->rcp); free(L->rli); free(L->rlj); free(L->rdir); free(L->rside);
+  free(L->rfp); free(L->rfi); free(L->rfj); free(L->racc);
   memset(L, 0, sizeof *L);
 }
 
@@ -425,6 +452,83 @@ static int find_patch(const olevel* L, int64_t I, int64_t J) {
       return p;
   }
   return -1;
+}
+
+/* Is level-(F-1) cell (Ic,Jc) covered, i.e. are all R x R children interior
+ * cells of level F?  (The updating rule of P:120-121.) */
+static int covered(const olevel* F, int R, int64_t Ic, int64_t Jc) {
+  for (int b = 0; b < R; ++b)
+    for (int a = 0; a < R; ++a)
+      if (find_patch(F, Ic * R + a, Jc * R + b) < 0) return 0;
+  return 1;
+}
+
+int oracle_set_reflux(oracle_ctx* c, int on) {
+  if (!c) return -1;
+  for (int l = 1; l <= MAXLEVEL; ++l)
+    if (c->lev[l].npatch) return fail(c, -2, "oracle_set_reflux must precede oracle_set_level");
+  c->reflux = on ? 1 : 0;
+  return 0;
+}
+
+/* Registers of fine level `level` (R17).  Needs the fine patches
+ * aligned to the coarse cells (so a coarse cell is covered entirely or not at
+ * all and every coarse-fine edge is a fine patch boundary). */
+static int build_registers(oracle_ctx* c, int level) {
+  olevel* F = &c->lev[level];
+  const olevel* C = &c->lev[level - 1];
+  const int R = F->ratio_to_coarser;
+  const int* bc = c->cfg.bc;
+  for (int p = 0; p < F->npatch; ++p)
+    if (F->i0[p] % R || F->j0[p] % R || F->desc[p].mx % R || F->desc[p].my % R)
+      return fail(c, -1, "conservation fix needs fine patches aligned to the coarse cells");
+  for (int pass = 0; pass < 2; ++pass) {
+    int n = 0;
+    for (int cp = 0; cp < C->npatch; ++cp) {
+      const oracle_patch_desc* cd = &C->desc[cp];
+      for (int lj = 0; lj < cd->my; ++lj)
+        for (int li = 0; li < cd->mx; ++li) {
+          const int64_t Ic = C->i0[cp] + li, Jc = C->j0[cp] + lj;
+          if (covered(F, R, Ic, Jc)) continue;
+          /* neighbours in the order x-, x+, y-, y+ */
+          for (int e = 0; e < 4; ++e) {
+            const int dir = e / 2, side = (e % 2 == 0) ? 1 : 0;  /* neighbour below/left: C is on the high side */
+            int64_t In = Ic + (dir == 0 ? (e % 2 ? 1 : -1) : 0);
+            int64_t Jn = Jc + (dir == 1 ? (e % 2 ? 1 : -1) : 0);
+            const int64_t n_ax = dir == 0 ? C->nx : C->ny;
+            const int64_t v = dir == 0 ? In : Jn;
+            if (v < 0 || v >= n_ax) {
+              if (bc[2 * dir] != 2) continue; /* physical boundary: no neighbour */
+              if (dir == 0) In = (In + C->nx) % C->nx; else Jn = (Jn + C->ny) % C->ny;
+            }
+            if (!covered(F, R, In, Jn)) continue;
+            if (pass == 1) {
+              /* first fine cell adjacent to E on the neighbour's side */
+              int64_t I, J;
+              if (dir == 0) { I = In * R + (side == 0 ? 0 : R - 1); J = Jc * R; }
+              else          { I = Ic * R; J = Jn * R + (side == 0 ? 0 : R - 1); }
+              const int fp = find_patch(F, I, J);
+              F->rcp[n] = cp; F->rli[n] = li; F->rlj[n] = lj;
+              F->rdir[n] = dir; F->rside[n] = side;
+              F->rfp[n] = fp;
+              F->rfi[n] = (int)(I - F->i0[fp]);
+              F->rfj[n] = (int)(J - F->j0[fp]);
+            }
+            ++n;
+          }
+        }
+    }
+    if (pass == 0) {
+      F->nreg = n;
+      const size_t k = (size_t)(n > 0 ? n : 1);
+      F->rcp = (int*)malloc(k * sizeof(int)); F->rli = (int*)malloc(k * sizeof(int));
+      F->rlj = (int*)malloc(k * sizeof(int)); F->rdir = (int*)malloc(k * sizeof(int));
+      F->rside = (int*)malloc(k * sizeof(int)); F->rfp = (int*)malloc(k * sizeof(int));
+      F->rfi = (int*)malloc(k * sizeof(int)); F->rfj = (int*)malloc(k * sizeof(int));
+      F->racc = (double*)calloc(k * MEQN, sizeof(double));
+    }
+  }
+  return 0;
 }
 
 int oracle_set_level(oracle_ctx* c, int level, int npatch,
@@ -520,6 +624,8 @@ int oracle_set_level(oracle_ctx* c, int level, int npatch,
     off += (size_t)MEQN * mx * my;
   }
   L->t_old = L->t_new = (level > 1) ? c->lev[level - 1].t_old : 0.0;
+  for (int l = level + 1; l <= MAXLEVEL; ++l) free_level(&c->lev[l]);
+  if (level > 1 && c->reflux) return build_registers(c, level);
   return 0;
 }
 
@@ -609,10 +715,88 @@ int oracle_fill_ghost(oracle_ctx* c, int level, double t) {
   return 0;
 }
 
+/* Edge-array entry (component m, Clawpack index i, j) of a patch's flux arrays. */
+static double edge(double* const* fl, int k, const oracle_patch_desc* d, int m, int i, int j) {
+  const size_t plane = (size_t)(d->mx + 4) * (d->my + 4);
+  return fl[k][m * plane + (size_t)(j + 1) * (d->mx + 4) + i + 1];
+}
+
+/* Coarse part of the registers of fine level `level` after level-1 advanced
+ * by dt with edge arrays cfl_[p] (Step A; terms eq:c2_3 and eq:c3_3).
+ * C left/below E: C's update used -dt/dx fm(E)  -> acc += dt/dx fm(E);
+ * C right/above E: C's update used +dt/dx fp(E) -> acc -= dt/dx fp(E). */
+static void reflux_coarse_part(oracle_ctx* c, int level, double dt, double** const* cfl_) {
+  olevel* F = &c->lev[level];
+  const olevel* C = &c->lev[level - 1];
+  for (int e = 0; e < F->nreg; ++e) {
+    const int cp = F->rcp[e], i = F->rli[e] + 1, j = F->rlj[e] + 1; /* Clawpack index of C */
+    const oracle_patch_desc* d = &C->desc[cp];
+    const double r = (F->rdir[e] == 0) ? dt / C->dx : dt / C->dy;
+    for (int m = 0; m < MEQN; ++m) {
+      double v;
+      if (F->rdir[e] == 0)
+        v = (F->rside[e] == 0) ? edge(cfl_[cp], 0, d, m, i + 1, j) : -edge(cfl_[cp], 1, d, m, i, j);
+      else
+        v = (F->rside[e] == 0) ? edge(cfl_[cp], 2, d, m, i, j + 1) : -edge(cfl_[cp], 3, d, m, i, j);
+      F->racc[e * MEQN + m] = F->racc[e * MEQN + m] + r * v;
+    }
+  }
+}
+
+/* Fine part after level `level` advanced by dt_f with edge arrays ffl[p]
+ * (Step B; terms eq:c1_1/c1_2, eq:c2_1/c2_2, eq:c3_1/c3_2).  For each
+ * of the R fine cells F along E, with fine state Qf at the start of this fine
+ * step and the coarse state Qc = Q_C^n at the start of the coarse step:
+ *   jump = A-dq + A+dq of the Riemann problem between Qc and Qf,
+ *          = f(right state) - f(left state);
+ *   C left/below E (F on the right): F's update used +dt_f/dx_f fp(e), so
+ *          acc -= (dt_f/dx_c)(1/R) (fp(e) + f(Qf) - f(Qc));
+ *   C right/above E (F on the left): acc += (dt_f/dx_c)(1/R) (fm(e) + f(Qf) - f(Qc)).
+ * (R17 derives these from "the coarse flux through E is replaced by
+ * the space-time average of the fine fluxes".) */
+static void reflux_fine_part(oracle_ctx* c, int level, double dt, double** const* ffl) {
+  olevel* F = &c->lev[level];
+  const olevel* C = &c->lev[level - 1];
+  const int R = F->ratio_to_coarser;
+  for (int e = 0; e < F->nreg; ++e) {
+    const int dir = F->rdir[e], side = F->rside[e];
+    const oracle_patch_desc* cd = &C->desc[F->rcp[e]];
+    const oracle_patch_desc* fd = &F->desc[F->rfp[e]];
+    const double w = ((dir == 0) ? dt / C->dx : dt / C->dy) / (double)R;
+    double qc[MEQN];
+    for (int m = 0; m < MEQN; ++m)
+      qc[m] = C->qold[F->rcp[e]][((size_t)m * cd->my + F->rlj[e]) * cd->mx + F->rli[e]];
+    for (int b = 0; b < R; ++b) {
+      const int fi = F->rfi[e] + (dir == 1 ? b : 0), fj = F->rfj[e] + (dir == 0 ? b : 0);
+      double qf[MEQN], wv[MWAVES * MEQN], sp[MWAVES], am[MEQN], ap[MEQN];
+      for (int m = 0; m < MEQN; ++m)
+        qf[m] = F->qold[F->rfp[e]][((size_t)m * fd->my + fj) * fd->mx + fi];
+      if (side == 0) oracle_rpn2(dir + 1, qc, qf, fd->rho, fd->K, wv, sp, am, ap);
+      else           oracle_rpn2(dir + 1, qf, qc, fd->rho, fd->K, wv, sp, am, ap);
+      const int i = fi + 1, j = fj + 1; /* Clawpack index of F */
+      for (int m = 0; m < MEQN; ++m) {
+        const double jump = am[m] + ap[m];
+        double v;
+        if (side == 0) {
+          const double fl = (dir == 0) ? edge(ffl[F->rfp[e]], 1, fd, m, i, j) : edge(ffl[F->rfp[e]], 3, fd, m, i, j);
+          v = -(fl + jump);
+        } else {
+          const double fl = (dir == 0) ? edge(ffl[F->rfp[e]], 0, fd, m, i + 1, j) : edge(ffl[F->rfp[e]], 2, fd, m, i, j + 1);
+          v = fl - jump;
+        }
+        F->racc[e * MEQN + m] = F->racc[e * MEQN + m] + w * v;
+      }
+    }
+  }
+}
+
 int oracle_advance_level(oracle_ctx* c, int level, double dt, double* cfl_max) {
   if (!c || level < 1 || level > MAXLEVEL || c->lev[level].npatch == 0)
     return fail(c, -2, "level not set");
   olevel* L = &c->lev[level];
+  const int fine_part = c->reflux && level > 1 && L->nreg > 0;
+  const int coarse_part = c->reflux && level < MAXLEVEL && c->lev[level + 1].nreg > 0;
+  double*** fl = (fine_part || coarse_part) ? (double***)calloc(L->npatch, sizeof(double**)) : NULL;
   int status = 0;
 #pragma omp parallel for schedule(dynamic, 1) num_threads(NTHREADS(c))
   for (int p = 0; p < L->npatch; ++p) {
@@ -621,8 +805,9 @@ int oracle_advance_level(oracle_ctx* c, int level, double dt, double* cfl_max) {
     const size_t plane = (size_t)(mx + 4) * (my + 4);
     double* qn = (double*)malloc(MEQN * plane * sizeof(double));
     double cfl = 0.0;
-    if (oracle_step_patch(mx, my, L->qpad[p], d->dx, d->dy, dt, d->rho, d->K,
-                          c->cfg.limiter, c->cfg.order_trans, qn, &cfl) != 0) {
+    if (fl) fl[p] = (double**)calloc(4, sizeof(double*));
+    if (step2(mx, my, L->qpad[p], d->dx, d->dy, dt, d->rho, d->K,
+              c->cfg.limiter, c->cfg.order_trans, qn, &cfl, fl ? fl[p] : NULL) != 0) {
 #pragma omp atomic write
       status = -1;
     }
@@ -634,6 +819,15 @@ int oracle_advance_level(oracle_ctx* c, int level, double dt, double* cfl_max) {
     memcpy(L->qpad[p], qn, MEQN * plane * sizeof(double));
     free(qn);
     L->pcfl[p] = cfl;
+  }
+  if (fl) {
+    if (!status && fine_part) reflux_fine_part(c, level, dt, (double** const*)fl);
+    if (!status && coarse_part) reflux_coarse_part(c, level + 1, dt, (double** const*)fl);
+    for (int p = 0; p < L->npatch; ++p) {
+      for (int k = 0; k < 4 && fl[p]; ++k) free(fl[p][k]);
+      free(fl[p]);
+    }
+    free(fl);
   }
   if (status) return fail(c, status, "step failed");
   double cmax = 0.0;
@@ -677,6 +871,39 @@ int oracle_update_level(oracle_ctx* c, int level) {
         for (int m = 0; m < MEQN; ++m)
           C->qpad[cp][m * cplane + (size_t)(lj + 2) * (cd->mx + 4) + li + 2] = v[m] / (double)(R * R);
       }
+  }
+  /* Conservation fix (Step 7 of the paper's flow chart): add each
+   * register to its coarse cell, then clear it for the next coarse step. */
+  if (c->reflux)
+    for (int e = 0; e < F->nreg; ++e) {
+      const int cp = F->rcp[e];
+      const oracle_patch_desc* cd = &C->desc[cp];
+      const size_t cplane = (size_t)(cd->mx + 4) * (cd->my + 4);
+      for (int m = 0; m < MEQN; ++m) {
+        double* q = &C->qpad[cp][m * cplane + (size_t)(F->rlj[e] + 2) * (cd->mx + 4) + F->rli[e] + 2];
+        *q = *q + F->racc[e * MEQN + m];
+        F->racc[e * MEQN + m] = 0.0;
+      }
+    }
+  return 0;
+}
+
+int oracle_reflux_count(const oracle_ctx* c, int level) {
+  if (!c || level < 2 || level > MAXLEVEL) return -1;
+  return c->lev[level].nreg;
+}
+
+int oracle_reflux_read(const oracle_ctx* c, int level, int32_t* edges, double* acc) {
+  if (!c || level < 2 || level > MAXLEVEL) return -1;
+  const olevel* F = &c->lev[level];
+  for (int e = 0; e < F->nreg; ++e) {
+    if (edges) {
+      int32_t* r = edges + 8 * e;
+      r[0] = F->rcp[e]; r[1] = F->rli[e]; r[2] = F->rlj[e]; r[3] = F->rdir[e];
+      r[4] = F->rside[e]; r[5] = F->rfp[e]; r[6] = F->rfi[e]; r[7] = F->rfj[e];
+    }
+    if (acc)
+      for (int m = 0; m < MEQN; ++m) acc[e * MEQN + m] = F->racc[e * MEQN + m];
   }
   return 0;
 }

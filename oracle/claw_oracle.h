@@ -81,8 +81,33 @@ int oracle_advance_level(oracle_ctx* ctx, int level, double dt, double* cfl_max)
 /* Updating: every level-(level-1) cell whose R x R
  * children are all interior cells of level `level` is overwritten by their
  * mean (sum over children, rows then columns, divided by R*R; R16).
- * Requires equal times (t_new) on both levels (else -2). */
+ * Requires equal times (t_new) on both levels (else -2).  With the
+ * conservation fix on, the registers of `level` are then applied (below).
+ * Setting a level discards every finer level. */
 int oracle_update_level(oracle_ctx* ctx, int level);
+
+/* Conservation fix (R17).  When on
+ * (call before the first oracle_set_level), every level L >= 2 keeps one
+ * register per coarse-fine edge E (a level L-1 cell C not covered by level L,
+ * sharing an edge -- through periodic wrap -- with a covered cell; fine
+ * patches must be aligned to the coarse cells, else set_level fails with -1):
+ *   - advancing level L-1 by dt adds the coarse flux through E that C's update
+ *     used (+dt/dx fm if C lies left/below E, -dt/dx fp otherwise);
+ *   - each advance of level L by dt_f subtracts (adds) the fine fluxes through
+ *     the R fine edges of E, (dt_f/dx_c)(1/R)(fp + A-dq + A+dq) with the
+ *     Riemann problem between Q_C^n and the fine cell (the paper's C1 + C2 +
+ *     C3 terms, eq:c123-eq:c3_3);
+ *   - oracle_update_level(L) then adds each register to its cell C and clears
+ *     it, so the level L-1 total equals the composite total.
+ * Protocol: Berger-Oliger order (level L-1 step, then its R level-L steps,
+ * then oracle_update_level(L)). */
+int oracle_set_reflux(oracle_ctx* ctx, int on);
+/* Number of registers of level L (>= 2), or -1. */
+int oracle_reflux_count(const oracle_ctx* ctx, int level);
+/* Registers of level L: edges[8e..8e+7] = coarse patch, C's local i, j,
+ * dir (0 x, 1 y), side (0: C left/below E), fine patch, first fine cell
+ * local i, j; acc[3e..3e+2] the accumulated values (either may be NULL). */
+int oracle_reflux_read(const oracle_ctx* ctx, int level, int32_t* edges, double* acc);
 
 int oracle_read(const oracle_ctx* ctx, int level, int patch, double* q_out);
 int oracle_write(oracle_ctx* ctx, int level, int patch, const double* q_in);
