@@ -83,7 +83,11 @@ typedef struct {
                                   claw_halo_unpack between claw_fill_ghost and
                                   claw_advance_level and reduces the CFL itself
                                   (tests and custom transports; no NCCL needed) */
-  int32_t reserved[5];
+  int32_t reflux;              /* 1: conservation fix at coarse-fine interfaces (P:122-123,
+                                  P:151-225; R17).  Fine patches
+                                  must be aligned to the coarser cells; single rank.
+                                  See claw_update_level. */
+  int32_t reserved[4];
 } claw_config;
 
 /* Kernel-level statistics, accumulated while profiling is on. */
@@ -166,6 +170,23 @@ int claw_level_mode(const claw_ctx* ctx, int32_t level, int32_t* mode);
  * (children summed row by row, divided by R*R).  Both levels must be at the
  * same time (else ESTATE).  Single rank. */
 int claw_update_level(claw_ctx* ctx, int32_t level);
+/* With claw_config.reflux = 1 the update is followed by the conservation fix
+ * (Step 7 of the paper's flow chart): every level-(level-1) cell C
+ * not covered by `level` that shares an edge E with a covered cell receives
+ * the register of E, which the steps have filled with
+ *   + dt/dx (fm or -fp through E as C's own update used it)   [coarse step]
+ *   - sum over the R fine edges of E and the fine sub-steps of
+ *     (dt_f/dx)/R (fp + f(Q_fine) - f(Q_C^n))  (mirror for C right/above E)
+ * -- the paper's C1 + C2 + C3 terms (eq:c123) with the coarse flux replaced
+ * by the space-time average of the fine fluxes -- and the register is
+ * cleared.  Call order: Berger-Oliger (level-1 step, its R level steps, then
+ * this call), as claw_advance_hierarchy does.
+ *
+ * Registers of fine level `level` (tests): *n = count; edges[8e..8e+7] =
+ * coarse patch, C's local i, j, dir (0 x, 1 y), side (0: C left/below E),
+ * fine patch, local i, j of the first fine cell along E (may be NULL);
+ * acc[3e..3e+2] = the accumulated values (device copy; may be NULL). */
+int claw_reflux_registers(claw_ctx* ctx, int32_t level, int64_t* n, int32_t* edges, double* acc);
 
 #define CLAW_HIER_UPDATE 1   /* claw_advance_hierarchy: average each finer level onto
                                 its coarser one when it has caught up */

@@ -33,7 +33,7 @@ EXPORTS = [
     "claw_debug_halo_counts", "claw_debug_halo_send", "claw_set_profiling", "claw_get_stats",
     "claw_reset_stats", "claw_synchronize", "claw_nccl_unique_id", "claw_version",
     "claw_level_mode", "claw_advance_hierarchy", "claw_halo_pack", "claw_halo_unpack",
-    "claw_update_level",
+    "claw_update_level", "claw_reflux_registers",
 ]
 CLAW_HIER_UPDATE = 1
 
@@ -52,7 +52,8 @@ class ClawConfig(ctypes.Structure):
                 ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
                 ("nccl_unique_id", ctypes.c_void_p), ("stream", ctypes.c_void_p),
                 ("tile_rows", ctypes.c_int32), ("path", ctypes.c_int32),
-                ("exchange", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
+                ("exchange", ctypes.c_int32), ("reflux", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 4)]
 
 
 class ClawStats(ctypes.Structure):
@@ -105,6 +106,7 @@ def load() -> ctypes.CDLL:
     L.claw_level_mode.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_int32)]
     L.claw_advance_hierarchy.argtypes = [vp, d, d, i32, dp]
     L.claw_update_level.argtypes = [vp, i32]
+    L.claw_reflux_registers.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_int64), vp, vp]
     L.claw_halo_pack.argtypes = [vp, i32, i32, dp]
     L.claw_halo_unpack.argtypes = [vp, i32, i32, dp]
     _lib = L
@@ -150,13 +152,14 @@ class Claw:
 
     def __init__(self, domain=(-1.0, 1.0, -1.0, 1.0), bc=(1, 1, 1, 1), limiter=4,
                  order_trans=2, device=0, rank=0, world=1, nccl_id: bytes | None = None,
-                 stream: int | None = None, tile_rows: int = 0, path: int = 0, exchange: int = 0):
+                 stream: int | None = None, tile_rows: int = 0, path: int = 0, exchange: int = 0,
+                 reflux: bool = False):
         L = load()
         self._idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None
         cfg = ClawConfig(*[float(v) for v in domain], (ctypes.c_int32 * 4)(*bc), int(limiter),
                          int(order_trans), int(device), int(rank), int(world),
                          ctypes.cast(self._idbuf, ctypes.c_void_p) if self._idbuf else None,
-                         stream, int(tile_rows), int(path), int(exchange))
+                         stream, int(tile_rows), int(path), int(exchange), int(bool(reflux)))
         self._h = ctypes.c_void_p()
         rc = L.claw_create(ctypes.byref(cfg), ctypes.byref(self._h))
         if rc:
@@ -273,8 +276,20 @@ class Claw:
         return c.value
 
     def update_level(self, level: int):
-        """Average `level` onto `level - 1` where fully covered."""
+        """Average `level` onto `level - 1` where fully covered (P:120-121);
+        with reflux on, then apply the conservation fix."""
         self._check(load().claw_update_level(self._h, level))
+
+    def reflux_registers(self, level: int, values: bool = True):
+        """(edges [n, 8] int32, acc [n, 3] or None): conservation-fix
+        registers of fine level `level` (see claw_reflux_registers)."""
+        n = ctypes.c_int64()
+        self._check(load().claw_reflux_registers(self._h, level, ctypes.byref(n), None, None))
+        e = np.zeros((n.value, 8), np.int32)
+        a = np.zeros((n.value, 3)) if values else None
+        self._check(load().claw_reflux_registers(self._h, level, ctypes.byref(n), e.ctypes.data,
+                                                 a.ctypes.data if values else None))
+        return e, a
 
     def level_owned(self, level: int):
         n, c, b = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()

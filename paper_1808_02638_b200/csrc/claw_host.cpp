@@ -166,6 +166,12 @@ struct Level {
   std::vector<int64_t> hu_src, hu_scs;   // slow entries: R*R (offset, cs) each
   DevBuf<claw::DevUpdate> du;
   DevBuf<int64_t> du_src, du_scs;
+  // conservation-fix registers of this fine level against level-1 (reflux on)
+  std::vector<claw::DevReflux> hreg;
+  std::vector<int32_t> hheads;           // first register of each coarse cell, + end
+  DevBuf<claw::DevReflux> dreg;
+  DevBuf<int32_t> dheads;
+  DevBuf<double> racc;                   // [nreg][3]
   int gen = 0;           // level CFL slot generation (lcfl[gen] is the last step's)
   unsigned long long* hier = nullptr;  // coarse-step slot while claw_advance_hierarchy runs
 
@@ -345,6 +351,9 @@ int validate_config(claw_ctx* c, const claw_config* cfg) {
   if (cfg->exchange != 0 && cfg->exchange != 1) return fail(c, CLAW_EINVAL, "exchange=%d: must be 0 or 1", cfg->exchange);
   if (cfg->world > 1 && cfg->exchange == 0 && !cfg->nccl_unique_id && cfg->device >= 0)
     return fail(c, CLAW_EINVAL, "world>1 needs nccl_unique_id");
+  if (cfg->reflux != 0 && cfg->reflux != 1) return fail(c, CLAW_EINVAL, "reflux=%d: must be 0 or 1", cfg->reflux);
+  if (cfg->reflux && cfg->world > 1)
+    return fail(c, CLAW_EINVAL, "reflux: the conservation fix is single-rank in this version (world=%d)", cfg->world);
   if (cfg->tile_rows < 0 || cfg->tile_rows > claw::max_tile_rows())
     return fail(c, CLAW_EINVAL, "tile_rows=%d: must be 0..%d", cfg->tile_rows, claw::max_tile_rows());
   return CLAW_OK;
@@ -913,6 +922,65 @@ int plan_level(claw_ctx* c, int level, Level& L) {
         }
     }
   }
+  // conservation-fix registers (same order as the oracle's: coarse patch, row,
+  // column, then neighbours x-, x+, y-, y+)
+  L.hreg.clear();
+  L.hheads.clear();
+  if (C && cfg.reflux) {
+    const int R = L.ratio;
+    for (int p = 0; p < np; ++p)
+      if (L.i0[p] % R || L.j0[p] % R || L.desc[p].mx % R || L.desc[p].my % R)
+        return fail(c, CLAW_EINVAL, "reflux: level %d patch %d is not aligned to the level-%d cells (R=%d)", level, p,
+                    level - 1, R);
+    auto covered = [&](int64_t Ic, int64_t Jc) {
+      for (int b = 0; b < R; ++b)
+        for (int a = 0; a < R; ++a)
+          if (L.find(Ic * R + a, Jc * R + b) < 0) return false;
+      return true;
+    };
+    for (int cq = 0; cq < C->npatch; ++cq) {
+      const int lc = C->local[cq];
+      for (int lj = 0; lj < C->desc[cq].my; ++lj)
+        for (int li = 0; li < C->desc[cq].mx; ++li) {
+          const int64_t Ic = C->i0[cq] + li, Jc = C->j0[cq] + lj;
+          if (covered(Ic, Jc)) continue;
+          bool head = true;
+          for (int e = 0; e < 4; ++e) {
+            const int dir = e / 2, side = (e % 2 == 0) ? 1 : 0;
+            int64_t In = Ic + (dir == 0 ? (e % 2 ? 1 : -1) : 0);
+            int64_t Jn = Jc + (dir == 1 ? (e % 2 ? 1 : -1) : 0);
+            const int64_t nax = dir == 0 ? C->nx : C->ny, v = dir == 0 ? In : Jn;
+            if (v < 0 || v >= nax) {
+              if (cfg.bc[2 * dir] != CLAW_BC_PERIODIC) continue;
+              if (dir == 0) In = (In + C->nx) % C->nx;
+              else Jn = (Jn + C->ny) % C->ny;
+            }
+            if (!covered(In, Jn)) continue;
+            int64_t I, J;
+            if (dir == 0) {
+              I = In * R + (side == 0 ? 0 : R - 1);
+              J = Jc * R;
+            } else {
+              I = Ic * R;
+              J = Jn * R + (side == 0 ? 0 : R - 1);
+            }
+            const int fq = L.find(I, J);
+            claw::DevReflux r{};
+            r.cp = lc;
+            r.ci = li;
+            r.cj = lj;
+            r.ds = dir | (side << 1);
+            r.fp = L.local[fq];
+            r.fi = static_cast<int32_t>(I - L.i0[fq]);
+            r.fj = static_cast<int32_t>(J - L.j0[fq]);
+            if (head) L.hheads.push_back(static_cast<int32_t>(L.hreg.size()));
+            head = false;
+            L.hreg.push_back(r);
+          }
+        }
+    }
+    L.hheads.push_back(static_cast<int32_t>(L.hreg.size()));
+  }
   return CLAW_OK;
 }
 
@@ -1137,6 +1205,10 @@ int claw_set_level(claw_ctx* ctx, int32_t level, int32_t npatch, const claw_patc
   if (int r2 = upload(ctx, L.du, L.hu)) return r2;
   if (int r2 = upload(ctx, L.du_src, L.hu_src)) return r2;
   if (int r2 = upload(ctx, L.du_scs, L.hu_scs)) return r2;
+  if (int r2 = upload(ctx, L.dreg, L.hreg)) return r2;
+  if (int r2 = upload(ctx, L.dheads, L.hheads)) return r2;
+  CUDA_TRY(L.racc.alloc(std::max<size_t>(3 * L.hreg.size(), 1)));
+  CUDA_TRY(cudaMemset(L.racc.p, 0, L.racc.n * 8));
   CUDA_TRY(L.pcfl.alloc(std::max<size_t>(L.owned.size(), 1)));
   CUDA_TRY(L.lcfl.alloc(2));
   CUDA_TRY(cudaMemset(L.pcfl.p, 0, L.pcfl.n * 8));
@@ -1331,6 +1403,24 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
   }
   record(ctx, ctx->ev_step, false);
   ctx->stats.cells_advanced += L.cells_owned;
+  if (ctx->cfg.reflux) {
+    // conservation fix: fine part of this level's registers (q^n of this level
+    // and of level-1, which advanced first), coarse part of level+1's
+    if (level > 1 && !L.hreg.empty()) {
+      const Level& C = ctx->lev[level - 1];
+      CUDA_TRY(static_cast<cudaError_t>(claw::launch_reflux(1, P, C.q[1 - C.cur].p, C.dpatch.p, L.dreg.p,
+                                                            static_cast<int64_t>(L.hreg.size()), L.ratio, L.racc.p,
+                                                            ctx->stream)));
+      ctx->stats.ghost_launches++;
+    }
+    if (level < kMaxLevel && ctx->lev[level + 1].set && !ctx->lev[level + 1].hreg.empty()) {
+      Level& F = ctx->lev[level + 1];
+      CUDA_TRY(static_cast<cudaError_t>(claw::launch_reflux(0, P, nullptr, nullptr, F.dreg.p,
+                                                            static_cast<int64_t>(F.hreg.size()), F.ratio, F.racc.p,
+                                                            ctx->stream)));
+      ctx->stats.ghost_launches++;
+    }
+  }
   if (ctx->cfg.world > 1 && ctx->cfg.exchange == 0) {
     ncclResult_t nr = g_nccl.AllReduce(L.lcfl.p + g, L.lcfl.p + g, 1, ncclFloat64, ncclMax, ctx->comm, ctx->stream);
     if (nr != ncclSuccess) return nccl_fail(ctx, nr, "ncclAllReduce(cfl, max)");
@@ -1499,6 +1589,40 @@ int claw_update_level(claw_ctx* ctx, int32_t level) {
   CUDA_TRY(static_cast<cudaError_t>(claw::launch_update(C.q[C.cur].p, F.q[F.cur].p, F.du.p, n, F.ratio,
                                                         F.du_src.p, F.du_scs.p, ctx->stream)));
   ctx->stats.ghost_launches++;
+  if (ctx->cfg.reflux && !F.hreg.empty()) {
+    CUDA_TRY(static_cast<cudaError_t>(claw::launch_reflux_apply(C.q[C.cur].p, C.dpatch.p, F.dreg.p, F.dheads.p,
+                                                                static_cast<int64_t>(F.hheads.size()) - 1, F.racc.p,
+                                                                ctx->stream)));
+    ctx->stats.ghost_launches++;
+  }
+  return CLAW_OK;
+}
+
+int claw_reflux_registers(claw_ctx* ctx, int32_t level, int64_t* n, int32_t* edges, double* acc) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (level < 2 || level > kMaxLevel || !ctx->lev[level].set) return fail(ctx, CLAW_ESTATE, "level %d is not set", level);
+  if (!n) return fail(ctx, CLAW_EINVAL, "n is NULL");
+  const Level& F = ctx->lev[level];
+  const Level& C = ctx->lev[level - 1];
+  *n = static_cast<int64_t>(F.hreg.size());
+  if (edges)
+    for (size_t e = 0; e < F.hreg.size(); ++e) {
+      const claw::DevReflux& r = F.hreg[e];
+      int32_t* o = edges + 8 * e;
+      o[0] = C.owned[r.cp];
+      o[1] = r.ci;
+      o[2] = r.cj;
+      o[3] = r.ds & 1;
+      o[4] = r.ds >> 1;
+      o[5] = F.owned[r.fp];
+      o[6] = r.fi;
+      o[7] = r.fj;
+    }
+  if (acc && !F.hreg.empty()) {
+    if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
+    CUDA_TRY(cudaMemcpyAsync(acc, F.racc.p, 3 * F.hreg.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  }
   return CLAW_OK;
 }
 

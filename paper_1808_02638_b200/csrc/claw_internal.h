@@ -116,6 +116,26 @@ struct DevUpdate {
 static_assert(sizeof(DevUpdate) == 32, "DevUpdate layout");
 int launch_update(double* q_coarse, const double* q_fine, const DevUpdate* tab, int64_t n, int R,
                   const int64_t* slow_off, const int64_t* slow_cs, void* stream);
+// Conservation-fix register of a fine level (NEXT-2, R17): coarse
+// cell C = (ci, cj) of owned coarse patch cp, not covered by the fine level,
+// sharing edge E (dir 0: x-edge, 1: y-edge) with a covered cell; side 0: C
+// lies left of / below E.  The R fine cells on the other side of E start at
+// (fi, fj) of owned fine patch fp and run along E.  Registers of one C are
+// consecutive (heads list).
+struct DevReflux {
+  int32_t cp, ci, cj;
+  int32_t ds;         // dir | side << 1
+  int32_t fp, fi, fj;
+  int32_t pad;
+};
+static_assert(sizeof(DevReflux) == 32, "DevReflux layout");
+// which 0: coarse part (p = the coarse level's step params with q = q^n);
+// which 1: fine part (p = the fine level's step params, qc = coarse q^n,
+// cpatches = coarse patch records).  acc: [n][3].
+int launch_reflux(int which, const StepParams& p, const double* qc, const DevPatch* cpatches,
+                  const DevReflux* tab, int64_t n, int R, double* acc, void* stream);
+int launch_reflux_apply(double* qc, const DevPatch* cpatches, const DevReflux* tab, const int32_t* heads,
+                        int64_t nheads, double* acc, void* stream);
 int max_tile_rows();
 int grid_strip();
 
