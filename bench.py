@@ -135,7 +135,7 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU oracle on a bounded sample (cpu_baseline / --impl reference)
 # ---------------------------------------------------------------------------
-def oracle_sample(wl: W.Workload, budget_s: float = 12.0, steps_cap: int | None = None):
+def oracle_sample(wl: W.Workload, budget_s: float = 12.0, steps_cap: int | None = None, reflux: bool = False):
     """Time the oracle as it stands on a sub-level of the same workload shape
     (same patch size, same scheme) for ~budget_s of CPU work.  Returns
     (cell-updates/s, cores, description)."""
@@ -156,7 +156,8 @@ def oracle_sample(wl: W.Workload, budget_s: float = 12.0, steps_cap: int | None 
         levels = [L.descs for L in wl.levels]
         desc = f"full {wl.name} hierarchy"
         q0 = None
-    o = oracle.Oracle(wl.domain if not uniform else dom, wl.bc, wl.limiter, wl.order_trans, nthreads=cores)
+    o = oracle.Oracle(wl.domain if not uniform else dom, wl.bc, wl.limiter, wl.order_trans, nthreads=cores,
+                      reflux=reflux and not uniform)
     if uniform:
         o.set_level(1, levels[0], q0)
         cells = int((levels[0]["mx"].astype(np.int64) * levels[0]["my"]).sum())
@@ -205,10 +206,11 @@ def run_reference(args, rank):
     desc = ""
     cores = host_cores()
     for _ in range(args.warmup):
-        oracle_sample(wl, budget_s=2.0, steps_cap=1)
+        oracle_sample(wl, budget_s=2.0, steps_cap=1, reflux=args.reflux)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        v, cores, desc = oracle_sample(wl, budget_s=max(1.0, 60.0 / max(args.steps, 1)), steps_cap=None)
+        v, cores, desc = oracle_sample(wl, budget_s=max(1.0, 60.0 / max(args.steps, 1)), steps_cap=None,
+                                       reflux=args.reflux)
         vals.append(v)
     el = time.perf_counter() - t0
     value = statistics.median(vals)
@@ -216,7 +218,8 @@ def run_reference(args, rank):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * el / max(args.steps, 1), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": wl.name, "note": wl.note},
+            "config": {"workload": wl.name, "note": wl.note,
+                       "conservation_fix": bool(args.reflux and len(wl.levels) > 1)},
             "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": cores, "kind": "oracle",
                              "sample": desc, "cpu": cpu_model()},
             "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -238,6 +241,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--tile-rows", type=int, default=0)
     ap.add_argument("--path", type=int, default=0, help="0 auto (grid kernel for uniform levels), 1 generic")
+    ap.add_argument("--reflux", action="store_true",
+                    help="multi-level configs: conservation fix at coarse-fine interfaces (NEXT-2)")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "host"],
                     help="host: TEST MODE -- halos through host memory over a gloo group "
                          "(claw exchange=1), ranks may share one GPU; never a bench number")
@@ -278,7 +283,7 @@ def main():
     stream = torch.cuda.current_stream()
     g = binding.Claw(wl.domain, wl.bc, wl.limiter, wl.order_trans, device=device, rank=rank,
                      world=world, nccl_id=nccl_id, stream=stream.cuda_stream, tile_rows=args.tile_rows,
-                     path=args.path, exchange=1 if host_x else 0)
+                     path=args.path, exchange=1 if host_x else 0, reflux=args.reflux and nlev > 1)
 
     # inputs: host-side synthetic data of the workload's shape, uploaded once
     # through the API; pinned so the e2e leg measures the real H2D path
@@ -428,7 +433,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle
         oracle.build()
-        v, cores, desc = oracle_sample(wl, budget_s=12.0)
+        v, cores, desc = oracle_sample(wl, budget_s=12.0, reflux=args.reflux)
         cpu = {"value": v, "unit": "cell-updates/s", "cores": cores, "kind": "oracle", "sample": desc,
                "cpu": cpu_model()}
 
@@ -445,6 +450,7 @@ def main():
                            "patches": int(sum(len(lv.descs) for lv in wl.levels)),
                            "cells_per_step": total_cells_per_step, "limiter": "MC", "order_trans": 2,
                            "cfl": wl.cfl, "ic": "ring (Clawpack acoustics_2d_radial qinit)",
+                           "conservation_fix": bool(args.reflux and nlev > 1),
                            "parallelism": f"patch-partitioned over {world} rank(s), NCCL halo + max all-reduce"
                            if world > 1 else "single GPU",
                            "l2": "state per buffer exceeds L2 (126 MB); no flush needed"
