@@ -72,6 +72,14 @@ def lib() -> ctypes.CDLL:
         L.oracle_level_time.argtypes = [vp, ctypes.c_int, dp, dp]
         L.oracle_update_level.argtypes = [vp, ctypes.c_int]
         L.oracle_set_reflux.argtypes = [vp, ctypes.c_int]
+        L.oracle_flag.argtypes = [vp, ctypes.c_int, ctypes.c_double, vp]
+        L.oracle_buffer_flags.argtypes = [vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, vp, vp]
+        L.oracle_buffer_flags.restype = None
+        L.oracle_cluster.argtypes = [vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_double, ctypes.c_int,
+                                     ctypes.c_int, vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+        L.oracle_regrid.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int]
+        L.oracle_level_count.argtypes = [vp, ctypes.c_int]
+        L.oracle_level_desc.argtypes = [vp, ctypes.c_int, vp]
         L.oracle_reflux_count.argtypes = [vp, ctypes.c_int]
         L.oracle_reflux_read.argtypes = [vp, ctypes.c_int, vp, vp]
         L.oracle_step_patch.argtypes = [ctypes.c_int, ctypes.c_int, dp, ctypes.c_double,
@@ -108,6 +116,7 @@ class Oracle:
         if rc != 0:
             raise OracleError(f"oracle_create failed ({rc})")
         self._descs = {}
+        self._dom = tuple(float(v) for v in domain)
         if reflux:
             self._check(lib().oracle_set_reflux(self._h, 1))
 
@@ -151,6 +160,35 @@ class Oracle:
         a = np.zeros((n, 3))
         self._check(lib().oracle_reflux_read(self._h, level, e.ctypes.data, a.ctypes.data))
         return e, a
+
+    def level_shape(self, level: int):
+        d = self.descs(level)
+        dx = float(d["dx"][0])
+        return (int(round((self._dom[1] - self._dom[0]) / dx)),
+                int(round((self._dom[3] - self._dom[2]) / float(d["dy"][0]))))
+
+    def descs(self, level: int) -> np.ndarray:
+        n = lib().oracle_level_count(self._h, level)
+        d = np.zeros(max(n, 0), ORACLE_PATCH_DTYPE)
+        if n > 0:
+            self._check(lib().oracle_level_desc(self._h, level, d.ctypes.data))
+        return d
+
+    def flag(self, level: int, tol: float) -> np.ndarray:
+        """Undivided-gradient flags of `level` over its index space [ny, nx] (uint8)."""
+        nx, ny = self.level_shape(level)
+        f = np.zeros((ny, nx), np.uint8)
+        self._check(lib().oracle_flag(self._h, level, float(tol), f.ctypes.data))
+        return f
+
+    def regrid(self, level: int, boxes, R: int):
+        """Replace level+1 by `boxes` ([n, 4] i0, j0, w, h in level index space) x R."""
+        b = np.ascontiguousarray(np.asarray(boxes, np.int32).reshape(-1, 4))
+        self._check(lib().oracle_regrid(self._h, level, len(b), b.ctypes.data, int(R)))
+        self._descs[level + 1] = self.descs(level + 1)
+        for l in list(self._descs):
+            if l > level + 1:
+                del self._descs[l]
 
     def read(self, level: int, patch: int) -> np.ndarray:
         d = self._descs[level][patch]
@@ -215,3 +253,29 @@ def rpt2(ixy, asdq, rho=1.0, K=1.0):
 
 def philim(limiter: int, r: float) -> float:
     return lib().oracle_philim(limiter, float(r))
+
+
+def buffer_flags(flags: np.ndarray, b: int, mask: np.ndarray | None = None) -> np.ndarray:
+    """Chebyshev dilation of a [ny, nx] uint8 flag map by b cells."""
+    f = np.ascontiguousarray(flags, np.uint8)
+    out = np.zeros_like(f)
+    m = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+    lib().oracle_buffer_flags(f.ctypes.data, f.shape[1], f.shape[0], int(b),
+                              None if m is None else m.ctypes.data, out.ctypes.data)
+    return out
+
+
+def cluster(flags: np.ndarray, cutoff: float, max_dim: int, min_dim: int) -> np.ndarray:
+    """Berger-Rigoutsos boxes [n, 4] = (i0, j0, w, h) of a [ny, nx] flag map."""
+    f = np.ascontiguousarray(flags, np.uint8)
+    n = ctypes.c_int()
+    rc = lib().oracle_cluster(f.ctypes.data, f.shape[1], f.shape[0], float(cutoff), int(max_dim),
+                              int(min_dim), None, 0, ctypes.byref(n))
+    if rc not in (0, -3):
+        raise OracleError(f"oracle_cluster rc={rc}")
+    b = np.zeros((max(n.value, 1), 4), np.int32)
+    rc = lib().oracle_cluster(f.ctypes.data, f.shape[1], f.shape[0], float(cutoff), int(max_dim),
+                              int(min_dim), b.ctypes.data, len(b), ctypes.byref(n))
+    if rc != 0:
+        raise OracleError(f"oracle_cluster rc={rc}")
+    return b[:n.value]

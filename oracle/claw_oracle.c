@@ -952,3 +952,260 @@ int oracle_level_time(const oracle_ctx* c, int level, double* t_old, double* t_n
   *t_new = c->lev[level].t_new;
   return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* Regridding (NEXT-3; R18)                  */
+/* ------------------------------------------------------------------------ */
+
+/* Flag every interior cell of `level` whose pressure differs from one of its
+ * four edge neighbours (composite values: the ghost frames as filled) by more
+ * than tol (undivided gradient of the first component; the paper
+ * allows "the gradient").  flags[J*nx + I] over the level's index
+ * space; cells outside the level's patches stay 0. */
+int oracle_flag(oracle_ctx* c, int level, double tol, uint8_t* flags) {
+  if (!c || level < 1 || level > MAXLEVEL || c->lev[level].npatch == 0 || !flags)
+    return fail(c, -2, "level not set");
+  const olevel* L = &c->lev[level];
+  memset(flags, 0, (size_t)(L->nx * L->ny));
+  for (int p = 0; p < L->npatch; ++p) {
+    const oracle_patch_desc* d = &L->desc[p];
+    const int PX = d->mx + 4;
+    const double* q = L->qpad[p];
+    for (int j = 1; j <= d->my; ++j)
+      for (int i = 1; i <= d->mx; ++i) {
+        const double pc = q[(size_t)(j + 1) * PX + i + 1];
+        const double pn[4] = {q[(size_t)(j + 1) * PX + i], q[(size_t)(j + 1) * PX + i + 2],
+                              q[(size_t)j * PX + i + 1], q[(size_t)(j + 2) * PX + i + 1]};
+        double g = 0.0;
+        for (int k = 0; k < 4; ++k) g = fmax(g, fabs(pn[k] - pc));
+        if (g > tol) flags[(L->j0[p] + j - 1) * L->nx + (L->i0[p] + i - 1)] = 1;
+      }
+  }
+  return 0;
+}
+
+/* Chebyshev dilation by b cells, clipped to [0,nx) x [0,ny) and,
+ * if mask is not NULL, to cells with mask != 0. */
+void oracle_buffer_flags(const uint8_t* in, int64_t nx, int64_t ny, int b, const uint8_t* mask,
+                         uint8_t* out) {
+  for (int64_t J = 0; J < ny; ++J)
+    for (int64_t I = 0; I < nx; ++I) {
+      uint8_t v = 0;
+      for (int64_t dj = -b; dj <= b && !v; ++dj)
+        for (int64_t di = -b; di <= b && !v; ++di) {
+          const int64_t a = I + di, bb = J + dj;
+          if (a >= 0 && a < nx && bb >= 0 && bb < ny && in[bb * nx + a]) v = 1;
+        }
+      if (mask && !mask[J * nx + I]) v = 0;
+      out[J * nx + I] = v;
+    }
+}
+
+/* Berger-Rigoutsos clustering (reading R18), recursive:
+ *   1. shrink the box to the bounding box of its flags (none: no box);
+ *   2. accept if efficiency = flags/area >= cutoff and both sides <= max_dim;
+ *   3. otherwise cut, trying in order
+ *        a. a zero of the column / row flag signature (a hole),
+ *        b. the strongest inflection of the signature's second difference
+ *           (largest |D2[k] - D2[k-1]| where D2 changes sign),
+ *        c. the middle of the longer side;
+ *      a cut at k splits [lo, k) | [k, hi) and must leave both parts at least
+ *      min_dim wide; for a and b the longer side is tried first, candidates
+ *      closest to the box centre win, ties to the lower index; if no cut is
+ *      allowed the box is accepted;
+ *   4. recurse on the low part, then the high part. */
+typedef struct { int32_t* out; int cap, n; const uint8_t* f; int64_t nx; double cutoff; int maxd, mind; } br_ctx;
+
+static void br_rec(br_ctx* B, int64_t x0, int64_t y0, int64_t x1, int64_t y1) {
+  /* 1. shrink */
+  int64_t a0 = x1, a1 = x0 - 1, b0 = y1, b1 = y0 - 1, nf = 0;
+  for (int64_t J = y0; J < y1; ++J)
+    for (int64_t I = x0; I < x1; ++I)
+      if (B->f[J * B->nx + I]) {
+        if (I < a0) a0 = I;
+        if (I > a1) a1 = I;
+        if (J < b0) b0 = J;
+        if (J > b1) b1 = J;
+        ++nf;
+      }
+  if (nf == 0) return;
+  x0 = a0; x1 = a1 + 1; y0 = b0; y1 = b1 + 1;
+  const int64_t w = x1 - x0, h = y1 - y0;
+  /* 2. accept */
+  if ((double)nf / (double)(w * h) >= B->cutoff && w <= B->maxd && h <= B->maxd) {
+    if (B->n < B->cap) {
+      B->out[4 * B->n + 0] = (int32_t)x0; B->out[4 * B->n + 1] = (int32_t)y0;
+      B->out[4 * B->n + 2] = (int32_t)w;  B->out[4 * B->n + 3] = (int32_t)h;
+    }
+    B->n++;
+    return;
+  }
+  /* signatures */
+  int64_t* sx = (int64_t*)calloc((size_t)w, sizeof(int64_t));
+  int64_t* sy = (int64_t*)calloc((size_t)h, sizeof(int64_t));
+  for (int64_t J = y0; J < y1; ++J)
+    for (int64_t I = x0; I < x1; ++I)
+      if (B->f[J * B->nx + I]) { sx[I - x0]++; sy[J - y0]++; }
+  int dirs[2];
+  if (w >= h) { dirs[0] = 0; dirs[1] = 1; } else { dirs[0] = 1; dirs[1] = 0; }
+  int cut_dir = -1;
+  int64_t cut = -1;
+  /* a. holes */
+  for (int t = 0; t < 2 && cut_dir < 0; ++t) {
+    const int d = dirs[t];
+    const int64_t n = d == 0 ? w : h;
+    const int64_t* sg = d == 0 ? sx : sy;
+    int64_t best = -1, bestdist = 0;
+    for (int64_t k = 1; k < n; ++k) {
+      if (sg[k] != 0) continue;
+      if (k < B->mind || n - k < B->mind) continue;
+      const int64_t dist = llabs(2 * k - n);  /* twice the distance of the cut from the centre */
+      if (best < 0 || dist < bestdist) { best = k; bestdist = dist; }
+    }
+    if (best >= 0) { cut_dir = d; cut = best; }
+  }
+  /* b. inflections: D2[k] = s[k-1] - 2 s[k] + s[k+1], k = 1..n-2; a sign
+   * change between D2[k-1] and D2[k] gives a cut at k (between cells k-1, k) */
+  if (cut_dir < 0) {
+    int64_t bestv = -1, bestdist = 0;
+    for (int t = 0; t < 2; ++t) {
+      const int d = dirs[t];
+      const int64_t n = d == 0 ? w : h;
+      const int64_t* sg = d == 0 ? sx : sy;
+      for (int64_t k = 2; k <= n - 2; ++k) {
+        const int64_t dp = sg[k - 2] - 2 * sg[k - 1] + sg[k];
+        const int64_t dc = sg[k - 1] - 2 * sg[k] + sg[k + 1];
+        if (!((dp < 0 && dc > 0) || (dp > 0 && dc < 0))) continue;
+        if (k < B->mind || n - k < B->mind) continue;
+        const int64_t v = llabs(dc - dp);
+        const int64_t dist = llabs(2 * k - n);
+        if (v > bestv || (v == bestv && dist < bestdist)) { bestv = v; bestdist = dist; cut_dir = d; cut = k; }
+      }
+    }
+  }
+  /* c. bisect the longer side */
+  if (cut_dir < 0) {
+    const int d = dirs[0];
+    const int64_t n = d == 0 ? w : h;
+    const int64_t k = n / 2;
+    if (k >= B->mind && n - k >= B->mind) { cut_dir = d; cut = k; }
+  }
+  free(sx);
+  free(sy);
+  if (cut_dir < 0) { /* no admissible cut: accept */
+    if (B->n < B->cap) {
+      B->out[4 * B->n + 0] = (int32_t)x0; B->out[4 * B->n + 1] = (int32_t)y0;
+      B->out[4 * B->n + 2] = (int32_t)w;  B->out[4 * B->n + 3] = (int32_t)h;
+    }
+    B->n++;
+    return;
+  }
+  if (cut_dir == 0) {
+    br_rec(B, x0, y0, x0 + cut, y1);
+    br_rec(B, x0 + cut, y0, x1, y1);
+  } else {
+    br_rec(B, x0, y0, x1, y0 + cut);
+    br_rec(B, x0, y0 + cut, x1, y1);
+  }
+}
+
+int oracle_cluster(const uint8_t* flags, int64_t nx, int64_t ny, double cutoff, int max_dim,
+                   int min_dim, int32_t* boxes, int cap, int* nbox) {
+  if (!flags || nx < 1 || ny < 1 || !(cutoff > 0.0) || cutoff > 1.0 || max_dim < 1 || min_dim < 1 ||
+      2 * min_dim > max_dim || !nbox)
+    return -1;
+  br_ctx B = {boxes, boxes ? cap : 0, 0, flags, nx, cutoff, max_dim, min_dim};
+  br_rec(&B, 0, 0, nx, ny);
+  *nbox = B.n;
+  return (boxes && B.n > cap) ? -3 : 0;
+}
+
+/* Replace level+1 by patches = boxes (in level-`level` index space) refined by
+ * R.  New fine cells take the value of the old level+1 cell at the same place
+ * if there is one ("copy from overlapping old same-level patches"), else
+ * the R10 interpolation from `level` at its current time (the ghost-fill
+ * formula with alpha = 1).  Levels finer than level+1 are discarded. */
+int oracle_regrid(oracle_ctx* c, int level, int nbox, const int32_t* boxes, int R) {
+  if (!c || level < 1 || level >= MAXLEVEL || c->lev[level].npatch == 0 || nbox < 0 || R < 1)
+    return fail(c, -1, "bad regrid arguments");
+  olevel* C = &c->lev[level];
+  olevel old = c->lev[level + 1];            /* take ownership of the old fine level */
+  memset(&c->lev[level + 1], 0, sizeof(olevel));
+  for (int l = level + 2; l <= MAXLEVEL; ++l) free_level(&c->lev[l]);
+  int rc = 0;
+  if (nbox > 0) {
+    const double dxf = C->dx / R, dyf = C->dy / R;
+    oracle_patch_desc* d = (oracle_patch_desc*)calloc((size_t)nbox, sizeof(oracle_patch_desc));
+    int64_t ncell = 0;
+    for (int b = 0; b < nbox; ++b) {
+      d[b].mx = boxes[4 * b + 2] * R;
+      d[b].my = boxes[4 * b + 3] * R;
+      d[b].dx = dxf;
+      d[b].dy = dyf;
+      d[b].xlower = c->cfg.xlo + (double)(boxes[4 * b + 0] * R) * dxf;
+      d[b].ylower = c->cfg.ylo + (double)(boxes[4 * b + 1] * R) * dyf;
+      d[b].mbc = 2;
+      d[b].rho = C->desc[0].rho;
+      d[b].K = C->desc[0].K;
+      ncell += (int64_t)d[b].mx * d[b].my;
+    }
+    double* q0 = (double*)calloc((size_t)(3 * ncell), sizeof(double));
+    const int* bc = c->cfg.bc;
+    int64_t off = 0;
+    for (int b = 0; b < nbox && !rc; ++b) {
+      const int64_t I0 = (int64_t)boxes[4 * b + 0] * R, J0 = (int64_t)boxes[4 * b + 1] * R;
+      for (int j = 0; j < d[b].my && !rc; ++j)
+        for (int i = 0; i < d[b].mx; ++i) {
+          const int64_t I = I0 + i, J = J0 + j;
+          double v[MEQN];
+          const int op = old.npatch ? find_patch(&old, I, J) : -1;
+          if (op >= 0) {
+            const oracle_patch_desc* od = &old.desc[op];
+            const size_t plane = (size_t)(od->mx + 4) * (od->my + 4);
+            for (int m = 0; m < MEQN; ++m)
+              v[m] = old.qpad[op][m * plane + (size_t)(J - old.j0[op] + 2) * (od->mx + 4) + (I - old.i0[op]) + 2];
+          } else {
+            const int64_t Ic = I / R, Jc = J / R;
+            double vc[MEQN], vxm[MEQN], vxp[MEQN], vym[MEQN], vyp[MEQN];
+            int ok = coarse_value(C, Ic, Jc, 1.0, vc);
+            ok &= coarse_value(C, map_axis(Ic - 1, C->nx, bc[0], bc[1]), Jc, 1.0, vxm);
+            ok &= coarse_value(C, map_axis(Ic + 1, C->nx, bc[0], bc[1]), Jc, 1.0, vxp);
+            ok &= coarse_value(C, Ic, map_axis(Jc - 1, C->ny, bc[2], bc[3]), 1.0, vym);
+            ok &= coarse_value(C, Ic, map_axis(Jc + 1, C->ny, bc[2], bc[3]), 1.0, vyp);
+            if (!ok) { rc = fail(c, -6, "regrid: new fine cell not nested in level"); break; }
+            const double xi = ((double)(I % R) + 0.5) / (double)R - 0.5;
+            const double eta = ((double)(J % R) + 0.5) / (double)R - 0.5;
+            for (int m = 0; m < MEQN; ++m) {
+              double sx = 0.0, sy = 0.0;
+              const double dxp = vxp[m] - vc[m], dxm = vc[m] - vxm[m];
+              const double dyp = vyp[m] - vc[m], dym = vc[m] - vym[m];
+              if (dxp * dxm > 0.0) sx = (dxp > 0.0 ? 1.0 : -1.0) * fmin(fabs(dxp), fabs(dxm));
+              if (dyp * dym > 0.0) sy = (dyp > 0.0 ? 1.0 : -1.0) * fmin(fabs(dyp), fabs(dym));
+              v[m] = vc[m] + sx * xi + sy * eta;
+            }
+          }
+          for (int m = 0; m < MEQN; ++m) q0[off + ((int64_t)m * d[b].my + j) * d[b].mx + i] = v[m];
+        }
+      off += 3 * (int64_t)d[b].mx * d[b].my;
+    }
+    if (!rc) rc = oracle_set_level(c, level + 1, nbox, d, q0);
+    free(q0);
+    free(d);
+  }
+  free_level(&old);
+  if (!rc && nbox > 0) {
+    c->lev[level + 1].t_old = c->lev[level + 1].t_new = C->t_new;
+  }
+  return rc;
+}
+
+int oracle_level_count(const oracle_ctx* c, int level) {
+  if (!c || level < 1 || level > MAXLEVEL) return -1;
+  return c->lev[level].npatch;
+}
+
+int oracle_level_desc(const oracle_ctx* c, int level, oracle_patch_desc* out) {
+  if (!c || level < 1 || level > MAXLEVEL || !out) return -1;
+  memcpy(out, c->lev[level].desc, sizeof(oracle_patch_desc) * (size_t)c->lev[level].npatch);
+  return 0;
+}

@@ -122,6 +122,28 @@ int oracle_step_patch(int mx, int my, const double* qpad, double dx, double dy,
                       double dt, double rho, double K, int limiter,
                       int order_trans, double* qout_pad, double* cfl);
 
+/* Regridding (NEXT-3; "every K time steps ... regenerated", "cells
+ * are flagged ... clustered into new rectangular grid patches"; S:219-290;
+ * DESIGN.md R18).
+ * oracle_flag: flags[J*nx + I] = 1 iff interior cell (I,J) of `level` has a
+ *   pressure jump > tol to one of its 4 edge neighbours (ghost frames as
+ *   filled by oracle_fill_ghost).
+ * oracle_buffer_flags: Chebyshev dilation by b, clipped to the index space
+ *   and (mask != NULL) to mask.
+ * oracle_cluster: Berger-Rigoutsos boxes (i0, j0, w, h) covering every flag
+ *   exactly once; -3 if more than cap boxes (nbox still set).
+ * oracle_regrid: replace level+1 by the boxes refined by R; data copied from
+ *   the old level+1 where it overlaps, else interpolated from `level` (R10
+ *   at alpha = 1); finer levels are discarded; -6 if a box is not on `level`. */
+int oracle_flag(oracle_ctx* ctx, int level, double tol, uint8_t* flags);
+void oracle_buffer_flags(const uint8_t* in, int64_t nx, int64_t ny, int b, const uint8_t* mask,
+                         uint8_t* out);
+int oracle_cluster(const uint8_t* flags, int64_t nx, int64_t ny, double cutoff, int max_dim,
+                   int min_dim, int32_t* boxes, int cap, int* nbox);
+int oracle_regrid(oracle_ctx* ctx, int level, int nbox, const int32_t* boxes, int R);
+int oracle_level_count(const oracle_ctx* ctx, int level);
+int oracle_level_desc(const oracle_ctx* ctx, int level, oracle_patch_desc* out);
+
 /* Riemann solvers and limiter function exposed for the pins.
  * ixy = 1 (x) or 2 (y).  ql, qr: 3-vectors.  wave: [2][3], s: [2]. */
 void oracle_rpn2(int ixy, const double* ql, const double* qr, double rho,
