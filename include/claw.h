@@ -202,6 +202,64 @@ int claw_advance_hierarchy(claw_ctx* ctx, double t, double dt, int32_t flags, do
 int claw_level_owned(const claw_ctx* ctx, int32_t level, int32_t* npatch_owned,
                      int64_t* cells_owned, int64_t* device_bytes);
 
+/* ---- Regridding ("every K time steps ... cells are flagged for
+ * refinement ... clustered into new rectangular grid patches"; S:219-290;
+ * DESIGN.md R18).  Single rank.  Levels are described on their own index
+ * space [0,nx) x [0,ny) (nx = domain width / dx); maps are [ny][nx] uint8,
+ * x fastest. ---- */
+
+/* Index-space extent of a set level. */
+int claw_level_extent(const claw_ctx* ctx, int32_t level, int64_t* nx, int64_t* ny);
+/* Number of patches of `level` (0 if unset) and their descriptors (the
+ * level's current patch list, e.g. after claw_regrid). */
+int claw_level_count(const claw_ctx* ctx, int32_t level, int32_t* npatch);
+int claw_level_descs(const claw_ctx* ctx, int32_t level, claw_patch_desc* out);
+
+/* Flag cells of `level` on the device.  A cell is flagged when its pressure
+ * differs from one of its four edge neighbours by more than tol (undivided
+ * gradient; neighbours are the composite values the step kernel reads
+ * -- call claw_fill_ghost(level, t) first for coarse-interpolated ghosts).
+ * The flags are then dilated by `buffer` cells in the Chebyshev metric
+ * (S:243-250), clipped to the index space and to
+ *   clip 0: nothing more; clip 1: the level's own cells; clip 2: the nesting
+ *   mask -- level cells whose in-domain neighbours within Chebyshev distance 2
+ *   all belong to the level (a fine box inside it has coarse donors for its
+ *   interpolation and its ghost frame).
+ * flags_out: host [ny][nx] (may be NULL); *nflag: set cells (may be NULL). */
+int claw_flag(claw_ctx* ctx, int32_t level, double tol, int32_t buffer, int32_t clip,
+              uint8_t* flags_out, int64_t* nflag);
+
+/* Berger-Rigoutsos clustering of a host flag map (host-only, no context):
+ * boxes[4k..4k+3] = (i0, j0, w, h) cover every flag exactly once.  Rules
+ * (R18): shrink to the flags' bounding box; accept when the
+ * efficiency flags/area >= cutoff and w, h <= max_dim; else cut at a hole of
+ * the row/column signature, else at the strongest inflection of its second
+ * difference, else at the middle of the longer side, each cut leaving >=
+ * min_dim cells on both sides (none possible: accept).  EINVAL unless
+ * 0 < cutoff <= 1, max_dim >= 2 min_dim >= 2.  *nbox is always set; ENOMEM
+ * (boxes untouched past cap) if more than cap boxes. */
+int claw_cluster(const uint8_t* flags, int64_t nx, int64_t ny, double cutoff, int32_t max_dim,
+                 int32_t min_dim, int32_t* boxes, int32_t cap, int32_t* nbox);
+
+/* Replace level+1 by the boxes (in level's index space) refined by R
+ * (P:110-111).  A new fine cell takes the value of the old level+1 cell at
+ * the same place if there is one, else the R10 coarse interpolation
+ * from `level` at its current time (the ghost-fill formula with alpha = 1).
+ * Levels finer than level+1 are discarded; nbox = 0 just removes them.  The
+ * new level's time is level's t_new.  EINVAL: box outside the index space or
+ * overlapping another; ENEST: a cell to interpolate has no coarse donor, or a
+ * ghost cell of the new level none.  Device memory comes from the library's
+ * caching pool (no cudaMalloc when a similar level was freed before). */
+int claw_regrid(claw_ctx* ctx, int32_t level, int32_t nbox, const int32_t* boxes, int32_t R);
+
+/* The whole regrid of level+1 in one call: claw_flag(level, tol, buffer,
+ * clip 2) on the device, the flag map to the host, claw_cluster, each box
+ * split into the row-run rectangles of the nesting mask (identical runs of
+ * consecutive rows merged; pieces without flags dropped), then claw_regrid.
+ * *nbox receives the number of new patches (may be NULL). */
+int claw_regrid_auto(claw_ctx* ctx, int32_t level, double tol, int32_t buffer, double cutoff,
+                     int32_t max_dim, int32_t min_dim, int32_t R, int32_t* nbox);
+
 /* Host-only introspection of the ghost-source tables (works with device=-1):
  * for every cell of the padded frame of `patch`, out[(j+2)*(mx+4)+(i+2)]
  * receives the global patch index whose interior supplies the value
@@ -224,6 +282,15 @@ int claw_debug_halo_counts(const claw_ctx* ctx, int32_t level, int32_t peer,
 /* The k-th cell sent to `peer`: global donor patch and local (i, j). */
 int claw_debug_halo_send(const claw_ctx* ctx, int32_t level, int32_t peer,
                          int64_t k, int32_t* patch, int32_t* i, int32_t* j);
+
+/* The process-wide device memory pool every context allocates from (the
+ * paper's GPU memory pool): requests served from cached blocks
+ * (hits) or cudaMalloc (misses), and the bytes cached for reuse.  Released
+ * blocks are cached per device and size class up to CLAW_POOL_LIMIT_MB
+ * (environment, default 16384).  claw_pool_trim returns every cached block
+ * to the driver (call with no kernel of the library in flight). */
+int claw_pool_stats(int64_t* hits, int64_t* misses, int64_t* cached_bytes);
+int claw_pool_trim(void);
 
 int claw_set_profiling(claw_ctx* ctx, int32_t on);
 int claw_get_stats(claw_ctx* ctx, claw_stats* out);   /* synchronises */

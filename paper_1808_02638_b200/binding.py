@@ -33,7 +33,9 @@ EXPORTS = [
     "claw_debug_halo_counts", "claw_debug_halo_send", "claw_set_profiling", "claw_get_stats",
     "claw_reset_stats", "claw_synchronize", "claw_nccl_unique_id", "claw_version",
     "claw_level_mode", "claw_advance_hierarchy", "claw_halo_pack", "claw_halo_unpack",
-    "claw_update_level", "claw_reflux_registers",
+    "claw_update_level", "claw_reflux_registers", "claw_level_extent", "claw_level_count",
+    "claw_level_descs", "claw_flag", "claw_cluster", "claw_regrid", "claw_regrid_auto",
+    "claw_pool_stats", "claw_pool_trim",
 ]
 CLAW_HIER_UPDATE = 1
 
@@ -107,6 +109,15 @@ def load() -> ctypes.CDLL:
     L.claw_advance_hierarchy.argtypes = [vp, d, d, i32, dp]
     L.claw_update_level.argtypes = [vp, i32]
     L.claw_reflux_registers.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_int64), vp, vp]
+    L.claw_level_extent.argtypes = [vp, i32, i64, i64]
+    L.claw_level_count.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_int32)]
+    L.claw_level_descs.argtypes = [vp, i32, vp]
+    L.claw_flag.argtypes = [vp, i32, d, i32, i32, vp, i64]
+    L.claw_cluster.argtypes = [vp, ctypes.c_int64, ctypes.c_int64, d, i32, i32, vp, i32,
+                               ctypes.POINTER(ctypes.c_int32)]
+    L.claw_regrid.argtypes = [vp, i32, i32, vp, i32]
+    L.claw_regrid_auto.argtypes = [vp, i32, d, i32, d, i32, i32, i32, ctypes.POINTER(ctypes.c_int32)]
+    L.claw_pool_stats.argtypes = [i64, i64, i64]
     L.claw_halo_pack.argtypes = [vp, i32, i32, dp]
     L.claw_halo_unpack.argtypes = [vp, i32, i32, dp]
     _lib = L
@@ -141,6 +152,30 @@ def nccl_unique_id() -> bytes:
     if rc:
         raise ClawError(rc, "NCCL unique id")
     return buf.raw
+
+
+def cluster(flags: np.ndarray, cutoff: float, max_dim: int, min_dim: int) -> np.ndarray:
+    """Berger-Rigoutsos boxes [n, 4] = (i0, j0, w, h) of a [ny, nx] flag map
+    (claw_cluster; host-only)."""
+    f = np.ascontiguousarray(flags, np.uint8)
+    n = ctypes.c_int32()
+    L = load()
+    rc = L.claw_cluster(f.ctypes.data, f.shape[1], f.shape[0], float(cutoff), int(max_dim), int(min_dim),
+                        None, 0, ctypes.byref(n))
+    if rc:
+        raise ClawError(rc, "claw_cluster: bad arguments")
+    out = np.zeros((n.value, 4), np.int32)
+    rc = L.claw_cluster(f.ctypes.data, f.shape[1], f.shape[0], float(cutoff), int(max_dim), int(min_dim),
+                        out.ctypes.data, n.value, ctypes.byref(n))
+    if rc:
+        raise ClawError(rc, "claw_cluster failed")
+    return out
+
+
+def pool_stats() -> dict:
+    h, m, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    load().claw_pool_stats(ctypes.byref(h), ctypes.byref(m), ctypes.byref(c))
+    return {"hits": h.value, "misses": m.value, "cached_bytes": c.value}
 
 
 def version() -> str:
@@ -295,6 +330,52 @@ class Claw:
         n, c, b = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()
         self._check(load().claw_level_owned(self._h, level, ctypes.byref(n), ctypes.byref(c), ctypes.byref(b)))
         return n.value, c.value, b.value
+
+    # -- regridding -----------------------------------------
+    def level_extent(self, level: int):
+        nx, ny = ctypes.c_int64(), ctypes.c_int64()
+        self._check(load().claw_level_extent(self._h, level, ctypes.byref(nx), ctypes.byref(ny)))
+        return nx.value, ny.value
+
+    def descs(self, level: int) -> np.ndarray:
+        """The level's current patch descriptors (after regridding too)."""
+        n = ctypes.c_int32()
+        self._check(load().claw_level_count(self._h, level, ctypes.byref(n)))
+        d = np.zeros(n.value, dtype=PATCH_DTYPE)
+        if n.value:
+            self._check(load().claw_level_descs(self._h, level, d.ctypes.data))
+        return d
+
+    def flag(self, level: int, tol: float, buffer: int = 0, clip: int = 0) -> np.ndarray:
+        """Device flag map [ny, nx] (uint8) of `level` (claw_flag)."""
+        nx, ny = self.level_extent(level)
+        f = np.zeros((ny, nx), np.uint8)
+        cnt = ctypes.c_int64()
+        self._check(load().claw_flag(self._h, level, float(tol), int(buffer), int(clip), f.ctypes.data,
+                                     ctypes.byref(cnt)))
+        assert int(f.sum()) == cnt.value
+        return f
+
+    def regrid(self, level: int, boxes, R: int):
+        b = np.ascontiguousarray(np.asarray(boxes, dtype=np.int32).reshape(-1, 4))
+        self._check(load().claw_regrid(self._h, level, len(b), b.ctypes.data if len(b) else None, int(R)))
+        self._refresh_descs(level + 1)
+
+    def regrid_auto(self, level: int, tol: float, buffer: int, cutoff: float, max_dim: int, min_dim: int,
+                    R: int) -> int:
+        n = ctypes.c_int32()
+        self._check(load().claw_regrid_auto(self._h, level, float(tol), int(buffer), float(cutoff),
+                                            int(max_dim), int(min_dim), int(R), ctypes.byref(n)))
+        self._refresh_descs(level + 1)
+        return n.value
+
+    def _refresh_descs(self, level: int):
+        for l in list(self._descs):
+            if l >= level:
+                del self._descs[l]
+        d = self.descs(level)
+        if len(d):
+            self._descs[level] = d
 
     # -- introspection ---------------------------------------------------
     def debug_ghost_sources(self, level: int, patch: int):

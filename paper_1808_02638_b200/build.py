@@ -30,12 +30,34 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every source to an object in parallel (nvcc -c), then link."""
     if not force and not stale():
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB, *SOURCES, "-ldl"]
+    from concurrent.futures import ThreadPoolExecutor
+
+    odir = os.path.join(PKG, "build")
+    os.makedirs(odir, exist_ok=True)
+    cflags = [f for f in NVCC_FLAGS if f != "-shared"]
+    jobs = []
+    # the kernels file is compiled once per wave limiter (-DCLAW_LIM=k: the
+    # step / reflux template instances of that limiter) plus once for the rest
+    units = [(src, []) for src in SOURCES] + [(SOURCES[0], [f"-DCLAW_LIM={k}"]) for k in range(5)]
+    for src, defs in units:
+        tag = defs[0].split("=")[1] if defs else ""
+        obj = os.path.join(odir, os.path.basename(src) + (f".lim{tag}" if tag else "") + ".o")
+        jobs.append((obj, [nvcc(), *cflags, *defs, "-I", os.path.join(ROOT, "include"), "-c", "-o", obj, src]))
     if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
+        for _, cmd in jobs:
+            print(" ".join(cmd), file=sys.stderr)
+    with ThreadPoolExecutor(len(jobs)) as ex:
+        for r in ex.map(lambda j: subprocess.run(j[1]), jobs):
+            if r.returncode:
+                raise subprocess.CalledProcessError(r.returncode, r.args)
+    link = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB,
+            *[o for o, _ in jobs], "-ldl"]
+    if verbose:
+        print(" ".join(link), file=sys.stderr)
+    subprocess.run(link, check=True)
     return LIB
 
 

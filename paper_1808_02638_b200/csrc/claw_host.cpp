@@ -12,11 +12,16 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
+#include <map>
 #include <memory>
+#include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -78,22 +83,136 @@ struct Nccl {
 };
 Nccl g_nccl;
 
+// ---------------------------------------------------------------------------
+// Device memory pool (the paper's GPU memory pool: cudaMalloc per
+// patch "can even dominate" with small patches).  Every device buffer of the
+// library comes from here.  Blocks are rounded up to size classes (8 per
+// power of two, >= 4 KiB) and cached per device on release; a request reuses
+// the smallest cached block of its class or up to two classes above (<= 25%
+// slack), so a regrid (which frees one level and allocates a similar one) or
+// a re-set level does not call cudaMalloc.  Releases happen only after the
+// owning context's stream is synchronised (set_level, regrid, destroy), so a
+// block is never reused while a kernel may still touch it.  Cached bytes are
+// capped (CLAW_POOL_LIMIT_MB, default 16384); a failing cudaMalloc first
+// returns the device's cached blocks to the driver and retries.
+// ---------------------------------------------------------------------------
+struct Pool {
+  std::mutex mu;
+  std::multimap<std::pair<int, size_t>, void*> cache;  // (device, class bytes) -> block
+  std::unordered_map<void*, std::pair<int, size_t>> live;
+  size_t cached = 0, limit = 0;
+  int64_t hits = 0, misses = 0;
+  Pool() {
+    const char* s = std::getenv("CLAW_POOL_LIMIT_MB");
+    limit = static_cast<size_t>(s ? std::atoll(s) : 16384) << 20;
+  }
+  static size_t size_class(size_t bytes) {
+    size_t b = std::max<size_t>(bytes, 4096);
+    int e = 63 - __builtin_clzll(b);  // 2^e <= b < 2^(e+1)
+    const size_t step = (size_t{1} << e) / 8;
+    return (b + step - 1) / step * step;
+  }
+  void trim_locked(int dev) {
+    for (auto it = cache.begin(); it != cache.end();) {
+      if (it->first.first == dev) {
+        cudaFree(it->second);
+        cached -= it->first.second;
+        it = cache.erase(it);
+      } else {
+        ++it;
+      }
+    }
+  }
+  cudaError_t alloc(void** out, size_t bytes) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const size_t cls = size_class(bytes);
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.lower_bound({dev, cls});
+    if (it != cache.end() && it->first.first == dev && it->first.second <= cls + cls / 4) {
+      *out = it->second;
+      live[it->second] = it->first;
+      cached -= it->first.second;
+      cache.erase(it);
+      ++hits;
+      return cudaSuccess;
+    }
+    e = cudaMalloc(out, cls);
+    if (e == cudaErrorMemoryAllocation) {
+      cudaGetLastError();
+      trim_locked(dev);
+      e = cudaMalloc(out, cls);
+    }
+    if (e != cudaSuccess) {
+      *out = nullptr;
+      return e;
+    }
+    live[*out] = {dev, cls};
+    ++misses;
+    return cudaSuccess;
+  }
+  void release(void* p) {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = live.find(p);
+    if (it == live.end()) return;
+    const auto key = it->second;
+    live.erase(it);
+    if (cached + key.second > limit) {
+      cudaFree(p);
+      return;
+    }
+    cache.emplace(key, p);
+    cached += key.second;
+  }
+  void trim_all() {
+    std::lock_guard<std::mutex> g(mu);
+    for (auto& kv : cache) cudaFree(kv.second);
+    cache.clear();
+    cached = 0;
+  }
+};
+Pool& pool() {
+  static Pool* p = new Pool();  // never destroyed: no cudaFree after the driver is torn down
+  return *p;
+}
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) {
+    o.p = nullptr;
+    o.n = 0;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      reset();
+      p = o.p;
+      n = o.n;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
   ~DevBuf() { reset(); }
   void reset() {
-    if (p) cudaFree(p);
+    if (p) pool().release(p);
     p = nullptr;
     n = 0;
   }
   cudaError_t alloc(size_t count) {
     reset();
     if (count == 0) return cudaSuccess;
-    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T));
-    if (e == cudaSuccess) n = count;
-    else p = nullptr;
+    void* v = nullptr;
+    cudaError_t e = pool().alloc(&v, count * sizeof(T));
+    if (e == cudaSuccess) {
+      p = static_cast<T*>(v);
+      n = count;
+    }
     return e;
   }
 };
@@ -1020,6 +1139,54 @@ int upload(claw_ctx* ctx, DevBuf<T>& b, const std::vector<T>& v) {
   return CLAW_OK;
 }
 
+// Device pool of a planned level: two ping-pong buffers, the frame, every
+// table (allocated once per set_level / regrid; no per-step allocation, cf.
+// the paper's memory pool P:422-426; blocks come from the caching Pool).
+int alloc_level(claw_ctx* ctx, int level, Level& L) {
+  for (int b = 0; b < 2; ++b) {
+    cudaError_t e = L.q[b].alloc(std::max<int64_t>(L.buf_elems, 1));
+    if (e != cudaSuccess) {
+      const long long bytes = 2ll * L.buf_elems * 8;
+      L = Level();
+      cudaGetLastError();
+      return fail(ctx, CLAW_ENOMEM, "level %d: cannot allocate %lld bytes of device pool", level, bytes);
+    }
+  }
+  CUDA_TRY(L.frame.alloc(std::max<int64_t>(L.frame_elems, 1)));
+  if (int r2 = upload(ctx, L.dpatch, L.hpatch)) return r2;
+  if (int r2 = upload(ctx, L.drect, L.hrect)) return r2;
+  if (int r2 = upload(ctx, L.dtile, L.htile)) return r2;
+  if (int r2 = upload(ctx, L.dinterp, L.hinterp)) return r2;
+  if (int r2 = upload(ctx, L.du, L.hu)) return r2;
+  if (int r2 = upload(ctx, L.du_src, L.hu_src)) return r2;
+  if (int r2 = upload(ctx, L.du_scs, L.hu_scs)) return r2;
+  if (int r2 = upload(ctx, L.dreg, L.hreg)) return r2;
+  if (int r2 = upload(ctx, L.dheads, L.hheads)) return r2;
+  CUDA_TRY(L.racc.alloc(std::max<size_t>(3 * L.hreg.size(), 1)));
+  CUDA_TRY(cudaMemset(L.racc.p, 0, L.racc.n * 8));
+  CUDA_TRY(L.pcfl.alloc(std::max<size_t>(L.owned.size(), 1)));
+  CUDA_TRY(L.lcfl.alloc(2));
+  CUDA_TRY(cudaMemset(L.pcfl.p, 0, L.pcfl.n * 8));
+  CUDA_TRY(cudaMemset(L.lcfl.p, 0, 16));
+  L.gen = 0;
+  const int world = ctx->cfg.world;
+  L.dsend_off.clear();
+  L.dsend_cs.clear();
+  L.dsend_buf.clear();
+  for (int r = 0; r < world; ++r) {
+    L.dsend_off.emplace_back(new DevBuf<int64_t>());
+    L.dsend_cs.emplace_back(new DevBuf<int64_t>());
+    L.dsend_buf.emplace_back(new DevBuf<double>());
+    if (int r2 = upload(ctx, *L.dsend_off[r], L.send_off[r])) return r2;
+    if (int r2 = upload(ctx, *L.dsend_cs[r], L.send_cs[r])) return r2;
+    CUDA_TRY(L.dsend_buf[r]->alloc(3 * L.send_off[r].size()));
+  }
+  L.device_bytes = 2 * L.buf_elems * 8 + L.frame_elems * 8 +
+                   static_cast<int64_t>(L.hpatch.size() * sizeof(DevPatch) + L.hrect.size() * sizeof(DevRect) +
+                                        L.htile.size() * sizeof(int4) + L.hinterp.size() * sizeof(DevInterp));
+  return CLAW_OK;
+}
+
 int check_ctx(claw_ctx* c) {
   if (!c) return CLAW_EINVAL;
   if (c->dead) return fail(c, CLAW_ECUDA, "context unusable after an earlier CUDA/NCCL error");
@@ -1186,49 +1353,7 @@ int claw_set_level(claw_ctx* ctx, int32_t level, int32_t npatch, const claw_patc
     L.set = true;
     return CLAW_OK;
   }
-  // device pool: two ping-pong buffers + frame + tables (allocated once; no
-  // per-step allocation, cf. the paper's memory pool P:422-426)
-  for (int b = 0; b < 2; ++b) {
-    cudaError_t e = L.q[b].alloc(std::max<int64_t>(L.buf_elems, 1));
-    if (e != cudaSuccess) {
-      L = Level();
-      cudaGetLastError();
-      return fail(ctx, CLAW_ENOMEM, "level %d: cannot allocate %lld bytes of device pool", level,
-                  (long long)(2 * L.buf_elems * 8));
-    }
-  }
-  CUDA_TRY(L.frame.alloc(std::max<int64_t>(L.frame_elems, 1)));
-  if (int r2 = upload(ctx, L.dpatch, L.hpatch)) return r2;
-  if (int r2 = upload(ctx, L.drect, L.hrect)) return r2;
-  if (int r2 = upload(ctx, L.dtile, L.htile)) return r2;
-  if (int r2 = upload(ctx, L.dinterp, L.hinterp)) return r2;
-  if (int r2 = upload(ctx, L.du, L.hu)) return r2;
-  if (int r2 = upload(ctx, L.du_src, L.hu_src)) return r2;
-  if (int r2 = upload(ctx, L.du_scs, L.hu_scs)) return r2;
-  if (int r2 = upload(ctx, L.dreg, L.hreg)) return r2;
-  if (int r2 = upload(ctx, L.dheads, L.hheads)) return r2;
-  CUDA_TRY(L.racc.alloc(std::max<size_t>(3 * L.hreg.size(), 1)));
-  CUDA_TRY(cudaMemset(L.racc.p, 0, L.racc.n * 8));
-  CUDA_TRY(L.pcfl.alloc(std::max<size_t>(L.owned.size(), 1)));
-  CUDA_TRY(L.lcfl.alloc(2));
-  CUDA_TRY(cudaMemset(L.pcfl.p, 0, L.pcfl.n * 8));
-  CUDA_TRY(cudaMemset(L.lcfl.p, 0, 16));
-  L.gen = 0;
-  const int world = ctx->cfg.world;
-  L.dsend_off.clear();
-  L.dsend_cs.clear();
-  L.dsend_buf.clear();
-  for (int r = 0; r < world; ++r) {
-    L.dsend_off.emplace_back(new DevBuf<int64_t>());
-    L.dsend_cs.emplace_back(new DevBuf<int64_t>());
-    L.dsend_buf.emplace_back(new DevBuf<double>());
-    if (int r2 = upload(ctx, *L.dsend_off[r], L.send_off[r])) return r2;
-    if (int r2 = upload(ctx, *L.dsend_cs[r], L.send_cs[r])) return r2;
-    CUDA_TRY(L.dsend_buf[r]->alloc(3 * L.send_off[r].size()));
-  }
-  L.device_bytes = 2 * L.buf_elems * 8 + L.frame_elems * 8 +
-                   static_cast<int64_t>(L.hpatch.size() * sizeof(DevPatch) + L.hrect.size() * sizeof(DevRect) +
-                                        L.htile.size() * sizeof(int4) + L.hinterp.size() * sizeof(DevInterp));
+  if (int r2 = alloc_level(ctx, level, L)) return r2;
   L.cur = 0;
   if (q0) {
     if (L.gapless) {
@@ -1246,6 +1371,9 @@ int claw_set_level(claw_ctx* ctx, int32_t level, int32_t npatch, const claw_patc
   }
   CUDA_TRY(cudaMemcpy(L.q[1].p, L.q[0].p, L.buf_elems * 8, cudaMemcpyDeviceToDevice));
   CUDA_TRY(cudaMemset(L.frame.p, 0, L.frame.n * 8));
+  // the copies above ran on the legacy stream; the library's stream is
+  // non-blocking, so finish them before any kernel can read the level
+  CUDA_TRY(cudaStreamSynchronize(nullptr));
   L.set = true;
   return CLAW_OK;
 }
@@ -1737,6 +1865,478 @@ int claw_debug_halo_send(const claw_ctx* ctx, int32_t level, int32_t peer, int64
   if (patch) *patch = static_cast<int32_t>(code >> 32);
   if (j) *j = static_cast<int32_t>((code >> 16) & 0xffff);
   if (i) *i = static_cast<int32_t>(code & 0xffff);
+  return CLAW_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Regridding (NEXT-3; "every K time steps ... cells are flagged
+// ... clustered into new rectangular grid patches"; DESIGN.md
+// R18).  Flagging and the new level's data stay on the device; only the flag
+// map crosses to the host for clustering, as in the paper (the CPU owns the
+// patch structure).
+// ---------------------------------------------------------------------------
+namespace {
+
+// Berger-Rigoutsos box splitter over a summed-area table (each box costs
+// O(w + h) instead of O(w h)).  Rules (R18): shrink to the flags'
+// bounding box; accept if efficiency >= cutoff and both sides <= max_dim;
+// else cut at (a) the hole of the signature closest to the centre (longer
+// side first), (b) the strongest sign change of the signature's second
+// difference (largest |jump|, then closest to the centre, longer side first),
+// (c) the middle of the longer side -- every cut leaving >= min_dim on both
+// sides; no admissible cut: accept.  Low part before high part.
+struct Clusterer {
+  int64_t nx, ny;
+  std::vector<int64_t> sat;  // (ny+1) x (nx+1) prefix counts
+  double cutoff;
+  int maxd, mind;
+  std::vector<int32_t> out;  // (x0, y0, w, h) quadruples
+
+  Clusterer(const uint8_t* f, int64_t nx_, int64_t ny_, double c, int mx, int mn)
+      : nx(nx_), ny(ny_), sat(static_cast<size_t>((nx_ + 1) * (ny_ + 1)), 0), cutoff(c), maxd(mx), mind(mn) {
+    for (int64_t J = 0; J < ny; ++J) {
+      int64_t run = 0;
+      for (int64_t I = 0; I < nx; ++I) {
+        run += f[J * nx + I] ? 1 : 0;
+        sat[(J + 1) * (nx + 1) + I + 1] = sat[J * (nx + 1) + I + 1] + run;
+      }
+    }
+  }
+  int64_t count(int64_t x0, int64_t y0, int64_t x1, int64_t y1) const {  // [x0,x1) x [y0,y1)
+    const int64_t W = nx + 1;
+    return sat[y1 * W + x1] - sat[y0 * W + x1] - sat[y1 * W + x0] + sat[y0 * W + x0];
+  }
+  void emit(int64_t x0, int64_t y0, int64_t w, int64_t h) {
+    out.push_back(static_cast<int32_t>(x0));
+    out.push_back(static_cast<int32_t>(y0));
+    out.push_back(static_cast<int32_t>(w));
+    out.push_back(static_cast<int32_t>(h));
+  }
+  bool admissible(int64_t k, int64_t n) const { return k >= mind && n - k >= mind; }
+
+  void run() {
+    struct Box { int64_t x0, y0, x1, y1; };
+    std::vector<Box> stack{{0, 0, nx, ny}};
+    std::vector<int64_t> sig[2];
+    while (!stack.empty()) {
+      Box b = stack.back();
+      stack.pop_back();
+      if (count(b.x0, b.y0, b.x1, b.y1) == 0) continue;
+      // shrink: first / last non-empty column and row
+      while (count(b.x0, b.y0, b.x0 + 1, b.y1) == 0) ++b.x0;
+      while (count(b.x1 - 1, b.y0, b.x1, b.y1) == 0) --b.x1;
+      while (count(b.x0, b.y0, b.x1, b.y0 + 1) == 0) ++b.y0;
+      while (count(b.x0, b.y1 - 1, b.x1, b.y1) == 0) --b.y1;
+      const int64_t w = b.x1 - b.x0, h = b.y1 - b.y0;
+      const int64_t nf = count(b.x0, b.y0, b.x1, b.y1);
+      if (static_cast<double>(nf) / static_cast<double>(w * h) >= cutoff && w <= maxd && h <= maxd) {
+        emit(b.x0, b.y0, w, h);
+        continue;
+      }
+      sig[0].resize(w);
+      sig[1].resize(h);
+      for (int64_t k = 0; k < w; ++k) sig[0][k] = count(b.x0 + k, b.y0, b.x0 + k + 1, b.y1);
+      for (int64_t k = 0; k < h; ++k) sig[1][k] = count(b.x0, b.y0 + k, b.x1, b.y0 + k + 1);
+      const int order[2] = {w >= h ? 0 : 1, w >= h ? 1 : 0};
+      const int64_t len[2] = {w, h};
+      int dir = -1;
+      int64_t cut = 0;
+      // (a) holes
+      for (int t = 0; t < 2 && dir < 0; ++t) {
+        const int d = order[t];
+        const int64_t n = len[d];
+        int64_t best = -1, bd = 0;
+        for (int64_t k = 1; k < n; ++k) {
+          if (sig[d][k] != 0 || !admissible(k, n)) continue;
+          const int64_t dist = std::llabs(2 * k - n);
+          if (best < 0 || dist < bd) {
+            best = k;
+            bd = dist;
+          }
+        }
+        if (best >= 0) {
+          dir = d;
+          cut = best;
+        }
+      }
+      // (b) inflections of the second difference
+      if (dir < 0) {
+        int64_t bv = -1, bd = 0;
+        for (int t = 0; t < 2; ++t) {
+          const int d = order[t];
+          const int64_t n = len[d];
+          const std::vector<int64_t>& g = sig[d];
+          for (int64_t k = 2; k + 2 <= n; ++k) {
+            const int64_t lap0 = g[k - 2] - 2 * g[k - 1] + g[k];
+            const int64_t lap1 = g[k - 1] - 2 * g[k] + g[k + 1];
+            const bool flip = (lap0 < 0 && lap1 > 0) || (lap0 > 0 && lap1 < 0);
+            if (!flip || !admissible(k, n)) continue;
+            const int64_t v = std::llabs(lap1 - lap0), dist = std::llabs(2 * k - n);
+            if (v > bv || (v == bv && dist < bd)) {
+              bv = v;
+              bd = dist;
+              dir = d;
+              cut = k;
+            }
+          }
+        }
+      }
+      // (c) bisect the longer side
+      if (dir < 0 && admissible(len[order[0]] / 2, len[order[0]])) {
+        dir = order[0];
+        cut = len[order[0]] / 2;
+      }
+      if (dir < 0) {
+        emit(b.x0, b.y0, w, h);
+        continue;
+      }
+      Box lo = b, hi = b;
+      if (dir == 0) lo.x1 = hi.x0 = b.x0 + cut;
+      else lo.y1 = hi.y0 = b.y0 + cut;
+      stack.push_back(hi);  // LIFO: the low part is processed (entirely) first
+      stack.push_back(lo);
+    }
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int claw_level_extent(const claw_ctx* ctx, int32_t level, int64_t* nx, int64_t* ny) {
+  if (!ctx || level < 1 || level > kMaxLevel || !ctx->lev[level].set) return CLAW_EINVAL;
+  if (nx) *nx = ctx->lev[level].nx;
+  if (ny) *ny = ctx->lev[level].ny;
+  return CLAW_OK;
+}
+
+int claw_level_count(const claw_ctx* ctx, int32_t level, int32_t* npatch) {
+  if (!ctx || !npatch || level < 1 || level > kMaxLevel) return CLAW_EINVAL;
+  *npatch = ctx->lev[level].set ? ctx->lev[level].npatch : 0;
+  return CLAW_OK;
+}
+
+int claw_level_descs(const claw_ctx* ctx, int32_t level, claw_patch_desc* out) {
+  if (!ctx || !out || level < 1 || level > kMaxLevel || !ctx->lev[level].set) return CLAW_EINVAL;
+  const Level& L = ctx->lev[level];
+  std::memcpy(out, L.desc.data(), sizeof(claw_patch_desc) * L.desc.size());
+  return CLAW_OK;
+}
+
+int claw_cluster(const uint8_t* flags, int64_t nx, int64_t ny, double cutoff, int32_t max_dim, int32_t min_dim,
+                 int32_t* boxes, int32_t cap, int32_t* nbox) {
+  if (!flags || nx < 1 || ny < 1 || !(cutoff > 0.0) || cutoff > 1.0 || max_dim < 1 || min_dim < 1 ||
+      2 * min_dim > max_dim || !nbox || nx >= (1ll << 31) || ny >= (1ll << 31))
+    return CLAW_EINVAL;
+  Clusterer cl(flags, nx, ny, cutoff, max_dim, min_dim);
+  cl.run();
+  const int64_t n = static_cast<int64_t>(cl.out.size() / 4);
+  *nbox = static_cast<int32_t>(n);
+  if (boxes) std::memcpy(boxes, cl.out.data(), sizeof(int32_t) * 4 * std::min<int64_t>(n, cap));
+  return (boxes && n > cap) ? CLAW_ENOMEM : CLAW_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Flag map of `level` on the device: raw flags, the level's own cells, and
+// (nest > 0) the nesting mask M = cells whose in-domain neighbours within
+// Chebyshev distance `nest` all belong to the level; then the dilation by
+// `buffer` clipped to (clip: the level's cells / M).  Leaves the result in
+// `out` (device) and its count in *nflag.
+int flag_device(claw_ctx* ctx, int level, double tol, int buffer, int clip, DevBuf<uint8_t>& out,
+                DevBuf<uint8_t>& on, int64_t* nflag) {
+  Level& L = ctx->lev[level];
+  const int64_t n = L.nx * L.ny;
+  DevBuf<uint8_t> raw, tmp;
+  DevBuf<int2> orig;
+  DevBuf<unsigned long long> cnt;
+  CUDA_TRY(raw.alloc(n));
+  CUDA_TRY(tmp.alloc(n));
+  CUDA_TRY(out.alloc(n));
+  CUDA_TRY(on.alloc(n));
+  CUDA_TRY(cnt.alloc(1));
+  std::vector<int2> ho(L.owned.size());
+  for (size_t lp = 0; lp < L.owned.size(); ++lp)
+    ho[lp] = make_int2(static_cast<int>(L.i0[L.owned[lp]]), static_cast<int>(L.j0[L.owned[lp]]));
+  if (int rc = upload(ctx, orig, ho)) return rc;
+  CUDA_TRY(cudaMemsetAsync(raw.p, 0, n, ctx->stream));
+  CUDA_TRY(cudaMemsetAsync(on.p, 0, n, ctx->stream));
+  CUDA_TRY(cudaMemsetAsync(cnt.p, 0, 8, ctx->stream));
+  claw::StepParams P{};
+  P.q = L.q[L.cur].p;
+  P.frame = L.frame.p;
+  P.patches = L.dpatch.p;
+  P.rects = L.drect.p;
+  CUDA_TRY(static_cast<cudaError_t>(claw::launch_flag(P, orig.p, static_cast<int32_t>(L.owned.size()), L.nx, tol,
+                                                      raw.p, on.p, ctx->stream)));
+  const uint8_t* mask = nullptr;
+  if (clip == 1) mask = on.p;
+  if (clip == 2) {
+    // M = on & ~dilate(~on, 2): the complement, dilated (clipped to the
+    // domain, so out-of-domain cells never veto), then inverted
+    DevBuf<uint8_t> off, offd;
+    DevBuf<unsigned long long> c2;
+    CUDA_TRY(off.alloc(n));
+    CUDA_TRY(offd.alloc(n));
+    CUDA_TRY(c2.alloc(1));
+    CUDA_TRY(static_cast<cudaError_t>(claw::launch_not(on.p, off.p, n, ctx->stream)));
+    CUDA_TRY(static_cast<cudaError_t>(claw::launch_dilate(off.p, tmp.p, offd.p, nullptr, L.nx, L.ny, 2, c2.p,
+                                                          ctx->stream)));
+    CUDA_TRY(static_cast<cudaError_t>(claw::launch_not(offd.p, on.p, n, ctx->stream)));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));  // off / offd go back to the pool
+    mask = on.p;
+  }
+  CUDA_TRY(static_cast<cudaError_t>(claw::launch_dilate(raw.p, tmp.p, out.p, mask, L.nx, L.ny, buffer, cnt.p,
+                                                        ctx->stream)));
+  unsigned long long c = 0;
+  CUDA_TRY(cudaMemcpyAsync(&c, cnt.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  if (nflag) *nflag = static_cast<int64_t>(c);
+  return CLAW_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int claw_flag(claw_ctx* ctx, int32_t level, double tol, int32_t buffer, int32_t clip, uint8_t* flags_out,
+              int64_t* nflag) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = check_level(ctx, level)) return rc;
+  if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
+  if (ctx->cfg.world > 1) return fail(ctx, CLAW_EINVAL, "flagging is single-rank in this version");
+  if (buffer < 0 || clip < 0 || clip > 2) return fail(ctx, CLAW_EINVAL, "buffer=%d clip=%d", buffer, clip);
+  DevBuf<uint8_t> out, on;
+  if (int rc = flag_device(ctx, level, tol, buffer, clip, out, on, nflag)) return rc;
+  const Level& L = ctx->lev[level];
+  if (flags_out) {
+    CUDA_TRY(cudaMemcpyAsync(flags_out, out.p, L.nx * L.ny, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  }
+  return CLAW_OK;
+}
+
+int claw_regrid(claw_ctx* ctx, int32_t level, int32_t nbox, const int32_t* boxes, int32_t R) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = check_level(ctx, level)) return rc;
+  if (level >= kMaxLevel) return fail(ctx, CLAW_EINVAL, "regrid: level %d has no finer level", level);
+  if (ctx->cfg.world > 1) return fail(ctx, CLAW_EINVAL, "regridding is single-rank in this version");
+  if (nbox < 0 || (nbox > 0 && !boxes) || R < 1) return fail(ctx, CLAW_EINVAL, "regrid: nbox=%d R=%d", nbox, R);
+  Level& C = ctx->lev[level];
+  for (int b = 0; b < nbox; ++b) {
+    const int32_t* x = boxes + 4 * b;
+    if (x[2] < 1 || x[3] < 1 || x[0] < 0 || x[1] < 0 || x[0] + x[2] > C.nx || x[1] + x[3] > C.ny)
+      return fail(ctx, CLAW_EINVAL, "regrid: box %d (%d,%d,%d,%d) outside level %d's index space", b, x[0], x[1],
+                  x[2], x[3], level);
+  }
+  if (!ctx->host_only) CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  Level old = std::move(ctx->lev[level + 1]);
+  for (int l = level + 1; l <= kMaxLevel; ++l) ctx->lev[l] = Level();
+  if (nbox == 0) return CLAW_OK;
+  // descriptors of the new level: boxes refined by R
+  const double dxf = C.dx / R, dyf = C.dy / R;
+  std::vector<claw_patch_desc> d(nbox);
+  for (int b = 0; b < nbox; ++b) {
+    d[b].mx = boxes[4 * b + 2] * R;
+    d[b].my = boxes[4 * b + 3] * R;
+    d[b].dx = dxf;
+    d[b].dy = dyf;
+    d[b].xlower = ctx->cfg.xlo + static_cast<double>(boxes[4 * b + 0] * R) * dxf;
+    d[b].ylower = ctx->cfg.ylo + static_cast<double>(boxes[4 * b + 1] * R) * dyf;
+    d[b].mbc = 2;
+    d[b].rho = C.desc[0].rho;
+    d[b].K = C.desc[0].K;
+  }
+  Level& L = ctx->lev[level + 1];
+  int rc = build_geometry(ctx, level + 1, nbox, d.data(), L);
+  if (!rc) rc = plan_level(ctx, level + 1, L);
+  if (rc) {
+    L = Level();
+    return rc;
+  }
+  // copy rectangles (old fine cells at the same place) and interpolation
+  // cells (the rest), built per new patch
+  std::vector<claw::DevCopyRect> rects;
+  std::vector<claw::DevRegridCell> cells;
+  for (int p = 0; p < nbox; ++p) {
+    const int lp = L.local[p];
+    const int mx = d[p].mx, my = d[p].my;
+    const int64_t I0 = L.i0[p], J0 = L.j0[p];
+    const int bw = boxes[4 * p + 2], bh = boxes[4 * p + 3];
+    std::vector<int32_t> cover(static_cast<size_t>(bw) * bh, 0);  // copied fine cells per coarse cell
+    if (old.set) {
+      std::vector<int> cand;
+      const int64_t bx0 = I0 / kBucket, bx1 = std::min(old.nbx - 1, (I0 + mx - 1) / kBucket);
+      const int64_t by0 = J0 / kBucket, by1 = std::min(old.nby - 1, (J0 + my - 1) / kBucket);
+      for (int64_t by = by0; by <= by1; ++by)
+        for (int64_t bx = bx0; bx <= bx1; ++bx)
+          for (int64_t k = old.bstart[by * old.nbx + bx]; k < old.bstart[by * old.nbx + bx + 1]; ++k)
+            cand.push_back(old.blist[k]);
+      std::sort(cand.begin(), cand.end());
+      cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+      for (int q : cand) {
+        const int64_t x0 = std::max(I0, old.i0[q]), x1 = std::min(I0 + mx, old.i0[q] + old.desc[q].mx);
+        const int64_t y0 = std::max(J0, old.j0[q]), y1 = std::min(J0 + my, old.j0[q] + old.desc[q].my);
+        if (x0 >= x1 || y0 >= y1) continue;
+        const int lq = old.local[q];
+        claw::DevCopyRect r{};
+        r.src = old.off[lq] + (y0 - old.j0[q]) * old.desc[q].mx + (x0 - old.i0[q]);
+        r.dst = L.off[lp] + (y0 - J0) * mx + (x0 - I0);
+        r.scs = static_cast<int64_t>(old.desc[q].mx) * old.desc[q].my;
+        r.dcs = static_cast<int64_t>(mx) * my;
+        r.smx = old.desc[q].mx;
+        r.dmx = mx;
+        r.w = static_cast<int32_t>(x1 - x0);
+        r.h = static_cast<int32_t>(y1 - y0);
+        rects.push_back(r);
+        for (int64_t J = y0; J < y1; ++J)
+          for (int64_t I = x0; I < x1; ++I) cover[((J - J0) / R) * bw + (I - I0) / R]++;
+      }
+    }
+    for (int cj = 0; cj < bh; ++cj)
+      for (int ci = 0; ci < bw; ++ci) {
+        claw::DevRegridCell e{};
+        e.dst = L.off[lp] + static_cast<int64_t>(cj) * R * mx + static_cast<int64_t>(ci) * R;
+        e.dcs = static_cast<int64_t>(mx) * my;
+        e.fmx = mx;
+        const int64_t Ic = boxes[4 * p + 0] + ci, Jc = boxes[4 * p + 1] + cj;
+        const bool copied = cover[cj * bw + ci] == R * R;
+        const int64_t cI[5] = {Ic, map_axis(Ic - 1, C.nx, ctx->cfg.bc[0], ctx->cfg.bc[1]),
+                               map_axis(Ic + 1, C.nx, ctx->cfg.bc[0], ctx->cfg.bc[1]), Ic, Ic};
+        const int64_t cJ[5] = {Jc, Jc, Jc, map_axis(Jc - 1, C.ny, ctx->cfg.bc[2], ctx->cfg.bc[3]),
+                               map_axis(Jc + 1, C.ny, ctx->cfg.bc[2], ctx->cfg.bc[3])};
+        bool ok = !copied;
+        for (int k = 0; k < 5 && ok; ++k) {
+          const int q = C.find(cI[k], cJ[k]);
+          if (q < 0) {
+            L = Level();
+            return fail(ctx, CLAW_ENEST, "regrid: new cell over level-%d cell (%lld,%lld) needs level-%d cell "
+                        "(%lld,%lld), which is not on the level", level, (long long)Ic, (long long)Jc, level,
+                        (long long)cI[k], (long long)cJ[k]);
+          }
+          e.off[k] = C.off[C.local[q]] + (cJ[k] - C.j0[q]) * C.desc[q].mx + (cI[k] - C.i0[q]);
+          e.cs[k] = static_cast<int64_t>(C.desc[q].mx) * C.desc[q].my;
+        }
+        if (!ok) e.off[0] = -1;
+        cells.push_back(e);
+      }
+  }
+  L.t_old = L.t_new = C.t_new;
+  if (ctx->host_only) {
+    L.set = true;
+    return CLAW_OK;
+  }
+  if (int r2 = alloc_level(ctx, level + 1, L)) return r2;
+  L.cur = 0;
+  DevBuf<claw::DevRegridCell> dcells;
+  DevBuf<claw::DevCopyRect> drects;
+  if (int r2 = upload(ctx, dcells, cells)) return r2;
+  if (int r2 = upload(ctx, drects, rects)) return r2;
+  CUDA_TRY(cudaStreamSynchronize(nullptr));  // alloc_level's legacy-stream memsets
+  CUDA_TRY(static_cast<cudaError_t>(claw::launch_regrid(C.q[1 - C.cur].p, C.q[C.cur].p, dcells.p,
+                                                        static_cast<int64_t>(cells.size()), R,
+                                                        old.set ? old.q[old.cur].p : nullptr, drects.p,
+                                                        static_cast<int32_t>(rects.size()), L.q[0].p, ctx->stream)));
+  CUDA_TRY(cudaMemcpyAsync(L.q[1].p, L.q[0].p, L.buf_elems * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  CUDA_TRY(cudaMemsetAsync(L.frame.p, 0, L.frame.n * 8, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));  // the old level and the tables go back to the pool
+  ctx->stats.ghost_launches += 2;
+  L.set = true;
+  return CLAW_OK;
+}
+
+int claw_regrid_auto(claw_ctx* ctx, int32_t level, double tol, int32_t buffer, double cutoff, int32_t max_dim,
+                     int32_t min_dim, int32_t R, int32_t* nbox_out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = check_level(ctx, level)) return rc;
+  if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
+  if (ctx->cfg.world > 1) return fail(ctx, CLAW_EINVAL, "regridding is single-rank in this version");
+  if (buffer < 0) return fail(ctx, CLAW_EINVAL, "buffer=%d", buffer);
+  const Level& C = ctx->lev[level];
+  const int64_t n = C.nx * C.ny;
+  DevBuf<uint8_t> out, on;
+  int64_t nflag = 0;
+  if (int rc = flag_device(ctx, level, tol, buffer, 2, out, on, &nflag)) return rc;
+  std::vector<uint8_t> f(n), m(n);
+  CUDA_TRY(cudaMemcpyAsync(f.data(), out.p, n, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(m.data(), on.p, n, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  std::vector<int32_t> boxes;
+  if (nflag > 0) {
+    if (!(cutoff > 0.0) || cutoff > 1.0 || max_dim < 1 || min_dim < 1 || 2 * min_dim > max_dim)
+      return fail(ctx, CLAW_EINVAL, "cluster: cutoff=%g max_dim=%d min_dim=%d", cutoff, max_dim, min_dim);
+    Clusterer cl(f.data(), C.nx, C.ny, cutoff, max_dim, min_dim);
+    cl.run();
+    // nesting: split each box into row-run rectangles of the nesting mask M
+    // (runs identical in consecutive rows merge), drop pieces without flags
+    Clusterer fs(f.data(), C.nx, C.ny, 1.0, 2, 1);  // only for its prefix counts
+    for (size_t b = 0; b < cl.out.size(); b += 4) {
+      const int64_t x0 = cl.out[b], y0 = cl.out[b + 1], x1 = x0 + cl.out[b + 2], y1 = y0 + cl.out[b + 3];
+      struct Open { int64_t a, e, y; };
+      std::vector<Open> open, next;
+      std::vector<std::array<int64_t, 4>> done;
+      for (int64_t J = y0; J <= y1; ++J) {
+        std::vector<std::pair<int64_t, int64_t>> runs;
+        if (J < y1)
+          for (int64_t I = x0; I < x1;) {
+            if (!m[J * C.nx + I]) {
+              ++I;
+              continue;
+            }
+            int64_t e = I;
+            while (e < x1 && m[J * C.nx + e]) ++e;
+            runs.emplace_back(I, e);
+            I = e;
+          }
+        next.clear();
+        for (const Open& o : open) {
+          bool cont = false;
+          for (auto& r : runs)
+            if (r.first == o.a && r.second == o.e) cont = true;
+          if (cont) next.push_back(o);
+          else done.push_back({o.a, o.y, o.e, J});
+        }
+        for (auto& r : runs) {
+          bool had = false;
+          for (const Open& o : open)
+            if (o.a == r.first && o.e == r.second) had = true;
+          if (!had) next.push_back(Open{r.first, r.second, J});
+        }
+        std::sort(next.begin(), next.end(), [](const Open& a, const Open& b) { return a.a < b.a; });
+        open.swap(next);
+      }
+      std::stable_sort(done.begin(), done.end(), [](const std::array<int64_t, 4>& a, const std::array<int64_t, 4>& b) {
+        return a[1] != b[1] ? a[1] < b[1] : a[0] < b[0];
+      });
+      for (auto& r : done)
+        if (fs.count(r[0], r[1], r[2], r[3]) > 0) {
+          boxes.push_back(static_cast<int32_t>(r[0]));
+          boxes.push_back(static_cast<int32_t>(r[1]));
+          boxes.push_back(static_cast<int32_t>(r[2] - r[0]));
+          boxes.push_back(static_cast<int32_t>(r[3] - r[1]));
+        }
+    }
+  }
+  const int32_t nb = static_cast<int32_t>(boxes.size() / 4);
+  if (nbox_out) *nbox_out = nb;
+  return claw_regrid(ctx, level, nb, boxes.data(), R);
+}
+
+int claw_pool_stats(int64_t* hits, int64_t* misses, int64_t* cached_bytes) {
+  Pool& P = pool();
+  std::lock_guard<std::mutex> g(P.mu);
+  if (hits) *hits = P.hits;
+  if (misses) *misses = P.misses;
+  if (cached_bytes) *cached_bytes = static_cast<int64_t>(P.cached);
+  return CLAW_OK;
+}
+
+int claw_pool_trim(void) {
+  pool().trim_all();
   return CLAW_OK;
 }
 

@@ -136,6 +136,36 @@ int launch_reflux(int which, const StepParams& p, const double* qc, const DevPat
                   const DevReflux* tab, int64_t n, int R, double* acc, void* stream);
 int launch_reflux_apply(double* qc, const DevPatch* cpatches, const DevReflux* tab, const int32_t* heads,
                         int64_t nheads, double* acc, void* stream);
+// Regridding (NEXT-3; R18).
+// Flagging: every interior cell of owned patch lp (origin orig[lp] in the
+// level index space) sets raw[J*nx+I] = (max over its 4 edge neighbours of
+// |p_n - p| > tol) and on[J*nx+I] = 1; neighbours resolved like the step
+// kernel's (p.q, p.frame, p.patches, p.rects).
+int launch_flag(const StepParams& p, const int2* orig, int32_t nown, int64_t nx, double tol, uint8_t* raw,
+                uint8_t* on, void* stream);
+// Chebyshev dilation by b, clipped to [0,nx) x [0,ny) and (mask != null) to
+// mask != 0; *count (device, zeroed by the caller) receives the set cells.
+int launch_dilate(const uint8_t* in, uint8_t* tmp, uint8_t* out, const uint8_t* mask, int64_t nx, int64_t ny, int b,
+                  unsigned long long* count, void* stream);
+int launch_not(const uint8_t* in, uint8_t* out, int64_t n, void* stream);
+// New fine level: coarse cell e of a new box supplies its R x R children by
+// the R10 interpolation at alpha = 1 (off[0] < 0: skip, every child is copied
+// from the old fine level); children at dst + b*fmx + a (component stride dcs).
+struct DevRegridCell {
+  int64_t off[5];
+  int64_t cs[5];
+  int64_t dst, dcs;
+  int32_t fmx, pad;
+};
+// Copy rectangle from the old fine level (same level index space).
+struct DevCopyRect {
+  int64_t src, dst;    // offsets (p component) of the rectangle's first cell
+  int64_t scs, dcs;    // component strides
+  int32_t smx, dmx;    // row pitches
+  int32_t w, h;
+};
+int launch_regrid(const double* qc_old, const double* qc_new, const DevRegridCell* cells, int64_t ncell, int R,
+                  const double* qf_old, const DevCopyRect* rects, int32_t nrect, double* qf, void* stream);
 int max_tile_rows();
 int grid_strip();
 
