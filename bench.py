@@ -57,7 +57,26 @@ def measured_peaks():
 
 
 def workload(name: str) -> W.Workload:
-    return {"c1": W.c1, "c2": W.c2, "c3": W.c3, "c4": W.c4, "c5": W.c5}[name]()
+    return {"c1": W.c1, "c2": W.c2, "c3": W.c3, "c4": W.c4, "c5": W.c5, "paper": W.paper}[name]()
+
+
+def hierarchy_ratios(wl: W.Workload) -> list:
+    """R_L between levels L and L+1 (fixed hierarchies: from the levels;
+    dynamic ones, created by regridding: from the workload's extra)."""
+    if wl.extra.get("ratios"):
+        return list(wl.extra["ratios"])
+    return [wl.levels[L].ratio for L in range(1, len(wl.levels))]
+
+
+def regrid_params(wl: W.Workload, L: int, dxl: float, dx1: float, tol_arg: float):
+    """(tol, buffer, cutoff, max_dim, min_dim, R) of the regrid of level L+1
+    from level L (R18/R19)."""
+    R = hierarchy_ratios(wl)
+    e = wl.extra
+    if e.get("ratios"):
+        buf = int(e["buffer_coarse_cells"] * np.prod(R[:L - 1]))
+        return e["tol_per_dx"] * dxl, buf, e["cutoff"], e["max_dim"], e["min_dim"], R[L - 1]
+    return tol_arg * dxl / dx1, 2, 0.7, 32, 4, R[L - 1]
 
 
 def host_cores():
@@ -142,7 +161,8 @@ def oracle_sample(wl: W.Workload, budget_s: float = 12.0, steps_cap: int | None 
     import oracle
     d0 = wl.levels[0].descs
     mx, my = int(d0["mx"][0]), int(d0["my"][0])
-    uniform = len(wl.levels) == 1 and (d0["mx"] == mx).all() and (d0["my"] == my).all()
+    uniform = len(wl.levels) == 1 and not wl.extra.get("ratios") and (d0["mx"] == mx).all() and \
+        (d0["my"] == my).all()
     cores = host_cores()
     if uniform:
         side = max(1, min(int(math.sqrt(len(d0))), max(1, 1024 // mx)))  # ~1024^2 cells max
@@ -171,29 +191,49 @@ def oracle_sample(wl: W.Workload, budget_s: float = 12.0, steps_cap: int | None 
             if el >= budget_s or (steps_cap and n >= steps_cap):
                 break
         return cells * n / el, cores, f"{desc}, {n} steps, {el:.1f} s"
+    dyn = bool(wl.extra.get("ratios"))
+    if dyn:  # the same dynamic workload on a 200^2 base (4 x 4 patches)
+        wl = W.paper(n1=200, npx=4)
+        o = oracle.Oracle(wl.domain, wl.bc, wl.limiter, wl.order_trans, nthreads=cores)
+        desc = f"{wl.name} (base 200^2 sample of the 1000^2 workload), regrid every {wl.extra['regrid_every']}"
     for L, (lv, q) in enumerate(zip(wl.levels, W.hierarchy_ic(wl)), start=1):
         o.set_level(L, lv.descs, q)
-    ratios = {L + 1: wl.levels[L + 1].ratio for L in range(len(wl.levels) - 1)}
-    nlev = len(wl.levels)
-    per_coarse = sum(wl.levels[L].cells * int(np.prod([wl.levels[k].ratio for k in range(1, L + 1)]))
-                     for L in range(nlev))
+    rat = hierarchy_ratios(wl)
+    nlev = 1 + len(rat)
+    dx1 = float(wl.levels[0].descs["dx"][0])
+    counted = [0]
+
+    def regrid(t):
+        for L in range(1, nlev):
+            if L > 1:
+                o.fill_ghost(L, t)
+            tol, buf, cut, mxd, mnd, R = regrid_params(wl, L, float(o.descs(L)["dx"][0]), dx1, 0.02)
+            oracle.regrid_auto(o, L, tol, buf, cut, mxd, mnd, R)
 
     def bo(level, t, dt):
         o.fill_ghost(level, t)
         o.advance_level(level, dt)
-        if level < nlev:
-            for k in range(ratios[level]):
-                bo(level + 1, t + k * dt / ratios[level], dt / ratios[level])
+        counted[0] += int((o.descs(level)["mx"].astype(np.int64) * o.descs(level)["my"]).sum())
+        if level < nlev and len(o.descs(level + 1)):
+            R = rat[level - 1]
+            for k in range(R):
+                bo(level + 1, t + k * dt / R, dt / R)
+            o.update_level(level + 1)
 
+    every = wl.extra.get("regrid_every", 0) if dyn else 0
+    if dyn:
+        regrid(0.0)
     dt = wl.dt0()
     n, t0 = 0, time.perf_counter()
     while True:
         bo(1, n * dt, dt)
         n += 1
+        if every and n % every == 0:
+            regrid(n * dt)
         el = time.perf_counter() - t0
         if el >= budget_s or (steps_cap and n >= steps_cap):
             break
-    return per_coarse * n / el, cores, f"{desc}, {n} coarse steps, {el:.1f} s"
+    return counted[0] / el, cores, f"{desc}, {n} coarse steps (with updating), {el:.1f} s"
 
 
 def run_reference(args, rank):
@@ -235,7 +275,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5", "paper"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -243,6 +283,10 @@ def main():
     ap.add_argument("--path", type=int, default=0, help="0 auto (grid kernel for uniform levels), 1 generic")
     ap.add_argument("--reflux", action="store_true",
                     help="multi-level configs: conservation fix at coarse-fine interfaces (NEXT-2)")
+    ap.add_argument("--regrid", type=int, default=-1,
+                    help="multi-level configs: regrid every K coarse steps inside the timed region (NEXT-3; "
+                         "claw_regrid_auto of levels 1..L-1, flag tol scaled by dx)")
+    ap.add_argument("--regrid-tol", type=float, default=0.02)
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "host"],
                     help="host: TEST MODE -- halos through host memory over a gloo group "
                          "(claw exchange=1), ranks may share one GPU; never a bench number")
@@ -269,7 +313,11 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     red_dev = "cpu" if host_x else "cuda"
     wl = workload(args.config)
-    nlev = len(wl.levels)
+    dyn = bool(wl.extra.get("ratios"))
+    rat = hierarchy_ratios(wl)
+    nlev = 1 + len(rat)
+    if args.regrid < 0:
+        args.regrid = wl.extra.get("regrid_every", 0) if dyn else 0
     if world > 1 and nlev > 1:
         raise SystemExit("multi-level configs are single-GPU in this version")
 
@@ -296,12 +344,27 @@ def main():
         W.ring_ic(mine, out=buf.numpy())
         g.set_level(L, lv.descs, buf)
         host_q.append(buf)
-    ratios = {L + 1: wl.levels[L + 1].ratio for L in range(nlev - 1)}
-    cells_owned = [g.level_owned(L)[1] for L in range(1, nlev + 1)]
-    mult = [int(np.prod([wl.levels[k].ratio for k in range(1, L + 1)])) for L in range(nlev)]
-    cells_per_step_rank = sum(c * m for c, m in zip(cells_owned, mult))
-    total_cells_per_step = sum(lv.cells * m for lv, m in zip(wl.levels, mult))
     dt = wl.dt0()
+    dx1 = float(wl.levels[0].descs["dx"][0])
+    regrid_ms = []
+    nstep = [0]
+
+    def regrid(t):
+        # every level L < nlev flags and re-creates L+1 (coarsest first)
+        t0 = time.perf_counter()
+        for L in range(1, nlev):
+            if L > 1:
+                g.fill_ghost(L, t)
+            tol, buf, cut, mxd, mnd, R = regrid_params(wl, L, float(g.descs(L)["dx"][0]), dx1, args.regrid_tol)
+            g.regrid_auto(L, tol, buf, cut, mxd, mnd, R)
+        regrid_ms.append(1000.0 * (time.perf_counter() - t0))
+
+    if dyn:
+        regrid(0.0)  # the initial hierarchy from the initial data
+    cells_owned = [g.level_owned(L)[1] for L in range(1, nlev + 1)]
+    mult = [int(np.prod(rat[:L])) for L in range(nlev)]
+    cells_per_step_rank = sum(c * m for c, m in zip(cells_owned, mult))
+    total_cells_per_step = wl.levels[0].cells if nlev == 1 else cells_per_step_rank
     t_sim = [0.0]
 
     def host_exchange():
@@ -335,6 +398,9 @@ def main():
         else:
             # native subcycled coarse step with updating, one host sync
             g.advance_hierarchy(t, dt, update=True)
+            nstep[0] += 1
+            if args.regrid and nstep[0] % args.regrid == 0:
+                regrid(t + dt)
         t_sim[0] = t + dt
 
     for _ in range(max(args.warmup, 3) if args.warmup > 0 else 0):
@@ -354,6 +420,7 @@ def main():
     time.sleep(0.3)
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    regrid_ms.clear()
     ev0.record(stream)
     for _ in range(args.steps):
         step()
@@ -362,6 +429,10 @@ def main():
     clocks.stop()
     ms = ev0.elapsed_time(ev1)
     st = g.stats()
+    if (args.regrid or dyn) and nlev > 1:
+        # the hierarchy changes: count the cell-updates the library performed
+        total_cells_per_step = st["cells_advanced"] / args.steps
+        cells_per_step_rank = total_cells_per_step
     g.set_profiling(False)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
@@ -401,7 +472,35 @@ def main():
 
     # ---- e2e through the public API with host buffers (H2D + steps + D2H)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and dyn:
+        # dynamic hierarchy: H2D of the level-1 data, the initial regrid, K
+        # coarse steps with their regrids, D2H of every level at the end
+        barrier()
+        t0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g.reset_stats()
+        g.set_level(1, wl.levels[0].descs, host_q[0])   # (re)starts the run at t = 0 from host data
+        t_sim[0] = 0.0
+        nstep[0] = 0
+        regrid(0.0)
+        for _ in range(args.steps):
+            step()
+        outs = [torch.empty(g.level_size(L), dtype=torch.float64, pin_memory=True) for L in range(1, nlev + 1)]
+        for L, b in enumerate(outs, start=1):
+            g.read_level(L, b)
+        e1.record(stream)
+        barrier()
+        ems = e0.elapsed_time(e1)
+        wall = (time.perf_counter() - t0) * 1000.0
+        e2e = {"value": g.stats()["cells_advanced"] / (ems / 1000.0), "unit": "cell-updates/s",
+               "h2d_bytes_per_step": 8 * host_q[0].numel() / args.steps,
+               "d2h_bytes_per_step": sum(8 * b.numel() for b in outs) / args.steps + 8,
+               "ms": ems, "wall_ms": wall,
+               "what": "set_level(1) from pinned host data + initial regrid + K x (coarse step + regrids every "
+                       f"{args.regrid}) + read_level of every level (device->pinned host); cell-updates of the "
+                       "timed run"}
+    if not args.no_e2e and not dyn and not (args.regrid and nlev > 1):  # (regridding changes the level arrays)
         out_host = [torch.empty_like(b, pin_memory=True) for b in host_q]
         barrier()
         t0 = time.perf_counter()
@@ -448,9 +547,15 @@ def main():
                 "data": "synthetic",
                 "config": {"workload": wl.name, "note": wl.note, "levels": nlev,
                            "patches": int(sum(len(lv.descs) for lv in wl.levels)),
-                           "cells_per_step": total_cells_per_step, "limiter": "MC", "order_trans": 2,
+                           "cells_per_step": total_cells_per_step, "limiter": wl.limiter, "order_trans": wl.order_trans,
                            "cfl": wl.cfl, "ic": "ring (Clawpack acoustics_2d_radial qinit)",
                            "conservation_fix": bool(args.reflux and nlev > 1),
+                           "regrid_every": args.regrid if nlev > 1 else 0,
+                           "dynamic_hierarchy": dyn,
+                           "limiter_name": {0: "none", 1: "minmod", 2: "superbee", 3: "van Leer", 4: "MC"}[wl.limiter],
+                           "regrids": len(regrid_ms),
+                           "regrid_ms_mean": statistics.mean(regrid_ms) if regrid_ms else None,
+                           "patches_after": [len(g.descs(L)) for L in range(1, nlev + 1)] if nlev > 1 else None,
                            "parallelism": f"patch-partitioned over {world} rank(s), NCCL halo + max all-reduce"
                            if world > 1 else "single GPU",
                            "l2": "state per buffer exceeds L2 (126 MB); no flush needed"

@@ -279,3 +279,74 @@ def cluster(flags: np.ndarray, cutoff: float, max_dim: int, min_dim: int) -> np.
     if rc != 0:
         raise OracleError(f"oracle_cluster rc={rc}")
     return b[:n.value]
+
+
+# ---------------------------------------------------------------------------
+# Regridding driver (DESIGN.md R18/R19): the oracle's composition of the
+# pinned pieces above -- plain numpy loops over the definitions, no sharing
+# with libclaw's claw_regrid_auto.
+# ---------------------------------------------------------------------------
+def cover_map(descs: np.ndarray, domain, nx: int, ny: int) -> np.ndarray:
+    """[ny, nx] uint8: 1 on the cells of the level's patches."""
+    m = np.zeros((ny, nx), np.uint8)
+    for e in descs:
+        i0 = int(round((e["xlower"] - domain[0]) / e["dx"]))
+        j0 = int(round((e["ylower"] - domain[2]) / e["dy"]))
+        m[j0:j0 + e["my"], i0:i0 + e["mx"]] = 1
+    return m
+
+
+def nest_mask(on: np.ndarray) -> np.ndarray:
+    """Nesting mask (R18): cells of the level whose in-domain neighbours
+    within Chebyshev distance 2 all belong to the level."""
+    ny, nx = on.shape
+    off = np.pad(1 - on.astype(np.uint8), 2, constant_values=0)   # out of domain: never a veto
+    bad = np.zeros((ny, nx), np.uint8)
+    for dj in range(5):
+        for di in range(5):
+            bad |= off[dj:dj + ny, di:di + nx]
+    return (on.astype(np.uint8) & (1 - bad)).astype(np.uint8)
+
+
+def split_boxes(boxes, M: np.ndarray, f: np.ndarray) -> np.ndarray:
+    """R18 nesting split: inside each box, the maximal runs of M in every row;
+    a run identical to one of the row below extends that rectangle; pieces
+    without a flag are dropped; pieces of a box ordered by (y0, x0)."""
+    out = []
+    for x0, y0, w, h in np.asarray(boxes, np.int64).reshape(-1, 4).tolist():
+        x1, y1 = x0 + w, y0 + h
+        opened, done = {}, []
+        for J in range(y0, y1 + 1):
+            runs = []
+            if J < y1:
+                I = x0
+                while I < x1:
+                    if not M[J, I]:
+                        I += 1
+                        continue
+                    e = I
+                    while e < x1 and M[J, e]:
+                        e += 1
+                    runs.append((I, e))
+                    I = e
+            for key in sorted(opened):
+                if key not in runs:
+                    done.append((key[0], opened.pop(key), key[1], J))
+            for r in runs:
+                opened.setdefault(r, J)
+        done.sort(key=lambda r: (r[1], r[0]))
+        out += [(a, y, e - a, J - y) for a, y, e, J in done if f[y:J, a:e].any()]
+    return np.array(out, np.int32).reshape(-1, 4)
+
+
+def regrid_auto(o: "Oracle", level: int, tol: float, buffer: int, cutoff: float, max_dim: int,
+                min_dim: int, R: int) -> int:
+    """flag -> buffer (clipped to the nesting mask) -> cluster -> nesting
+    split -> regrid, on the oracle; the ghost frames of `level` must be
+    filled.  Returns the number of new patches."""
+    nx, ny = o.level_shape(level)
+    M = nest_mask(cover_map(o.descs(level), o._dom, nx, ny))
+    f = buffer_flags(o.flag(level, tol), buffer, M)
+    pieces = split_boxes(cluster(f, cutoff, max_dim, min_dim), M, f) if f.any() else np.zeros((0, 4), np.int32)
+    o.regrid(level, pieces, R)
+    return len(pieces)

@@ -12,6 +12,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <array>
 #include <cmath>
 #include <cstdarg>
@@ -23,6 +24,7 @@
 #include <mutex>
 #include <unordered_map>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/claw.h"
@@ -282,6 +284,9 @@ struct Level {
   // updating table (this fine level onto level-1): covered coarse cells and
   // their R*R children
   std::vector<claw::DevUpdate> hu;
+  std::vector<claw::DevUpdateRect> hur;  // rectangles of coarse cells inside one fine patch
+  DevBuf<claw::DevUpdateRect> dur;
+  int32_t hur_max = 0;                   // largest rectangle (coarse cells)
   std::vector<int64_t> hu_src, hu_scs;   // slow entries: R*R (offset, cs) each
   DevBuf<claw::DevUpdate> du;
   DevBuf<int64_t> du_src, du_scs;
@@ -332,6 +337,8 @@ struct claw_ctx {
   cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
   DevBuf<unsigned long long> hier_buf;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_free;  // event pool
+  uint8_t* h_stage = nullptr;  // pinned staging for flag maps (regrid)
+  size_t h_stage_bytes = 0;
 };
 
 namespace {
@@ -551,10 +558,21 @@ int build_geometry(claw_ctx* c, int level, int npatch, const claw_patch_desc* d,
   return CLAW_OK;
 }
 
-// Compress per-cell sources of a patch's padded frame into rectangles.
+// Index of ghost cell (i, j) of an mx x my patch in its frame ring of
+// 4(mx+my)+16 cells: the two rows below, the two rows above (full padded
+// width), then 4 cells per interior row.
+inline int64_t frame_index(int i, int j, int mx, int my) {
+  const int64_t PX = mx + 4;
+  if (j < 0) return (j + 2) * PX + (i + 2);
+  if (j >= my) return 2 * PX + (j - my) * PX + (i + 2);
+  return 4 * PX + 4ll * j + (i < 0 ? i + 2 : 2 + (i - mx));
+}
+inline int64_t frame_size(int mx, int my) { return 4ll * (mx + my) + 16; }
+
+// Compress per-cell sources of a patch's ghost frame (frame_index order)
+// into rectangles.
 void compress_rects(const std::vector<Src>& cell, int mx, int my, std::vector<DevRect>& out) {
-  const int PX = mx + 4;
-  auto at = [&](int i, int j) -> const Src& { return cell[(j + 2) * PX + (i + 2)]; };
+  auto at = [&](int i, int j) -> const Src& { return cell[frame_index(i, j, mx, my)]; };
   struct Run {
     int i0, i1, j0, j1;  // [i0, i1) x [j0, j1)
     int kind;
@@ -563,8 +581,9 @@ void compress_rects(const std::vector<Src>& cell, int mx, int my, std::vector<De
   };
   std::vector<Run> runs;
   std::vector<Run> prev;  // runs of the previous row that can still grow
+  std::vector<Run> row, next;
   for (int j = -2; j <= my + 1; ++j) {
-    std::vector<Run> row;
+    row.clear();
     auto emit_segment = [&](int a, int b) {  // ghost cells [a, b) of row j
       int i = a;
       while (i < b) {
@@ -594,7 +613,7 @@ void compress_rects(const std::vector<Src>& cell, int mx, int my, std::vector<De
       emit_segment(mx, mx + 2);
     }
     // vertical merge with runs ending at row j
-    std::vector<Run> next;
+    next.clear();
     for (Run& r : row) {
       bool merged = false;
       for (Run& p : prev) {
@@ -614,7 +633,7 @@ void compress_rects(const std::vector<Src>& cell, int mx, int my, std::vector<De
     }
     for (Run& p : prev)
       if (p.open) runs.push_back(p);
-    prev = next;
+    prev.swap(next);
     for (Run& p : prev) p.open = true;
   }
   for (Run& p : prev) runs.push_back(p);
@@ -636,7 +655,59 @@ void compress_rects(const std::vector<Src>& cell, int mx, int my, std::vector<De
 // The composite ghost rule (R1, R8-R10) for every padded
 // cell of every owned patch, the halo plan, coarse-interpolation specs, and
 // device tables.
+// Phase timer for CLAW_TRACE_PLAN=1 (stderr), host wall clock.
+struct PhaseTrace {
+  bool on;
+  const char* tag;
+  int level;
+  std::chrono::steady_clock::time_point t;
+  PhaseTrace(const char* tg, int lv)
+      : on(std::getenv("CLAW_TRACE_PLAN") != nullptr), tag(tg), level(lv), t(std::chrono::steady_clock::now()) {}
+  void operator()(const char* what) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[%s L%d] %-10s %8.2f ms\n", tag, level, what,
+                 std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+
+// Host threads for the planner's per-patch loops (results are assembled in
+// patch order, so they do not depend on the thread count).
+int host_threads(int nwork) {
+  static const int hw = [] {
+    const char* e = std::getenv("CLAW_HOST_THREADS");
+    const int n = e ? std::atoi(e) : static_cast<int>(std::thread::hardware_concurrency());
+    return std::max(1, std::min(n, 32));
+  }();
+  return std::max(1, std::min(hw, nwork / 64));
+}
+
+template <class F>
+void parallel_for(int nthr, int n, F&& f) {
+  if (nthr <= 1) {
+    for (int k = 0; k < n; ++k) f(k);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 0; t < nthr; ++t)
+    th.emplace_back([&, t] {
+      for (int k = t; k < n; k += nthr) f(k);
+    });
+  for (auto& x : th) x.join();
+}
+
 int plan_level(claw_ctx* c, int level, Level& L) {
+  static const bool trace = std::getenv("CLAW_TRACE_PLAN") != nullptr;
+  auto tnow = [] { return std::chrono::steady_clock::now(); };
+  auto t_last = tnow();
+  auto lap = [&](const char* what) {
+    if (!trace) return;
+    const auto t = tnow();
+    std::fprintf(stderr, "[plan L%d] %-10s %8.2f ms\n", level,
+                 what, std::chrono::duration<double, std::milli>(t - t_last).count());
+    t_last = t;
+  };
   const claw_config& cfg = c->cfg;
   const int me = cfg.rank, world = cfg.world;
   const int np = L.npatch;
@@ -770,33 +841,34 @@ int plan_level(claw_ctx* c, int level, Level& L) {
     int64_t Ic, Jc, I, J;  // coarse spec inputs (kind 2)
   };
   std::vector<std::vector<Src>> cells(L.owned.size());
-  std::vector<Pending> pend;
 
-  for (int p = 0; p < np; ++p) {
-    if (!need[p]) continue;
+  auto ghost_patch = [&](int p, std::vector<Pending>& pend, std::string& emsg) -> int {
     const int dst_owner = L.owner[p];
     const bool mine = dst_owner == me;
     const int mx = L.desc[p].mx, my = L.desc[p].my, PX = mx + 4;
     const int lp = mine ? L.local[p] : -1;
     if (mine) {
-      cells[lp].assign(static_cast<size_t>(PX) * (my + 4), Src{-1, 0, 0});
-      L.dbg_src[lp].assign(static_cast<size_t>(PX) * (my + 4), 0);
-      L.dbg_remote[lp].assign(static_cast<size_t>(PX) * (my + 4), 0);
+      const size_t nf = static_cast<size_t>(frame_size(mx, my));
+      cells[lp].assign(nf, Src{-1, 0, 0});
+      L.dbg_src[lp].assign(nf, 0);
+      L.dbg_remote[lp].assign(nf, 0);
     }
+    (void)PX;
+    int qlast = -1;
     for (int j = -2; j <= my + 1; ++j)
       for (int i = -2; i <= mx + 1; ++i) {
-        const bool interior = i >= 0 && i < mx && j >= 0 && j < my;
-        const int idx = (j + 2) * PX + (i + 2);
-        if (interior) {
-          if (mine) {
-            L.dbg_src[lp][idx] = (static_cast<int64_t>(p) << 32) | (static_cast<int64_t>(j) << 16) | i;
-            cells[lp][idx] = Src{0, L.off[lp] + static_cast<int64_t>(j) * mx + i, static_cast<int64_t>(mx) * my};
-          }
+        if (i >= 0 && i < mx && j >= 0 && j < my) {  // interior: the kernels address it directly
+          i = mx - 1;
           continue;
         }
+        const int idx = static_cast<int>(frame_index(i, j, mx, my));
         const int64_t I = map_axis(L.i0[p] + i, L.nx, cfg.bc[0], cfg.bc[1]);
         const int64_t J = map_axis(L.j0[p] + j, L.ny, cfg.bc[2], cfg.bc[3]);
-        const int q = L.find(I, J);
+        // neighbouring ghost cells usually share their donor patch
+        if (!(qlast >= 0 && I >= L.i0[qlast] && I < L.i0[qlast] + L.desc[qlast].mx && J >= L.j0[qlast] &&
+              J < L.j0[qlast] + L.desc[qlast].my))
+          qlast = L.find(I, J);
+        const int q = qlast;
         if (q >= 0) {
           const int li = static_cast<int>(I - L.i0[q]), lj = static_cast<int>(J - L.j0[q]);
           const int src_owner = L.owner[q];
@@ -813,7 +885,10 @@ int plan_level(claw_ctx* c, int level, Level& L) {
                 const int64_t raw[4] = {L.Y0 - 2, L.Y0 - 1, L.Y1, L.Y1 + 1};
                 for (int k2 = 0; k2 < 4; ++k2)
                   if (L.hoff[k2] >= 0 && map_axis(raw[k2], L.ny, cfg.bc[2], cfg.bc[3]) == J) kk = k2;
-                if (kk < 0) return fail(c, CLAW_EINVAL, "band halo row not planned");
+                if (kk < 0) {
+                  emsg = "band halo row not planned";
+                  return CLAW_EINVAL;
+                }
                 cells[lp][idx] = Src{1, L.hoff[kk] + I, L.hcs[kk]};
               } else {
                 pend.push_back(Pending{lp, idx, 1, src_owner, 0, 0, 0, 0});
@@ -832,14 +907,35 @@ int plan_level(claw_ctx* c, int level, Level& L) {
           continue;
         }
         if (!mine) continue;
-        if (!C) return fail(c, CLAW_ENEST, "level %d patch %d: ghost cell (%d,%d) has no donor", level, p, i, j);
+        if (!C) {
+          char b[160];
+          std::snprintf(b, sizeof b, "level %d patch %d: ghost cell (%d,%d) has no donor", level, p, i, j);
+          emsg = b;
+          return CLAW_ENEST;
+        }
         const int R = L.ratio;
         const int64_t Ic = I / R, Jc = J / R;
         pend.push_back(Pending{lp, idx, 2, -1, Ic, Jc, I, J});
         L.dbg_src[lp][idx] = -1;
       }
-  }
-
+      return CLAW_OK;
+  };
+  lap("pre");
+  // per patch; in parallel on one rank (every patch is owned, nothing is
+  // sent), the pending frame cells concatenated in patch order afterwards
+  std::vector<std::vector<Pending>> pend_p(np);
+  std::vector<int> rc_p(np, CLAW_OK);
+  std::vector<std::string> msg_p(np);
+  const int nthr = world == 1 ? host_threads(np) : 1;
+  parallel_for(nthr, np, [&](int p) {
+    if (need[p]) rc_p[p] = ghost_patch(p, pend_p[p], msg_p[p]);
+  });
+  lap("ghost-par");
+  for (int p = 0; p < np; ++p)
+    if (rc_p[p]) return fail(c, rc_p[p], "%s", msg_p[p].c_str());
+  std::vector<Pending> pend;
+  for (int p = 0; p < np; ++p) pend.insert(pend.end(), pend_p[p].begin(), pend_p[p].end());
+  lap("ghosts");
   // frame layout: [peer 0 segment][peer 1 segment]...[coarse segment], each [3][n]
   // (band mode: planned above, full halo rows per source rank)
   int64_t fo = L.band ? L.frame_elems : 0;
@@ -888,7 +984,13 @@ int plan_level(claw_ctx* c, int level, Level& L) {
     }
   }
 
-  // rectangles and device patch records
+  lap("frame");
+  // rectangles (per patch, in parallel) and device patch records
+  std::vector<std::vector<DevRect>> rects_p(L.owned.size());
+  parallel_for(world == 1 ? host_threads(static_cast<int>(L.owned.size())) : 1, static_cast<int>(L.owned.size()),
+               [&](int lp) {
+                 compress_rects(cells[lp], L.desc[L.owned[lp]].mx, L.desc[L.owned[lp]].my, rects_p[lp]);
+               });
   L.hpatch.clear();
   L.hrect.clear();
   for (size_t lp = 0; lp < L.owned.size(); ++lp) {
@@ -899,7 +1001,7 @@ int plan_level(claw_ctx* c, int level, Level& L) {
     d.mx = L.desc[p].mx;
     d.my = L.desc[p].my;
     d.rect_begin = static_cast<int32_t>(L.hrect.size());
-    compress_rects(cells[lp], d.mx, d.my, L.hrect);
+    L.hrect.insert(L.hrect.end(), rects_p[lp].begin(), rects_p[lp].end());
     d.rect_end = static_cast<int32_t>(L.hrect.size());
     // regions: strips W (i in [-2,0), j in [0,my)), E, S, N and 2x2 corners
     // SW, SE, NW, NE, each covered by one rectangle (or -1)
@@ -922,6 +1024,7 @@ int plan_level(claw_ctx* c, int level, Level& L) {
     d.Z = L.desc[p].rho * d.c;
     L.hpatch.push_back(d);
   }
+  lap("rects");
   // tiles: strips of <= 32 columns x <= tile_rows rows, largest first
   L.uniform = true;
   for (size_t lp = 1; lp < L.hpatch.size(); ++lp)
@@ -991,9 +1094,12 @@ int plan_level(claw_ctx* c, int level, Level& L) {
   L.ntile_interior = 0;
   while (L.ntile_interior < static_cast<int64_t>(L.htile.size()) && !remote[L.htile[L.ntile_interior].x])
     ++L.ntile_interior;
+  lap("tiles");
   // updating table: coarse cells (level-1) whose R x R children are all
   // interior cells of this level
   L.hu.clear();
+  L.hur.clear();
+  L.hur_max = 0;
   L.hu_src.clear();
   L.hu_scs.clear();
   if (C && world == 1) {
@@ -1001,10 +1107,50 @@ int plan_level(claw_ctx* c, int level, Level& L) {
     for (int fp = 0; fp < np; ++fp) {
       const int64_t ic0 = L.i0[fp] / R, ic1 = (L.i0[fp] + L.desc[fp].mx - 1) / R;
       const int64_t jc0 = L.j0[fp] / R, jc1 = (L.j0[fp] + L.desc[fp].my - 1) / R;
+      const int64_t fi0 = L.i0[fp], fi1 = L.i0[fp] + L.desc[fp].mx, fj0 = L.j0[fp], fj1 = L.j0[fp] + L.desc[fp].my;
+      // coarse cells whose R x R children all lie in this patch: rectangles
+      // (one per overlapping coarse patch), averaged by one CTA each
+      const int64_t ia = (fi0 + R - 1) / R, ib = fi1 / R, ja = (fj0 + R - 1) / R, jb = fj1 / R;
+      if (ia < ib && ja < jb) {
+        std::vector<int> cand;
+        for (int64_t by = ja / kBucket; by <= (jb - 1) / kBucket && by < C->nby; ++by)
+          for (int64_t bx = ia / kBucket; bx <= (ib - 1) / kBucket && bx < C->nbx; ++bx)
+            for (int64_t k = C->bstart[by * C->nbx + bx]; k < C->bstart[by * C->nbx + bx + 1]; ++k)
+              cand.push_back(C->blist[k]);
+        std::sort(cand.begin(), cand.end());
+        cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+        for (int cq : cand) {
+          const int64_t x0 = std::max(ia, C->i0[cq]), x1 = std::min(ib, C->i0[cq] + C->desc[cq].mx);
+          const int64_t y0 = std::max(ja, C->j0[cq]), y1 = std::min(jb, C->j0[cq] + C->desc[cq].my);
+          if (x0 >= x1 || y0 >= y1) continue;
+          const int lc = C->local[cq];
+          claw::DevUpdateRect r{};
+          r.dst = C->off[lc] + (y0 - C->j0[cq]) * C->desc[cq].mx + (x0 - C->i0[cq]);
+          r.src = L.off[L.local[fp]] + (y0 * R - fj0) * L.desc[fp].mx + (x0 * R - fi0);
+          r.dcs = static_cast<int64_t>(C->desc[cq].mx) * C->desc[cq].my;
+          r.fcs = static_cast<int64_t>(L.desc[fp].mx) * L.desc[fp].my;
+          r.cmx = C->desc[cq].mx;
+          r.fmx = L.desc[fp].mx;
+          r.w = static_cast<int32_t>(x1 - x0);
+          r.h = static_cast<int32_t>(y1 - y0);
+          L.hur.push_back(r);
+          L.hur_max = std::max(L.hur_max, r.w * r.h);
+        }
+      }
+      // the rest of the footprint (patches not aligned to the coarse cells):
+      // cell by cell
+      int cq = -1;
       for (int64_t Jc = jc0; Jc <= jc1; ++Jc)
         for (int64_t Ic = ic0; Ic <= ic1; ++Ic) {
-          const int cq = C->find(Ic, Jc);
+          if (Jc >= ja && Jc < jb && Ic >= ia && Ic < ib) {
+            Ic = ib - 1;
+            continue;
+          }
+          if (cq < 0 || Ic < C->i0[cq] || Ic >= C->i0[cq] + C->desc[cq].mx || Jc < C->j0[cq] ||
+              Jc >= C->j0[cq] + C->desc[cq].my)
+            cq = C->find(Ic, Jc);
           if (cq < 0) continue;
+          const int lc = C->local[cq];
           // each coarse cell once: only from the fine patch holding its first child
           if (L.find(Ic * R, Jc * R) != fp) continue;
           bool all = true, one = true;
@@ -1022,7 +1168,6 @@ int plan_level(claw_ctx* c, int level, Level& L) {
               sc.push_back(static_cast<int64_t>(L.desc[q].mx) * L.desc[q].my);
             }
           if (!all) continue;
-          const int lc = C->local[cq];
           claw::DevUpdate u{};
           u.dst = C->off[lc] + (Jc - C->j0[cq]) * C->desc[cq].mx + (Ic - C->i0[cq]);
           u.dcs = C->desc[cq].mx * C->desc[cq].my;
@@ -1041,6 +1186,7 @@ int plan_level(claw_ctx* c, int level, Level& L) {
         }
     }
   }
+  lap("update");
   // conservation-fix registers (same order as the oracle's: coarse patch, row,
   // column, then neighbours x-, x+, y-, y+)
   L.hreg.clear();
@@ -1158,6 +1304,7 @@ int alloc_level(claw_ctx* ctx, int level, Level& L) {
   if (int r2 = upload(ctx, L.dtile, L.htile)) return r2;
   if (int r2 = upload(ctx, L.dinterp, L.hinterp)) return r2;
   if (int r2 = upload(ctx, L.du, L.hu)) return r2;
+  if (int r2 = upload(ctx, L.dur, L.hur)) return r2;
   if (int r2 = upload(ctx, L.du_src, L.hu_src)) return r2;
   if (int r2 = upload(ctx, L.du_scs, L.hu_scs)) return r2;
   if (int r2 = upload(ctx, L.dreg, L.hreg)) return r2;
@@ -1321,6 +1468,7 @@ int claw_destroy(claw_ctx* ctx) {
   ctx->hier_buf.reset();
   if (ctx->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(ctx->comm);
   if (ctx->h_cfl) cudaFreeHost(ctx->h_cfl);
+  if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
   if (ctx->ev_ready) cudaEventDestroy(ctx->ev_ready);
@@ -1714,9 +1862,12 @@ int claw_update_level(claw_ctx* ctx, int32_t level) {
     return fail(ctx, CLAW_ESTATE, "update: level %d (t=%.17g) has not caught up with level %d (t=%.17g)", level,
                 F.t_new, level - 1, C.t_new);
   const int64_t n = static_cast<int64_t>(F.hu.size());
+  CUDA_TRY(static_cast<cudaError_t>(claw::launch_update_rects(C.q[C.cur].p, F.q[F.cur].p, F.dur.p,
+                                                              static_cast<int32_t>(F.hur.size()), F.ratio,
+                                                              F.hur_max, ctx->stream)));
   CUDA_TRY(static_cast<cudaError_t>(claw::launch_update(C.q[C.cur].p, F.q[F.cur].p, F.du.p, n, F.ratio,
                                                         F.du_src.p, F.du_scs.p, ctx->stream)));
-  ctx->stats.ghost_launches++;
+  ctx->stats.ghost_launches += (F.hur.empty() ? 0 : 1) + (n > 0 ? 1 : 0);
   if (ctx->cfg.reflux && !F.hreg.empty()) {
     CUDA_TRY(static_cast<cudaError_t>(claw::launch_reflux_apply(C.q[C.cur].p, C.dpatch.p, F.dreg.p, F.dheads.p,
                                                                 static_cast<int64_t>(F.hheads.size()) - 1, F.racc.p,
@@ -1809,11 +1960,16 @@ int claw_debug_ghost_sources(const claw_ctx* ctx, int32_t level, int32_t patch, 
   const Level& L = ctx->lev[level];
   if (patch < 0 || patch >= L.npatch || L.local[patch] < 0) return CLAW_EINVAL;
   const auto& v = L.dbg_src[L.local[patch]];
-  std::memcpy(out, v.data(), v.size() * sizeof(int64_t));
-  if (out2) {
-    const auto& w = L.dbg_remote[L.local[patch]];
-    std::memcpy(out2, w.data(), w.size() * sizeof(int64_t));
-  }
+  const auto& w = L.dbg_remote[L.local[patch]];
+  const int mx = L.desc[patch].mx, my = L.desc[patch].my, PX = mx + 4;
+  for (int j = -2; j <= my + 1; ++j)
+    for (int i = -2; i <= mx + 1; ++i) {
+      const int64_t o = static_cast<int64_t>(j + 2) * PX + (i + 2);
+      const bool interior = i >= 0 && i < mx && j >= 0 && j < my;
+      const int64_t f = interior ? -1 : frame_index(i, j, mx, my);
+      out[o] = interior ? (static_cast<int64_t>(patch) << 32) | (static_cast<int64_t>(j) << 16) | i : v[f];
+      if (out2) out2[o] = interior ? 0 : w[f];
+    }
   return CLAW_OK;
 }
 
@@ -1889,24 +2045,42 @@ namespace {
 // sides; no admissible cut: accept.  Low part before high part.
 struct Clusterer {
   int64_t nx, ny;
-  std::vector<int64_t> sat;  // (ny+1) x (nx+1) prefix counts
+  std::vector<int32_t> sat;  // (ny+1) x (nx+1) prefix counts (maps < 2^31 cells)
   double cutoff;
   int maxd, mind;
   std::vector<int32_t> out;  // (x0, y0, w, h) quadruples
 
   Clusterer(const uint8_t* f, int64_t nx_, int64_t ny_, double c, int mx, int mn)
-      : nx(nx_), ny(ny_), sat(static_cast<size_t>((nx_ + 1) * (ny_ + 1)), 0), cutoff(c), maxd(mx), mind(mn) {
-    for (int64_t J = 0; J < ny; ++J) {
-      int64_t run = 0;
+      : nx(nx_), ny(ny_), sat(static_cast<size_t>((nx_ + 1) * (ny_ + 1))), cutoff(c), maxd(mx), mind(mn) {
+    const int64_t W = nx + 1;
+    const int nt = host_threads(static_cast<int>(std::min<int64_t>(ny, 1 << 20)) * 4);
+    // row prefix sums (rows in parallel), then running sums down each column
+    // (column blocks in parallel)
+    std::fill(sat.begin(), sat.begin() + W, 0);
+    parallel_for(nt, static_cast<int>(ny), [&](int J) {
+      int32_t run = 0;
+      int32_t* row = sat.data() + (J + 1) * W;
+      row[0] = 0;
+      const uint8_t* fr = f + static_cast<int64_t>(J) * nx;
       for (int64_t I = 0; I < nx; ++I) {
-        run += f[J * nx + I] ? 1 : 0;
-        sat[(J + 1) * (nx + 1) + I + 1] = sat[J * (nx + 1) + I + 1] + run;
+        run += fr[I] ? 1 : 0;
+        row[I + 1] = run;
       }
-    }
+    });
+    const int64_t blk = 256;
+    const int nb = static_cast<int>((W + blk - 1) / blk);
+    parallel_for(std::min(nt, nb), nb, [&](int b) {
+      const int64_t a0 = b * blk, a1 = std::min(W, a0 + blk);
+      for (int64_t J = 1; J <= ny; ++J) {
+        int32_t* r = sat.data() + J * W;
+        const int32_t* q = r - W;
+        for (int64_t I = a0; I < a1; ++I) r[I] += q[I];
+      }
+    });
   }
   int64_t count(int64_t x0, int64_t y0, int64_t x1, int64_t y1) const {  // [x0,x1) x [y0,y1)
     const int64_t W = nx + 1;
-    return sat[y1 * W + x1] - sat[y0 * W + x1] - sat[y1 * W + x0] + sat[y0 * W + x0];
+    return static_cast<int64_t>(sat[y1 * W + x1]) - sat[y0 * W + x1] - sat[y1 * W + x0] + sat[y0 * W + x0];
   }
   void emit(int64_t x0, int64_t y0, int64_t w, int64_t h) {
     out.push_back(static_cast<int32_t>(x0));
@@ -2028,7 +2202,7 @@ int claw_level_descs(const claw_ctx* ctx, int32_t level, claw_patch_desc* out) {
 int claw_cluster(const uint8_t* flags, int64_t nx, int64_t ny, double cutoff, int32_t max_dim, int32_t min_dim,
                  int32_t* boxes, int32_t cap, int32_t* nbox) {
   if (!flags || nx < 1 || ny < 1 || !(cutoff > 0.0) || cutoff > 1.0 || max_dim < 1 || min_dim < 1 ||
-      2 * min_dim > max_dim || !nbox || nx >= (1ll << 31) || ny >= (1ll << 31))
+      2 * min_dim > max_dim || !nbox || nx >= (1ll << 31) || ny >= (1ll << 31) || nx * ny >= (1ll << 31))
     return CLAW_EINVAL;
   Clusterer cl(flags, nx, ny, cutoff, max_dim, min_dim);
   cl.run();
@@ -2133,6 +2307,10 @@ int claw_regrid(claw_ctx* ctx, int32_t level, int32_t nbox, const int32_t* boxes
       return fail(ctx, CLAW_EINVAL, "regrid: box %d (%d,%d,%d,%d) outside level %d's index space", b, x[0], x[1],
                   x[2], x[3], level);
   }
+  if (ctx->lev[level + 1].set && nbox > 0 && ctx->lev[level + 1].ratio != R)
+    return fail(ctx, CLAW_EINVAL, "regrid: R=%d differs from the existing level %d's ratio %d", R, level + 1,
+                ctx->lev[level + 1].ratio);
+  PhaseTrace lap("regrid", level);
   if (!ctx->host_only) CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   Level old = std::move(ctx->lev[level + 1]);
   for (int l = level + 1; l <= kMaxLevel; ++l) ctx->lev[l] = Level();
@@ -2158,93 +2336,75 @@ int claw_regrid(claw_ctx* ctx, int32_t level, int32_t nbox, const int32_t* boxes
     L = Level();
     return rc;
   }
-  // copy rectangles (old fine cells at the same place) and interpolation
-  // cells (the rest), built per new patch
-  std::vector<claw::DevCopyRect> rects;
-  std::vector<claw::DevRegridCell> cells;
-  for (int p = 0; p < nbox; ++p) {
-    const int lp = L.local[p];
-    const int mx = d[p].mx, my = d[p].my;
-    const int64_t I0 = L.i0[p], J0 = L.j0[p];
-    const int bw = boxes[4 * p + 2], bh = boxes[4 * p + 3];
-    std::vector<int32_t> cover(static_cast<size_t>(bw) * bh, 0);  // copied fine cells per coarse cell
-    if (old.set) {
-      std::vector<int> cand;
-      const int64_t bx0 = I0 / kBucket, bx1 = std::min(old.nbx - 1, (I0 + mx - 1) / kBucket);
-      const int64_t by0 = J0 / kBucket, by1 = std::min(old.nby - 1, (J0 + my - 1) / kBucket);
-      for (int64_t by = by0; by <= by1; ++by)
-        for (int64_t bx = bx0; bx <= bx1; ++bx)
-          for (int64_t k = old.bstart[by * old.nbx + bx]; k < old.bstart[by * old.nbx + bx + 1]; ++k)
-            cand.push_back(old.blist[k]);
-      std::sort(cand.begin(), cand.end());
-      cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
-      for (int q : cand) {
-        const int64_t x0 = std::max(I0, old.i0[q]), x1 = std::min(I0 + mx, old.i0[q] + old.desc[q].mx);
-        const int64_t y0 = std::max(J0, old.j0[q]), y1 = std::min(J0 + my, old.j0[q] + old.desc[q].my);
-        if (x0 >= x1 || y0 >= y1) continue;
-        const int lq = old.local[q];
-        claw::DevCopyRect r{};
-        r.src = old.off[lq] + (y0 - old.j0[q]) * old.desc[q].mx + (x0 - old.i0[q]);
-        r.dst = L.off[lp] + (y0 - J0) * mx + (x0 - I0);
-        r.scs = static_cast<int64_t>(old.desc[q].mx) * old.desc[q].my;
-        r.dcs = static_cast<int64_t>(mx) * my;
-        r.smx = old.desc[q].mx;
-        r.dmx = mx;
-        r.w = static_cast<int32_t>(x1 - x0);
-        r.h = static_cast<int32_t>(y1 - y0);
-        rects.push_back(r);
-        for (int64_t J = y0; J < y1; ++J)
-          for (int64_t I = x0; I < x1; ++I) cover[((J - J0) / R) * bw + (I - I0) / R]++;
-      }
-    }
-    for (int cj = 0; cj < bh; ++cj)
-      for (int ci = 0; ci < bw; ++ci) {
-        claw::DevRegridCell e{};
-        e.dst = L.off[lp] + static_cast<int64_t>(cj) * R * mx + static_cast<int64_t>(ci) * R;
-        e.dcs = static_cast<int64_t>(mx) * my;
-        e.fmx = mx;
-        const int64_t Ic = boxes[4 * p + 0] + ci, Jc = boxes[4 * p + 1] + cj;
-        const bool copied = cover[cj * bw + ci] == R * R;
-        const int64_t cI[5] = {Ic, map_axis(Ic - 1, C.nx, ctx->cfg.bc[0], ctx->cfg.bc[1]),
-                               map_axis(Ic + 1, C.nx, ctx->cfg.bc[0], ctx->cfg.bc[1]), Ic, Ic};
-        const int64_t cJ[5] = {Jc, Jc, Jc, map_axis(Jc - 1, C.ny, ctx->cfg.bc[2], ctx->cfg.bc[3]),
-                               map_axis(Jc + 1, C.ny, ctx->cfg.bc[2], ctx->cfg.bc[3])};
-        bool ok = !copied;
-        for (int k = 0; k < 5 && ok; ++k) {
-          const int q = C.find(cI[k], cJ[k]);
-          if (q < 0) {
-            L = Level();
-            return fail(ctx, CLAW_ENEST, "regrid: new cell over level-%d cell (%lld,%lld) needs level-%d cell "
-                        "(%lld,%lld), which is not on the level", level, (long long)Ic, (long long)Jc, level,
-                        (long long)cI[k], (long long)cJ[k]);
-          }
-          e.off[k] = C.off[C.local[q]] + (cJ[k] - C.j0[q]) * C.desc[q].mx + (cI[k] - C.i0[q]);
-          e.cs[k] = static_cast<int64_t>(C.desc[q].mx) * C.desc[q].my;
-        }
-        if (!ok) e.off[0] = -1;
-        cells.push_back(e);
-      }
-  }
+  lap("plan");
   L.t_old = L.t_new = C.t_new;
+  lap("tables");
   if (ctx->host_only) {
     L.set = true;
     return CLAW_OK;
   }
   if (int r2 = alloc_level(ctx, level + 1, L)) return r2;
+  lap("alloc");
   L.cur = 0;
-  DevBuf<claw::DevRegridCell> dcells;
-  DevBuf<claw::DevCopyRect> drects;
-  if (int r2 = upload(ctx, dcells, cells)) return r2;
-  if (int r2 = upload(ctx, drects, rects)) return r2;
   CUDA_TRY(cudaStreamSynchronize(nullptr));  // alloc_level's legacy-stream memsets
-  CUDA_TRY(static_cast<cudaError_t>(claw::launch_regrid(C.q[1 - C.cur].p, C.q[C.cur].p, dcells.p,
-                                                        static_cast<int64_t>(cells.size()), R,
-                                                        old.set ? old.q[old.cur].p : nullptr, drects.p,
-                                                        static_cast<int32_t>(rects.size()), L.q[0].p, ctx->stream)));
+  // patch-id maps (coarse level; old fine level) and origins, all on the
+  // device: no per-cell host work (P:373 runs regridding on the GPU)
+  auto origins = [](const Level& X) {
+    std::vector<int2> o(X.owned.size());
+    for (size_t lp = 0; lp < X.owned.size(); ++lp)
+      o[lp] = make_int2(static_cast<int>(X.i0[X.owned[lp]]), static_cast<int>(X.j0[X.owned[lp]]));
+    return o;
+  };
+  DevBuf<int32_t> cmap, omap, err;
+  DevBuf<int2> corig, oorig, norig;
+  if (int r2 = upload(ctx, corig, origins(C))) return r2;
+  if (int r2 = upload(ctx, norig, origins(L))) return r2;
+  CUDA_TRY(cmap.alloc(C.nx * C.ny));
+  CUDA_TRY(err.alloc(1));
+  CUDA_TRY(cudaMemsetAsync(cmap.p, 0xff, C.nx * C.ny * 4, ctx->stream));
+  CUDA_TRY(cudaMemsetAsync(err.p, 0, 4, ctx->stream));
+  CUDA_TRY(static_cast<cudaError_t>(claw::launch_paint(cmap.p, C.nx, corig.p, C.dpatch.p,
+                                                       static_cast<int32_t>(C.owned.size()), ctx->stream)));
+  claw::RegridParams P{};
+  if (old.set) {
+    if (int r2 = upload(ctx, oorig, origins(old))) return r2;
+    CUDA_TRY(omap.alloc(old.nx * old.ny));
+    CUDA_TRY(cudaMemsetAsync(omap.p, 0xff, old.nx * old.ny * 4, ctx->stream));
+    CUDA_TRY(static_cast<cudaError_t>(claw::launch_paint(omap.p, old.nx, oorig.p, old.dpatch.p,
+                                                         static_cast<int32_t>(old.owned.size()), ctx->stream)));
+    P.qf_old = old.q[old.cur].p;
+    P.oldmap = omap.p;
+    P.opatch = old.dpatch.p;
+    P.oorig = oorig.p;
+  }
+  P.qc_old = C.q[1 - C.cur].p;
+  P.qc_new = C.q[C.cur].p;
+  P.cmap = cmap.p;
+  P.cpatch = C.dpatch.p;
+  P.corig = corig.p;
+  P.cnx = C.nx;
+  P.cny = C.ny;
+  P.fnx = L.nx;
+  P.qf = L.q[0].p;
+  P.npatch = L.dpatch.p;
+  P.norig = norig.p;
+  P.R = R;
+  P.per_x = ctx->cfg.bc[0] == CLAW_BC_PERIODIC;
+  P.per_y = ctx->cfg.bc[2] == CLAW_BC_PERIODIC;
+  P.err = err.p;
+  CUDA_TRY(static_cast<cudaError_t>(claw::launch_regrid(P, static_cast<int32_t>(L.owned.size()), ctx->stream)));
+  int32_t herr = 0;
+  CUDA_TRY(cudaMemcpyAsync(&herr, err.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaMemcpyAsync(L.q[1].p, L.q[0].p, L.buf_elems * 8, cudaMemcpyDeviceToDevice, ctx->stream));
   CUDA_TRY(cudaMemsetAsync(L.frame.p, 0, L.frame.n * 8, ctx->stream));
-  CUDA_TRY(cudaStreamSynchronize(ctx->stream));  // the old level and the tables go back to the pool
-  ctx->stats.ghost_launches += 2;
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));  // the old level and the maps go back to the pool
+  if (herr) {
+    L = Level();
+    return fail(ctx, CLAW_ENEST, "regrid: a new level-%d cell to interpolate has a coarse donor that is not on "
+                "level %d", level + 1, level);
+  }
+  lap("kernels");
+  ctx->stats.ghost_launches += old.set ? 3 : 2;
   L.set = true;
   return CLAW_OK;
 }
@@ -2258,29 +2418,44 @@ int claw_regrid_auto(claw_ctx* ctx, int32_t level, double tol, int32_t buffer, d
   if (buffer < 0) return fail(ctx, CLAW_EINVAL, "buffer=%d", buffer);
   const Level& C = ctx->lev[level];
   const int64_t n = C.nx * C.ny;
+  PhaseTrace lap("auto", level);
   DevBuf<uint8_t> out, on;
   int64_t nflag = 0;
   if (int rc = flag_device(ctx, level, tol, buffer, 2, out, on, &nflag)) return rc;
-  std::vector<uint8_t> f(n), m(n);
-  CUDA_TRY(cudaMemcpyAsync(f.data(), out.p, n, cudaMemcpyDeviceToHost, ctx->stream));
-  CUDA_TRY(cudaMemcpyAsync(m.data(), on.p, n, cudaMemcpyDeviceToHost, ctx->stream));
+  lap("flag");
+  if (ctx->h_stage_bytes < static_cast<size_t>(2 * n)) {
+    if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+    ctx->h_stage = nullptr;
+    ctx->h_stage_bytes = 0;
+    CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_stage), static_cast<size_t>(2 * n)));
+    ctx->h_stage_bytes = static_cast<size_t>(2 * n);
+  }
+  const uint8_t* f = ctx->h_stage;
+  const uint8_t* m = ctx->h_stage + n;
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_stage, out.p, n, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_stage + n, on.p, n, cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   std::vector<int32_t> boxes;
   if (nflag > 0) {
     if (!(cutoff > 0.0) || cutoff > 1.0 || max_dim < 1 || min_dim < 1 || 2 * min_dim > max_dim)
       return fail(ctx, CLAW_EINVAL, "cluster: cutoff=%g max_dim=%d min_dim=%d", cutoff, max_dim, min_dim);
-    Clusterer cl(f.data(), C.nx, C.ny, cutoff, max_dim, min_dim);
+    if (n >= (1ll << 31)) return fail(ctx, CLAW_EINVAL, "regrid_auto: flag map of %lld cells", (long long)n);
+    Clusterer cl(f, C.nx, C.ny, cutoff, max_dim, min_dim);
     cl.run();
     // nesting: split each box into row-run rectangles of the nesting mask M
-    // (runs identical in consecutive rows merge), drop pieces without flags
-    Clusterer fs(f.data(), C.nx, C.ny, 1.0, 2, 1);  // only for its prefix counts
-    for (size_t b = 0; b < cl.out.size(); b += 4) {
+    // (runs identical in consecutive rows merge), drop pieces without flags;
+    // boxes in parallel, pieces concatenated in box order
+    const int nbx = static_cast<int>(cl.out.size() / 4);
+    std::vector<std::vector<int32_t>> piece(nbx);
+    parallel_for(host_threads(nbx * 16), nbx, [&](int bi) {
+      const size_t b = 4 * static_cast<size_t>(bi);
       const int64_t x0 = cl.out[b], y0 = cl.out[b + 1], x1 = x0 + cl.out[b + 2], y1 = y0 + cl.out[b + 3];
       struct Open { int64_t a, e, y; };
       std::vector<Open> open, next;
       std::vector<std::array<int64_t, 4>> done;
+      std::vector<std::pair<int64_t, int64_t>> runs;
       for (int64_t J = y0; J <= y1; ++J) {
-        std::vector<std::pair<int64_t, int64_t>> runs;
+        runs.clear();
         if (J < y1)
           for (int64_t I = x0; I < x1;) {
             if (!m[J * C.nx + I]) {
@@ -2313,17 +2488,21 @@ int claw_regrid_auto(claw_ctx* ctx, int32_t level, double tol, int32_t buffer, d
         return a[1] != b[1] ? a[1] < b[1] : a[0] < b[0];
       });
       for (auto& r : done)
-        if (fs.count(r[0], r[1], r[2], r[3]) > 0) {
-          boxes.push_back(static_cast<int32_t>(r[0]));
-          boxes.push_back(static_cast<int32_t>(r[1]));
-          boxes.push_back(static_cast<int32_t>(r[2] - r[0]));
-          boxes.push_back(static_cast<int32_t>(r[3] - r[1]));
+        if (cl.count(r[0], r[1], r[2], r[3]) > 0) {
+          piece[bi].push_back(static_cast<int32_t>(r[0]));
+          piece[bi].push_back(static_cast<int32_t>(r[1]));
+          piece[bi].push_back(static_cast<int32_t>(r[2] - r[0]));
+          piece[bi].push_back(static_cast<int32_t>(r[3] - r[1]));
         }
-    }
+    });
+    for (auto& pc : piece) boxes.insert(boxes.end(), pc.begin(), pc.end());
   }
   const int32_t nb = static_cast<int32_t>(boxes.size() / 4);
+  lap("cluster");
   if (nbox_out) *nbox_out = nb;
-  return claw_regrid(ctx, level, nb, boxes.data(), R);
+  const int rc = claw_regrid(ctx, level, nb, boxes.data(), R);
+  lap("regrid");
+  return rc;
 }
 
 int claw_pool_stats(int64_t* hits, int64_t* misses, int64_t* cached_bytes) {

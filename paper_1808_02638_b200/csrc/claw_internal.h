@@ -114,6 +114,16 @@ struct DevUpdate {
   int32_t fmx, slow;
 };
 static_assert(sizeof(DevUpdate) == 32, "DevUpdate layout");
+// Updating rectangle: w x h coarse cells (row pitch cmx) whose R x R children
+// all lie in one fine patch (row pitch fmx); dst / src: offsets of the first
+// coarse cell and of its first child (p components).
+struct DevUpdateRect {
+  int64_t dst, src;
+  int64_t dcs, fcs;
+  int32_t cmx, fmx, w, h;
+};
+int launch_update_rects(double* q_coarse, const double* q_fine, const DevUpdateRect* rects, int32_t n, int R,
+                        int32_t max_cells, void* stream);
 int launch_update(double* q_coarse, const double* q_fine, const DevUpdate* tab, int64_t n, int R,
                   const int64_t* slow_off, const int64_t* slow_cs, void* stream);
 // Conservation-fix register of a fine level (NEXT-2, R17): coarse
@@ -148,24 +158,33 @@ int launch_flag(const StepParams& p, const int2* orig, int32_t nown, int64_t nx,
 int launch_dilate(const uint8_t* in, uint8_t* tmp, uint8_t* out, const uint8_t* mask, int64_t nx, int64_t ny, int b,
                   unsigned long long* count, void* stream);
 int launch_not(const uint8_t* in, uint8_t* out, int64_t n, void* stream);
-// New fine level: coarse cell e of a new box supplies its R x R children by
-// the R10 interpolation at alpha = 1 (off[0] < 0: skip, every child is copied
-// from the old fine level); children at dst + b*fmx + a (component stride dcs).
-struct DevRegridCell {
-  int64_t off[5];
-  int64_t cs[5];
-  int64_t dst, dcs;
-  int32_t fmx, pad;
+// Patch-id map of a level's index space: map[J*nx + I] = owned patch index
+// or -1 (map memset to 0xff first); one CTA per patch paints its rectangle.
+int launch_paint(int32_t* map, int64_t nx, const int2* orig, const DevPatch* patches, int32_t npatch, void* stream);
+// New fine level (regrid): one CTA per new patch, one thread per cell.  A cell
+// takes the old fine level's value where oldmap (fine index space, may be
+// null) names a patch, else the R10 interpolation at alpha = 1 from the
+// coarse level (donors through cmap and the BCs); a missing donor sets *err.
+struct RegridParams {
+  const double* qc_old;
+  const double* qc_new;
+  const int32_t* cmap;
+  const DevPatch* cpatch;
+  const int2* corig;
+  int64_t cnx, cny;
+  const double* qf_old;
+  const int32_t* oldmap;
+  const DevPatch* opatch;
+  const int2* oorig;
+  int64_t fnx;
+  double* qf;
+  const DevPatch* npatch;
+  const int2* norig;
+  int32_t R;
+  int32_t per_x, per_y;
+  int32_t* err;
 };
-// Copy rectangle from the old fine level (same level index space).
-struct DevCopyRect {
-  int64_t src, dst;    // offsets (p component) of the rectangle's first cell
-  int64_t scs, dcs;    // component strides
-  int32_t smx, dmx;    // row pitches
-  int32_t w, h;
-};
-int launch_regrid(const double* qc_old, const double* qc_new, const DevRegridCell* cells, int64_t ncell, int R,
-                  const double* qf_old, const DevCopyRect* rects, int32_t nrect, double* qf, void* stream);
+int launch_regrid(const RegridParams& p, int32_t nnew, void* stream);
 int max_tile_rows();
 int grid_strip();
 

@@ -303,6 +303,24 @@ def c3(w2: float = 0.45, w3: float = 0.40) -> Workload:
                     note=f"3 levels R=(2,4): {len(b1)} + {len(b2)} + {len(b3)} patches")
 
 
+def paper(n1: int = 1000, npx: int = 4) -> Workload:
+    """NEXT-4, the paper's own benchmark shape: 3 levels
+    with refinement ratio 2 between levels, a 1000 x 1000 base level in
+    patches of at most 260 x 260 (here 4 x 4 patches of 250^2), the van Leer
+    limiter with corner transport (order_trans 2), the ring, double precision.
+    Levels 2 and 3 are not fixed: they are created by flagging and
+    Berger-Rigoutsos clustering (cutoff 0.7) at t = 0 and re-created every 8
+    coarse steps (regrid interval 8), with a buffer of 8 coarse cells
+    (R19).  Flag: pressure jump to a neighbour above
+    tol_per_dx * dx of the flagged level (a gradient threshold)."""
+    l1 = uniform_level(npx, npx, n1 // npx, n1 // npx)
+    return Workload(f"paper_3level_r2_vanleer_{n1}", [Level(l1)], limiter=3, order_trans=2, steps=40,
+                    note=f"paper-shaped dynamic AMR: base {n1}^2 ({npx}x{npx} patches), 3 levels R=2, "
+                         "van Leer, regrid every 8 coarse steps (cutoff 0.7)",
+                    extra={"ratios": [2, 2], "regrid_every": 8, "cutoff": 0.7, "max_dim": 130, "min_dim": 8,
+                           "tol_per_dx": 2.0, "buffer_coarse_cells": 8})
+
+
 def hierarchy_ic(wl: Workload) -> list:
     """Ring initial data point-sampled on every level."""
     return [ring_ic(L.descs) for L in wl.levels]

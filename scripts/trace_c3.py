@@ -5,10 +5,17 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_1808_02638_b200 import binding, workloads as W
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c3"
-wl = {"c2": W.c2, "c3": W.c3}[cfg]()
+wl = {"c2": W.c2, "c3": W.c3, "paper": W.paper}[cfg]()
 g = binding.Claw(wl.domain, wl.bc, wl.limiter, wl.order_trans, device=0)
 for L, (lev, q) in enumerate(zip(wl.levels, W.hierarchy_ic(wl)), start=1):
     g.set_level(L, lev.descs, q)
+if wl.extra.get("ratios"):  # dynamic: the initial hierarchy by regridding
+    import bench
+    dx1 = float(wl.levels[0].descs["dx"][0])
+    for L in range(1, 1 + len(wl.extra["ratios"])):
+        if L > 1:
+            g.fill_ghost(L, 0.0)
+        g.regrid_auto(L, *bench.regrid_params(wl, L, float(g.descs(L)["dx"][0]), dx1, 0.02))
 dt = wl.dt0()
 t = 0.0
 for n in range(5):

@@ -9,7 +9,6 @@ the same operation order).  Runs continued after a regrid stay within the
 north_star bar (1e-12 relative)."""
 import numpy as np
 import pytest
-from scipy import ndimage
 
 import oracle
 from paper_1808_02638_b200 import binding, workloads as W
@@ -58,55 +57,10 @@ def sync(g, o, nlev):
 
 
 def cover_map(descs, nx, ny, dom=DOM):
-    m = np.zeros((ny, nx), np.uint8)
-    for e in descs:
-        i0 = int(round((e["xlower"] - dom[0]) / e["dx"]))
-        j0 = int(round((e["ylower"] - dom[2]) / e["dy"]))
-        m[j0:j0 + e["my"], i0:i0 + e["mx"]] = 1
-    return m
+    return oracle.cover_map(descs, dom, nx, ny)
 
 
-def nest_mask(on):
-    """Level cells whose in-domain neighbours within Chebyshev distance 2 are
-    all on the level (claw_flag clip 2), by brute force."""
-    ny, nx = on.shape
-    M = np.zeros_like(on)
-    for J in range(ny):
-        for I in range(nx):
-            blk = on[max(J - 2, 0):J + 3, max(I - 2, 0):I + 3]
-            M[J, I] = 1 if on[J, I] and blk.all() else 0
-    return M
-
-
-def split_boxes(boxes, M, f):
-    """claw_regrid_auto's nesting split: row runs of M inside each box, runs
-    identical in consecutive rows merged, pieces without flags dropped,
-    ordered by (y0, x0) within a box."""
-    out = []
-    for x0, y0, w, h in np.asarray(boxes).tolist():
-        x1, y1 = x0 + w, y0 + h
-        opened, done = {}, []
-        for J in range(y0, y1 + 1):
-            runs = []
-            if J < y1:
-                I = x0
-                while I < x1:
-                    if not M[J, I]:
-                        I += 1
-                        continue
-                    e = I
-                    while e < x1 and M[J, e]:
-                        e += 1
-                    runs.append((I, e))
-                    I = e
-            for key in sorted(opened):
-                if key not in runs:
-                    done.append((key[0], opened.pop(key), key[1], J))
-            for r in runs:
-                opened.setdefault(r, J)
-        done.sort(key=lambda r: (r[1], r[0]))
-        out += [(a, y, e - a, J - y) for a, y, e, J in done if f[y:J, a:e].any()]
-    return np.array(out, np.int32).reshape(-1, 4)
+nest_mask = oracle.nest_mask
 
 
 def same_level(g, o, level):
@@ -246,14 +200,7 @@ def test_regrid_auto_equals_oracle_composition_and_continues():
 
     def oracle_auto(level, R):
         o.fill_ghost(level, t)
-        nx, ny = o.level_shape(level)
-        on = cover_map(o.descs(level), nx, ny, W.DOMAIN)
-        M = nest_mask(on)
-        fb = oracle.buffer_flags(o.flag(level, cfg["tol"]), cfg["buffer"], M)
-        boxes = oracle.cluster(fb, cfg["cutoff"], cfg["max_dim"], cfg["min_dim"])
-        pieces = split_boxes(boxes, M, fb)
-        o.regrid(level, pieces, R)
-        return len(pieces)
+        return oracle.regrid_auto(o, level, R=R, **cfg)
 
     g.fill_ghost(1, t)
     nb = g.regrid_auto(1, R=4, **cfg)

@@ -216,3 +216,48 @@ def test_ring_regrid_covers_every_flag():
         j0 = int(round((e["ylower"] - wl.domain[2]) / e["dy"])) // 4
         cov[j0:j0 + e["my"] // 4, i0:i0 + e["mx"] // 4] = True
     assert cov[f == 1].all()
+
+
+def brute_nest_mask(on):
+    ny, nx = on.shape
+    M = np.zeros_like(on)
+    for J in range(ny):
+        for I in range(nx):
+            blk = on[max(J - 2, 0):J + 3, max(I - 2, 0):I + 3]
+            M[J, I] = 1 if on[J, I] and blk.all() else 0
+    return M
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_nest_mask_brute_force(seed):
+    rng = np.random.default_rng(40 + seed)
+    on = np.zeros((30, 37), np.uint8)
+    for _ in range(6):
+        a, b = rng.integers(0, 30), rng.integers(0, 25)
+        on[b:b + rng.integers(3, 15), a:a + rng.integers(3, 15)] = 1
+    assert np.array_equal(oracle.nest_mask(on), brute_nest_mask(on))
+    full = np.ones((9, 11), np.uint8)
+    assert oracle.nest_mask(full).all()                 # the domain edge never vetoes
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_split_boxes_postconditions(seed):
+    rng = np.random.default_rng(60 + seed)
+    on = np.zeros((50, 60), np.uint8)
+    for _ in range(5):
+        a, b = rng.integers(0, 50), rng.integers(0, 40)
+        on[b:b + rng.integers(5, 25), a:a + rng.integers(5, 25)] = 1
+    M = oracle.nest_mask(on)
+    f = ((rng.uniform(size=on.shape) > 0.8) & (M == 1)).astype(np.uint8)
+    f = oracle.buffer_flags(f, 1, M)
+    boxes = oracle.cluster(f, 0.6, 24, 3)
+    pieces = oracle.split_boxes(boxes, M, f)
+    cover = np.zeros(on.shape, np.int32)
+    for x0, y0, w, h in pieces:
+        blk = M[y0:y0 + h, x0:x0 + w]
+        assert blk.all()                                 # inside the nesting mask
+        assert f[y0:y0 + h, x0:x0 + w].any()             # holds a flag
+        assert any(bx <= x0 and x0 + w <= bx + bw and by <= y0 and y0 + h <= by + bh
+                   for bx, by, bw, bh in boxes)           # inside one cluster box
+        cover[y0:y0 + h, x0:x0 + w] += 1
+    assert cover.max() <= 1 and (cover[f == 1] == 1).all()
