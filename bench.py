@@ -37,6 +37,7 @@ sys.path.insert(0, ROOT)
 
 from paper_1808_02638_b200 import workloads as W  # noqa: E402
 
+LIMNAME = {0: "none", 1: "minmod", 2: "superbee", 3: "vanLeer", 4: "MC"}
 BYTES_PER_CELL = 48  # algorithmic: read q^n (3 x fp64) + write q^{n+1} (3 x fp64)
 
 
@@ -463,7 +464,8 @@ def main():
             traffic = None
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-            "kernel": ("step_grid_kernel<MC,2>" if g.level_mode(1) == "grid" else "step_kernel<MC,2,uniform>"),
+            "kernel": (f"step_grid_kernel<{LIMNAME[wl.limiter]},{wl.order_trans}>" if g.level_mode(1) == "grid" and nlev == 1
+                       else f"step_kernel<{LIMNAME[wl.limiter]},{wl.order_trans},uniform>"),
             "bytes_per_cell": BYTES_PER_CELL,
             "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,
             "kernel_share_of_step": (st["step_ms"] / ms) if ms > 0 else None,

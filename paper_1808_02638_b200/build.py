@@ -29,23 +29,27 @@ def stale() -> bool:
     return any(os.path.getmtime(s) > t for s in SOURCES + HEADERS + [__file__])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile every source to an object in parallel (nvcc -c), then link."""
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, defs=(), out: str | None = None) -> str:
+    """Compile every source to an object in parallel (nvcc -c), then link.
+    defs / out: tuning variants (-D knobs) linked to another path."""
+    lib = out or LIB
+    if not force and out is None and not defs and not stale():
         return LIB
     from concurrent.futures import ThreadPoolExecutor
 
-    odir = os.path.join(PKG, "build")
+    odir = os.path.join(PKG, "build", "v_" + "_".join(d.lstrip("-D") for d in defs)) if defs else \
+        os.path.join(PKG, "build")
     os.makedirs(odir, exist_ok=True)
     cflags = [f for f in NVCC_FLAGS if f != "-shared"]
     jobs = []
     # the kernels file is compiled once per wave limiter (-DCLAW_LIM=k: the
     # step / reflux template instances of that limiter) plus once for the rest
     units = [(src, []) for src in SOURCES] + [(SOURCES[0], [f"-DCLAW_LIM={k}"]) for k in range(5)]
-    for src, defs in units:
-        tag = defs[0].split("=")[1] if defs else ""
+    for src, dfs in units:
+        tag = dfs[0].split("=")[1] if dfs else ""
         obj = os.path.join(odir, os.path.basename(src) + (f".lim{tag}" if tag else "") + ".o")
-        jobs.append((obj, [nvcc(), *cflags, *defs, "-I", os.path.join(ROOT, "include"), "-c", "-o", obj, src]))
+        jobs.append((obj, [nvcc(), *cflags, *dfs, *defs, "-I", os.path.join(ROOT, "include"), "-c", "-o", obj,
+                           src]))
     if verbose:
         for _, cmd in jobs:
             print(" ".join(cmd), file=sys.stderr)
@@ -53,12 +57,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for r in ex.map(lambda j: subprocess.run(j[1]), jobs):
             if r.returncode:
                 raise subprocess.CalledProcessError(r.returncode, r.args)
-    link = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB,
+    link = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", lib,
             *[o for o, _ in jobs], "-ldl"]
     if verbose:
         print(" ".join(link), file=sys.stderr)
     subprocess.run(link, check=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
