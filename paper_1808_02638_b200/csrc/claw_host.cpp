@@ -316,6 +316,17 @@ struct Level {
   }
 };
 
+// One captured coarse step of claw_advance_hierarchy (the
+// per-step launch sequence replayed as a CUDA graph).  Valid for the key it
+// was captured under: context epoch, dt, flags, profiling, and every level's
+// ping-pong buffer / CFL-slot parity.
+struct HierGraph {
+  std::vector<uint64_t> key;
+  cudaGraphExec_t exec = nullptr;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_step, ev_ghost;  // timing nodes (profiling)
+};
+constexpr int kMaxAlpha = 4096;  // interpolation launches per coarse step
+
 }  // namespace
 
 struct claw_ctx {
@@ -339,6 +350,16 @@ struct claw_ctx {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_free;  // event pool
   uint8_t* h_stage = nullptr;  // pinned staging for flag maps (regrid)
   size_t h_stage_bytes = 0;
+  // CUDA graphs of the hierarchy's coarse step
+  std::vector<HierGraph> graphs;
+  uint64_t epoch = 0;          // bumped whenever levels are (re)defined
+  bool graphs_on = false;      // CLAW_GRAPH=1 enables
+  bool in_hier = false;        // inside claw_advance_hierarchy (alpha through d_alpha)
+  bool dry = false;            // host bookkeeping only: the graph launches the work
+  bool capturing = false;
+  int alpha_n = 0;
+  double* h_alpha = nullptr;   // pinned [kMaxAlpha], copied to d_alpha by the graph
+  DevBuf<double> d_alpha;
 };
 
 namespace {
@@ -1347,7 +1368,8 @@ int check_level(claw_ctx* c, int level) {
 }
 
 void record(claw_ctx* c, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v, bool start) {
-  if (!c->profiling) return;
+  if (!c->profiling || c->dry) return;
+  const unsigned fl = c->capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
   if (start) {
     std::pair<cudaEvent_t, cudaEvent_t> e;
     if (!c->ev_free.empty()) {
@@ -1358,10 +1380,20 @@ void record(claw_ctx* c, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v, bo
       cudaEventCreate(&e.second);
     }
     v.push_back(e);
-    cudaEventRecord(e.first, c->stream);
+    cudaEventRecordWithFlags(e.first, c->stream, fl);
   } else {
-    cudaEventRecord(v.back().second, c->stream);
+    cudaEventRecordWithFlags(v.back().second, c->stream, fl);
   }
+}
+
+void drop_graphs(claw_ctx* c) {
+  for (HierGraph& g : c->graphs) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    for (auto& e : g.ev_step) c->ev_free.push_back(e);
+    for (auto& e : g.ev_ghost) c->ev_free.push_back(e);
+  }
+  c->graphs.clear();
+  c->epoch++;
 }
 
 double drain(claw_ctx* c, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
@@ -1418,6 +1450,12 @@ int claw_create(const claw_config* cfg, claw_ctx** out) {
   }
   ctx->tile_rows = cfg->tile_rows > 0 ? cfg->tile_rows : claw::max_tile_rows();
   ctx->host_only = cfg->device < 0;
+  {
+    // opt-in (CLAW_GRAPH=1): measured slower than the asynchronous launch
+    // sequence, which never starves the GPU inside a coarse step
+    const char* gv = std::getenv("CLAW_GRAPH");
+    ctx->graphs_on = gv && gv[0] == '1';
+  }
   *out = ctx;
   if (ctx->host_only) return CLAW_OK;
   CUDA_TRY(cudaSetDevice(cfg->device));
@@ -1460,6 +1498,9 @@ int claw_destroy(claw_ctx* ctx) {
   if (!ctx->host_only && !ctx->dead) cudaStreamSynchronize(ctx->stream);
   drain(ctx, ctx->ev_step);
   drain(ctx, ctx->ev_ghost);
+  drop_graphs(ctx);
+  if (ctx->h_alpha) cudaFreeHost(ctx->h_alpha);
+  ctx->d_alpha.reset();
   for (auto& L : ctx->lev) L = Level();
   for (auto& e : ctx->ev_free) {
     cudaEventDestroy(e.first);
@@ -1488,6 +1529,7 @@ int claw_set_level(claw_ctx* ctx, int32_t level, int32_t npatch, const claw_patc
   if (level > 1 && ctx->cfg.world > 1)
     return fail(ctx, CLAW_EINVAL, "multi-level hierarchies are single-rank in this version (world=%d)", ctx->cfg.world);
   if (!ctx->host_only) CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  drop_graphs(ctx);
   for (int l = level; l <= kMaxLevel; ++l) ctx->lev[l] = Level();
   Level& L = ctx->lev[level];
   int rc = build_geometry(ctx, level, npatch, descs, L);
@@ -1540,10 +1582,21 @@ int claw_fill_ghost(claw_ctx* ctx, int32_t level, double t) {
       return fail(ctx, CLAW_ESTATE, "fill_ghost(level %d, t=%.17g): outside level %d's [%.17g, %.17g]", level, t,
                   level - 1, C.t_old, C.t_new);
     const double alpha = (span > 0) ? (t - C.t_old) / span : 0.0;
+    // inside claw_advance_hierarchy alpha goes through device memory, so a
+    // replayed graph interpolates at this step's time
+    const double* adev = nullptr;
+    if (ctx->in_hier) {
+      if (ctx->alpha_n >= kMaxAlpha) return fail(ctx, CLAW_EINVAL, "more than %d interpolations per coarse step", kMaxAlpha);
+      ctx->h_alpha[ctx->alpha_n] = alpha;
+      adev = ctx->d_alpha.p + ctx->alpha_n;
+      ctx->alpha_n++;
+    }
     // C.q[C.cur] holds t_new, the other buffer t_old
     // DevInterp.dst is an absolute frame offset; components are ncoarse apart
-    CUDA_TRY(static_cast<cudaError_t>(claw::launch_interp(C.q[1 - C.cur].p, C.q[C.cur].p, alpha, L.dinterp.p,
-                                                          L.ncoarse, L.frame.p, L.ncoarse, ctx->stream)));
+    if (!ctx->dry)
+      CUDA_TRY(static_cast<cudaError_t>(claw::launch_interp(C.q[1 - C.cur].p, C.q[C.cur].p, alpha, adev,
+                                                            L.dinterp.p, L.ncoarse, L.frame.p, L.ncoarse,
+                                                            ctx->stream)));
     ctx->stats.ghost_launches++;
   }
   if (ctx->cfg.world > 1 && ctx->cfg.exchange == 0) {
@@ -1660,7 +1713,7 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
     }
     if (n_int > 0 && Pi.ntiles > 0) {
       Pe.level_cfl_reset = nullptr;  // reset once (by the interior launch)
-      CUDA_TRY(static_cast<cudaError_t>(claw::launch_step(Pi, ctx->stream)));
+      if (!ctx->dry) CUDA_TRY(static_cast<cudaError_t>(claw::launch_step(Pi, ctx->stream)));
       ctx->stats.step_launches++;
     } else {
       Pe = P;                        // no split: one launch after the halo
@@ -1670,11 +1723,11 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
       L.halo_pending = false;
     }
     if (n_all && Pe.ntiles > 0) {
-      CUDA_TRY(static_cast<cudaError_t>(claw::launch_step(Pe, ctx->stream)));
+      if (!ctx->dry) CUDA_TRY(static_cast<cudaError_t>(claw::launch_step(Pe, ctx->stream)));
       ctx->stats.step_launches++;
     }
   } else {
-    CUDA_TRY(static_cast<cudaError_t>(claw::launch_step(P, ctx->stream)));
+    if (!ctx->dry) CUDA_TRY(static_cast<cudaError_t>(claw::launch_step(P, ctx->stream)));
     ctx->stats.step_launches++;
   }
   record(ctx, ctx->ev_step, false);
@@ -1684,14 +1737,14 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
     // and of level-1, which advanced first), coarse part of level+1's
     if (level > 1 && !L.hreg.empty()) {
       const Level& C = ctx->lev[level - 1];
-      CUDA_TRY(static_cast<cudaError_t>(claw::launch_reflux(1, P, C.q[1 - C.cur].p, C.dpatch.p, L.dreg.p,
+      if (!ctx->dry) CUDA_TRY(static_cast<cudaError_t>(claw::launch_reflux(1, P, C.q[1 - C.cur].p, C.dpatch.p, L.dreg.p,
                                                             static_cast<int64_t>(L.hreg.size()), L.ratio, L.racc.p,
                                                             ctx->stream)));
       ctx->stats.ghost_launches++;
     }
     if (level < kMaxLevel && ctx->lev[level + 1].set && !ctx->lev[level + 1].hreg.empty()) {
       Level& F = ctx->lev[level + 1];
-      CUDA_TRY(static_cast<cudaError_t>(claw::launch_reflux(0, P, nullptr, nullptr, F.dreg.p,
+      if (!ctx->dry) CUDA_TRY(static_cast<cudaError_t>(claw::launch_reflux(0, P, nullptr, nullptr, F.dreg.p,
                                                             static_cast<int64_t>(F.hreg.size()), F.ratio, F.racc.p,
                                                             ctx->stream)));
       ctx->stats.ghost_launches++;
@@ -1862,14 +1915,14 @@ int claw_update_level(claw_ctx* ctx, int32_t level) {
     return fail(ctx, CLAW_ESTATE, "update: level %d (t=%.17g) has not caught up with level %d (t=%.17g)", level,
                 F.t_new, level - 1, C.t_new);
   const int64_t n = static_cast<int64_t>(F.hu.size());
-  CUDA_TRY(static_cast<cudaError_t>(claw::launch_update_rects(C.q[C.cur].p, F.q[F.cur].p, F.dur.p,
+  if (!ctx->dry) CUDA_TRY(static_cast<cudaError_t>(claw::launch_update_rects(C.q[C.cur].p, F.q[F.cur].p, F.dur.p,
                                                               static_cast<int32_t>(F.hur.size()), F.ratio,
                                                               F.hur_max, ctx->stream)));
-  CUDA_TRY(static_cast<cudaError_t>(claw::launch_update(C.q[C.cur].p, F.q[F.cur].p, F.du.p, n, F.ratio,
+  if (!ctx->dry) CUDA_TRY(static_cast<cudaError_t>(claw::launch_update(C.q[C.cur].p, F.q[F.cur].p, F.du.p, n, F.ratio,
                                                         F.du_src.p, F.du_scs.p, ctx->stream)));
   ctx->stats.ghost_launches += (F.hur.empty() ? 0 : 1) + (n > 0 ? 1 : 0);
   if (ctx->cfg.reflux && !F.hreg.empty()) {
-    CUDA_TRY(static_cast<cudaError_t>(claw::launch_reflux_apply(C.q[C.cur].p, C.dpatch.p, F.dreg.p, F.dheads.p,
+    if (!ctx->dry) CUDA_TRY(static_cast<cudaError_t>(claw::launch_reflux_apply(C.q[C.cur].p, C.dpatch.p, F.dreg.p, F.dheads.p,
                                                                 static_cast<int64_t>(F.hheads.size()) - 1, F.racc.p,
                                                                 ctx->stream)));
     ctx->stats.ghost_launches++;
@@ -1929,19 +1982,100 @@ int claw_advance_hierarchy(claw_ctx* ctx, double t, double dt, int32_t flags, do
   while (nlev < kMaxLevel && ctx->lev[nlev + 1].set) ++nlev;
   if (nlev == 0) return fail(ctx, CLAW_ESTATE, "no level set");
   if (!ctx->hier_buf.p) CUDA_TRY(ctx->hier_buf.alloc(1));
-  CUDA_TRY(cudaMemsetAsync(ctx->hier_buf.p, 0, 8, ctx->stream));
+  const bool graph = ctx->graphs_on && ctx->cfg.world == 1;
+  if (!graph) {
+    CUDA_TRY(cudaMemsetAsync(ctx->hier_buf.p, 0, 8, ctx->stream));
+    ctx->hier_slot = ctx->hier_buf.p;
+    const int rc = advance_rec(ctx, 1, t, dt, nlev, flags);
+    ctx->hier_slot = nullptr;
+    if (rc) return rc;
+    if (ctx->cfg.world > 1 && ctx->cfg.exchange == 0) {
+      ncclResult_t nr = g_nccl.AllReduce(ctx->hier_buf.p, ctx->hier_buf.p, 1, ncclFloat64, ncclMax, ctx->comm,
+                                         ctx->stream);
+      if (nr != ncclSuccess) return nccl_fail(ctx, nr, "ncclAllReduce(cfl, max)");
+    }
+    CUDA_TRY(cudaMemcpyAsync(ctx->h_cfl, ctx->hier_buf.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    *cfl_max = *ctx->h_cfl;
+    return CLAW_OK;
+  }
+  // CUDA-graph path: the whole coarse step -- every fill,
+  // step, reflux and update launch -- is captured once per key and replayed;
+  // the host only redoes its bookkeeping (times, buffer parity) and the
+  // interpolation weights, which reach the graph through pinned memory.
+  if (!ctx->h_alpha) {
+    CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_alpha), kMaxAlpha * sizeof(double)));
+    CUDA_TRY(ctx->d_alpha.alloc(kMaxAlpha));
+  }
+  std::vector<uint64_t> key = {ctx->epoch, 0, static_cast<uint64_t>(flags), ctx->profiling ? 1u : 0u,
+                               static_cast<uint64_t>(nlev)};
+  std::memcpy(&key[1], &dt, 8);
+  for (int l = 1; l <= nlev; ++l) key.push_back(static_cast<uint64_t>(ctx->lev[l].cur | (ctx->lev[l].gen << 1)));
+  HierGraph* hg = nullptr;
+  for (HierGraph& g : ctx->graphs)
+    if (g.key == key) hg = &g;
+  ctx->in_hier = true;
+  ctx->alpha_n = 0;
   ctx->hier_slot = ctx->hier_buf.p;
-  const int rc = advance_rec(ctx, 1, t, dt, nlev, flags);
+  int rc = CLAW_OK;
+  if (hg) {
+    ctx->dry = true;
+    rc = advance_rec(ctx, 1, t, dt, nlev, flags);
+    ctx->dry = false;
+    if (!rc) {
+      cudaError_t e = cudaGraphLaunch(hg->exec, ctx->stream);
+      if (e != cudaSuccess) rc = cuda_fail(ctx, e, "cudaGraphLaunch");
+    }
+  } else {
+    const size_t s0 = ctx->ev_step.size(), g0 = ctx->ev_ghost.size();
+    cudaError_t e = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) rc = cuda_fail(ctx, e, "cudaStreamBeginCapture");
+    if (!rc) {
+      ctx->capturing = true;
+      cudaMemcpyAsync(ctx->d_alpha.p, ctx->h_alpha, kMaxAlpha * sizeof(double), cudaMemcpyHostToDevice, ctx->stream);
+      cudaMemsetAsync(ctx->hier_buf.p, 0, 8, ctx->stream);
+      rc = advance_rec(ctx, 1, t, dt, nlev, flags);
+      cudaMemcpyAsync(ctx->h_cfl, ctx->hier_buf.p, 8, cudaMemcpyDeviceToHost, ctx->stream);
+      ctx->capturing = false;
+      cudaGraph_t gr = nullptr;
+      e = cudaStreamEndCapture(ctx->stream, &gr);
+      if (!rc && e != cudaSuccess) rc = cuda_fail(ctx, e, "cudaStreamEndCapture");
+      if (!rc) {
+        HierGraph ng;
+        ng.key = key;
+        e = cudaGraphInstantiate(&ng.exec, gr, 0);
+        if (e != cudaSuccess) rc = cuda_fail(ctx, e, "cudaGraphInstantiate");
+        ng.ev_step.assign(ctx->ev_step.begin() + s0, ctx->ev_step.end());
+        ng.ev_ghost.assign(ctx->ev_ghost.begin() + g0, ctx->ev_ghost.end());
+        ctx->ev_step.resize(s0);
+        ctx->ev_ghost.resize(g0);
+        if (!rc) {
+          ctx->graphs.push_back(std::move(ng));
+          hg = &ctx->graphs.back();
+          e = cudaGraphLaunch(hg->exec, ctx->stream);
+          if (e != cudaSuccess) rc = cuda_fail(ctx, e, "cudaGraphLaunch");
+        }
+      }
+      if (gr) cudaGraphDestroy(gr);
+    }
+  }
+  ctx->in_hier = false;
   ctx->hier_slot = nullptr;
   if (rc) return rc;
-  if (ctx->cfg.world > 1 && ctx->cfg.exchange == 0) {
-    ncclResult_t nr = g_nccl.AllReduce(ctx->hier_buf.p, ctx->hier_buf.p, 1, ncclFloat64, ncclMax, ctx->comm,
-                                       ctx->stream);
-    if (nr != ncclSuccess) return nccl_fail(ctx, nr, "ncclAllReduce(cfl, max)");
-  }
-  CUDA_TRY(cudaMemcpyAsync(ctx->h_cfl, ctx->hier_buf.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   *cfl_max = *ctx->h_cfl;
+  if (ctx->profiling) {  // this replay's timing nodes
+    for (auto& p : hg->ev_step) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, p.first, p.second);
+      ctx->stats.step_ms += ms;
+    }
+    for (auto& p : hg->ev_ghost) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, p.first, p.second);
+      ctx->stats.ghost_ms += ms;
+    }
+  }
   return CLAW_OK;
 }
 
@@ -2312,6 +2446,7 @@ int claw_regrid(claw_ctx* ctx, int32_t level, int32_t nbox, const int32_t* boxes
                 ctx->lev[level + 1].ratio);
   PhaseTrace lap("regrid", level);
   if (!ctx->host_only) CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  drop_graphs(ctx);
   Level old = std::move(ctx->lev[level + 1]);
   for (int l = level + 1; l <= kMaxLevel; ++l) ctx->lev[l] = Level();
   if (nbox == 0) return CLAW_OK;
