@@ -302,6 +302,7 @@ struct Level {
   int npx = 0;
   int64_t ngrid_tiles = 0;
   int64_t ngrid_blocks = 0;   // row blocks of the band (grid mode)
+  int grid_th = 0;            // rows per grid tile (> my: tiles span patch rows)
   int64_t ntile_interior = 0; // generic tiles [0, n) read no remote ghost cell
   bool halo_pending = false;  // NCCL halo in flight on the comm stream
 
@@ -1084,9 +1085,30 @@ int plan_level(claw_ctx* c, int level, Level& L) {
         L.Y0 = 0;
         L.Y1 = L.ny;
       }
-      const int th = std::min(L.th, my);
+      // rows per grid tile: within one patch row (th <= my), or spanning
+      // several whole patch rows (the kernel steps its row pointers across
+      // patch-row boundaries), which halves the per-tile prologue on 32-row
+      // patches; CLAW_GRID_TH overrides (tuning)
+      int th = std::min(L.th, my);
+      const int64_t nstrip0 = (L.nx + claw::grid_strip() - 1) / claw::grid_strip();
+      auto span_ok = [&](int w) { return w > my && w % my == 0 && my % 4 == 0 && my >= 8 && w <= 512; };
+      if (const char* e = std::getenv("CLAW_GRID_TH")) {
+        if (span_ok(std::atoi(e))) th = std::atoi(e);
+      } else if (c->cfg.tile_rows > 0) {
+        if (span_ok(c->cfg.tile_rows)) th = c->cfg.tile_rows;
+      } else if (L.th == 64) {
+        // large level: the tallest tile (<= 256 rows) that still gives two
+        // waves of warps (148 SMs x 16 resident warps x 2); measured C5 +3.6%,
+        // C4 +7% over one-patch-row tiles (profiles/r01_grid_tile_rows.txt)
+        for (int w = 256; w > my; w /= 2)
+          if (span_ok(w) && nstrip0 * ((L.Y1 - L.Y0 + w - 1) / w) >= 148 * 16 * 2) {
+            th = w;
+            break;
+          }
+      }
+      L.grid_th = th;
       const int64_t nstrip = (L.nx + claw::grid_strip() - 1) / claw::grid_strip();
-      L.ngrid_blocks = ((L.Y1 - L.Y0) / my) * ((my + th - 1) / th);
+      L.ngrid_blocks = th > my ? ((L.Y1 - L.Y0) + th - 1) / th : ((L.Y1 - L.Y0) / my) * ((my + th - 1) / th);
       L.ngrid_tiles = nstrip * L.ngrid_blocks;
     }
   }
@@ -1673,7 +1695,7 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
     P.mx = L.desc[0].mx;
     P.my = L.desc[0].my;
     P.npx = L.npx;
-    P.th = std::min(L.th, P.my);
+    P.th = L.grid_th;
     P.per_x = ctx->cfg.bc[0] == CLAW_BC_PERIODIC;
     P.per_y = ctx->cfg.bc[2] == CLAW_BC_PERIODIC;
     P.ntiles = static_cast<int32_t>(L.ngrid_tiles);

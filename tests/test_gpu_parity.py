@@ -430,3 +430,27 @@ def test_update_level_unaligned_fine_patches_bitwise():
     out = g.read_level(1)
     assert np.array_equal(out, o.read_level(1))
     assert not np.array_equal(out, qc)
+
+
+@pytest.mark.parametrize("npx,npy,mx,my,th,bc", [
+    (8, 8, 32, 32, 64, W.EXTRAP), (6, 5, 16, 16, 48, W.PERIODIC), (4, 7, 24, 8, 32, (2, 2, 1, 1)),
+    (3, 3, 32, 32, 96, W.EXTRAP)])
+def test_grid_tiles_spanning_patch_rows(npx, npy, mx, my, th, bc, monkeypatch):
+    """Grid tiles of th > my rows (several patch rows; the kernel steps its row
+    pointers across patch-row boundaries, ragged last tile): bitwise equal to
+    the generic kernel."""
+    d = W.uniform_level(npx, npy, mx, my)
+    q0 = W.random_ic(d, 7 * mx + th)
+    dt = 0.9 * 2 / max(npx * mx, npy * my)
+    res = []
+    for path in (0, 1):
+        monkeypatch.setenv("CLAW_GRID_TH", str(th))
+        g = binding.Claw(W.DOMAIN, bc, 4, 2, device=0, path=path)
+        g.set_level(1, d, q0)
+        assert g.level_mode(1) == ("grid" if path == 0 else "generic")
+        for n in range(5):
+            g.fill_ghost(1, n * dt)
+            c = g.advance_level(1, dt)
+        res.append((g.read_level(1), c))
+        g.close()
+    assert np.array_equal(res[0][0], res[1][0]) and res[0][1] == res[1][1]
