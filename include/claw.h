@@ -245,7 +245,10 @@ int claw_cluster(const uint8_t* flags, int64_t nx, int64_t ny, double cutoff, in
  * (P:110-111).  A new fine cell takes the value of the old level+1 cell at
  * the same place if there is one, else the R10 coarse interpolation
  * from `level` at its current time (the ghost-fill formula with alpha = 1).
- * Levels finer than level+1 are discarded; nbox = 0 just removes them.  The
+ * Levels finer than level+1 are discarded -- but kept as the copy sources of
+ * the regrid that re-creates them next, until any level advances, so a regrid
+ * of levels 1, 2, ... in turn keeps every level's old data (R18);
+ * nbox = 0 just removes them.  The
  * new level's time is level's t_new.  EINVAL: box outside the index space or
  * overlapping another; ENEST: a cell to interpolate has no coarse donor, or a
  * ghost cell of the new level none.  Device memory comes from the library's

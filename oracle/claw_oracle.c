@@ -77,6 +77,8 @@ struct oracle_ctx {
   oracle_config cfg;
   int reflux;             /* conservation fix on (oracle_set_reflux) */
   olevel lev[MAXLEVEL + 1];
+  olevel stash[MAXLEVEL + 1]; /* levels discarded by a regrid: copy sources for
+                                 the regrid that re-creates them (R18) */
   char err[512];
 };
 
@@ -437,7 +439,10 @@ int oracle_create(const oracle_config* cfg, oracle_ctx** out) {
 
 int oracle_destroy(oracle_ctx* c) {
   if (!c) return -1;
-  for (int l = 0; l <= MAXLEVEL; ++l) free_level(&c->lev[l]);
+  for (int l = 0; l <= MAXLEVEL; ++l) {
+    free_level(&c->lev[l]);
+    free_level(&c->stash[l]);
+  }
   free(c);
   return 0;
 }
@@ -531,8 +536,16 @@ static int build_registers(oracle_ctx* c, int level) {
   return 0;
 }
 
+static int set_level_impl(oracle_ctx* c, int level, int npatch, const oracle_patch_desc* descs,
+                          const double* q0, int keep_stash);
+
 int oracle_set_level(oracle_ctx* c, int level, int npatch,
                      const oracle_patch_desc* descs, const double* q0) {
+  return set_level_impl(c, level, npatch, descs, q0, 0);
+}
+
+static int set_level_impl(oracle_ctx* c, int level, int npatch, const oracle_patch_desc* descs,
+                          const double* q0, int keep_stash) {
   if (!c || level < 1 || level > MAXLEVEL || npatch < 1 || !descs)
     return fail(c, -1, "bad arguments");
   if (level > 1 && c->lev[level - 1].npatch == 0)
@@ -625,6 +638,8 @@ int oracle_set_level(oracle_ctx* c, int level, int npatch,
   }
   L->t_old = L->t_new = (level > 1) ? c->lev[level - 1].t_old : 0.0;
   for (int l = level + 1; l <= MAXLEVEL; ++l) free_level(&c->lev[l]);
+  if (!keep_stash)
+    for (int l = level; l <= MAXLEVEL; ++l) free_level(&c->stash[l]);
   if (level > 1 && c->reflux) return build_registers(c, level);
   return 0;
 }
@@ -793,6 +808,7 @@ static void reflux_fine_part(oracle_ctx* c, int level, double dt, double** const
 int oracle_advance_level(oracle_ctx* c, int level, double dt, double* cfl_max) {
   if (!c || level < 1 || level > MAXLEVEL || c->lev[level].npatch == 0)
     return fail(c, -2, "level not set");
+  for (int l = 1; l <= MAXLEVEL; ++l) free_level(&c->stash[l]);  /* stale once time moves */
   olevel* L = &c->lev[level];
   const int fine_part = c->reflux && level > 1 && L->nreg > 0;
   const int coarse_part = c->reflux && level < MAXLEVEL && c->lev[level + 1].nreg > 0;
@@ -1129,9 +1145,29 @@ int oracle_regrid(oracle_ctx* c, int level, int nbox, const int32_t* boxes, int 
   if (!c || level < 1 || level >= MAXLEVEL || c->lev[level].npatch == 0 || nbox < 0 || R < 1)
     return fail(c, -1, "bad regrid arguments");
   olevel* C = &c->lev[level];
-  olevel old = c->lev[level + 1];            /* take ownership of the old fine level */
-  memset(&c->lev[level + 1], 0, sizeof(olevel));
-  for (int l = level + 2; l <= MAXLEVEL; ++l) free_level(&c->lev[l]);
+  /* the old fine level: the current level+1, else the one a regrid of a
+   * coarser level discarded just before (R18: a regrid of levels 1, 2, ...
+   * in turn copies every level's old data) */
+  olevel old;
+  if (c->lev[level + 1].npatch) {
+    old = c->lev[level + 1];
+    memset(&c->lev[level + 1], 0, sizeof(olevel));
+    free_level(&c->stash[level + 1]);
+  } else {
+    old = c->stash[level + 1];
+    memset(&c->stash[level + 1], 0, sizeof(olevel));
+  }
+  if (old.npatch && nbox > 0 && (int)(C->dx / old.dx + 0.5) != R) {
+    free_level(&old);
+    return fail(c, -1, "regrid: R differs from the old fine level's ratio");
+  }
+  for (int l = level + 2; l <= MAXLEVEL; ++l) { /* discarded levels become copy sources */
+    if (c->lev[l].npatch) {
+      free_level(&c->stash[l]);
+      c->stash[l] = c->lev[l];
+      memset(&c->lev[l], 0, sizeof(olevel));
+    }
+  }
   int rc = 0;
   if (nbox > 0) {
     const double dxf = C->dx / R, dyf = C->dy / R;
@@ -1188,7 +1224,7 @@ int oracle_regrid(oracle_ctx* c, int level, int nbox, const int32_t* boxes, int 
         }
       off += 3 * (int64_t)d[b].mx * d[b].my;
     }
-    if (!rc) rc = oracle_set_level(c, level + 1, nbox, d, q0);
+    if (!rc) rc = set_level_impl(c, level + 1, nbox, d, q0, 1);
     free(q0);
     free(d);
   }

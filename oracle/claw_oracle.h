@@ -134,7 +134,10 @@ int oracle_step_patch(int mx, int my, const double* qpad, double dx, double dy,
  *   exactly once; -3 if more than cap boxes (nbox still set).
  * oracle_regrid: replace level+1 by the boxes refined by R; data copied from
  *   the old level+1 where it overlaps, else interpolated from `level` (R10
- *   at alpha = 1); finer levels are discarded; -6 if a box is not on `level`. */
+ *   at alpha = 1); finer levels are discarded but kept as the copy sources of
+ *   the regrid that re-creates them next (until any level advances), so a
+ *   regrid of levels 1, 2, ... in turn keeps every level's old data; -6 if a
+ *   box is not on `level`. */
 int oracle_flag(oracle_ctx* ctx, int level, double tol, uint8_t* flags);
 void oracle_buffer_flags(const uint8_t* in, int64_t nx, int64_t ny, int b, const uint8_t* mask,
                          uint8_t* out);

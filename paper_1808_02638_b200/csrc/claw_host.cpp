@@ -338,6 +338,9 @@ struct claw_ctx {
   bool own_stream = false;
   ncclComm_t comm = nullptr;
   Level lev[kMaxLevel + 1];
+  Level stash[kMaxLevel + 1];  // levels discarded by a regrid: copy sources for the
+                               // regrid that re-creates them (R18), until time moves
+  bool stashed = false;
   double* h_cfl = nullptr;  // pinned 8 bytes
   std::string err;
   bool profiling = false;
@@ -1524,6 +1527,7 @@ int claw_destroy(claw_ctx* ctx) {
   if (ctx->h_alpha) cudaFreeHost(ctx->h_alpha);
   ctx->d_alpha.reset();
   for (auto& L : ctx->lev) L = Level();
+  for (auto& L : ctx->stash) L = Level();
   for (auto& e : ctx->ev_free) {
     cudaEventDestroy(e.first);
     cudaEventDestroy(e.second);
@@ -1552,7 +1556,10 @@ int claw_set_level(claw_ctx* ctx, int32_t level, int32_t npatch, const claw_patc
     return fail(ctx, CLAW_EINVAL, "multi-level hierarchies are single-rank in this version (world=%d)", ctx->cfg.world);
   if (!ctx->host_only) CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   drop_graphs(ctx);
-  for (int l = level; l <= kMaxLevel; ++l) ctx->lev[l] = Level();
+  for (int l = level; l <= kMaxLevel; ++l) {
+    ctx->lev[l] = Level();
+    ctx->stash[l] = Level();
+  }
   Level& L = ctx->lev[level];
   int rc = build_geometry(ctx, level, npatch, descs, L);
   if (!rc) rc = plan_level(ctx, level, L);
@@ -1664,6 +1671,10 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
   if (int rc = check_level(ctx, level)) return rc;
   if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
   if (!(dt >= 0) || !std::isfinite(dt)) return fail(ctx, CLAW_EINVAL, "dt=%g: must be finite and >= 0", dt);
+  if (ctx->stashed) {  // discarded levels are stale once time moves (no kernel reads them)
+    for (auto& X : ctx->stash) X = Level();
+    ctx->stashed = false;
+  }
   Level& L = ctx->lev[level];
   // CFL slots: this step accumulates into lcfl[g] (zeroed by the previous
   // step's kernel, or at set_level) and zeroes lcfl[1-g] for the next step
@@ -2463,14 +2474,23 @@ int claw_regrid(claw_ctx* ctx, int32_t level, int32_t nbox, const int32_t* boxes
       return fail(ctx, CLAW_EINVAL, "regrid: box %d (%d,%d,%d,%d) outside level %d's index space", b, x[0], x[1],
                   x[2], x[3], level);
   }
-  if (ctx->lev[level + 1].set && nbox > 0 && ctx->lev[level + 1].ratio != R)
-    return fail(ctx, CLAW_EINVAL, "regrid: R=%d differs from the existing level %d's ratio %d", R, level + 1,
-                ctx->lev[level + 1].ratio);
+  // the old fine level: the current level+1, else the one a regrid of a
+  // coarser level discarded just before (R18)
+  Level& src = ctx->lev[level + 1].set ? ctx->lev[level + 1] : ctx->stash[level + 1];
+  if (src.set && nbox > 0 && src.ratio != R)
+    return fail(ctx, CLAW_EINVAL, "regrid: R=%d differs from the old level %d's ratio %d", R, level + 1, src.ratio);
   PhaseTrace lap("regrid", level);
   if (!ctx->host_only) CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   drop_graphs(ctx);
-  Level old = std::move(ctx->lev[level + 1]);
-  for (int l = level + 1; l <= kMaxLevel; ++l) ctx->lev[l] = Level();
+  Level old = std::move(src);
+  ctx->lev[level + 1] = Level();
+  ctx->stash[level + 1] = Level();
+  for (int l = level + 2; l <= kMaxLevel; ++l)  // discarded levels become copy sources
+    if (ctx->lev[l].set) {
+      ctx->stash[l] = std::move(ctx->lev[l]);
+      ctx->lev[l] = Level();
+      ctx->stashed = true;
+    }
   if (nbox == 0) return CLAW_OK;
   // descriptors of the new level: boxes refined by R
   const double dxf = C.dx / R, dyf = C.dy / R;

@@ -241,3 +241,24 @@ def test_regrid_reuses_pool_blocks():
     s1 = binding.pool_stats()
     assert s1["misses"] == s0["misses"] and s1["hits"] > s0["hits"]
     g.close()
+
+
+def test_regrid_in_turn_keeps_every_levels_data():
+    """R18: regrid(1) then regrid(2) copy both finer levels' old data (the
+    level 3 discarded by the first regrid is the second one's copy source),
+    as the oracle does; new boxes mix copied and interpolated cells."""
+    rng = np.random.default_rng(21)
+    n1 = 16
+    g, o = pair(n1, 2, rng.uniform(-1, 1, (3, n1, n1)).ravel(),
+                fine=[([(3, 3, 10, 9)], 2, None), ([(8, 8, 10, 8)], 2, None)])
+    q3 = g.read(3, 0)
+    for h in (g, o):
+        h.regrid(1, [(3, 3, 10, 9)], 2)
+        h.regrid(2, [(8, 8, 10, 8)], 2)
+    assert np.array_equal(g.read(3, 0), q3)
+    for h in (g, o):
+        h.regrid(1, [(2, 3, 11, 10)], 2)
+        h.regrid(2, [(7, 9, 12, 6), (9, 16, 5, 3)], 2)
+    same_level(g, o, 2)
+    same_level(g, o, 3)
+    g.close()

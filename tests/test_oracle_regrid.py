@@ -261,3 +261,31 @@ def test_split_boxes_postconditions(seed):
                    for bx, by, bw, bh in boxes)           # inside one cluster box
         cover[y0:y0 + h, x0:x0 + w] += 1
     assert cover.max() <= 1 and (cover[f == 1] == 1).all()
+
+
+def test_regrid_in_turn_keeps_every_levels_data():
+    """R18: regridding level 1, then level 2, onto the same boxes keeps levels
+    2 and 3 bitwise (the level-3 data discarded by the first regrid is the copy
+    source of the second); once a level advances, the discarded data is gone
+    and level 3 is interpolated from level 2."""
+    n, R = 16, 2
+    rng = np.random.default_rng(12)
+    dom = (0.0, 1.0, 0.0, 1.0)
+    o = oracle.Oracle(dom, W.EXTRAP, 4, 2)
+    o.set_level(1, W.uniform_level(1, 1, n, n, dom), rng.uniform(-1, 1, 3 * n * n))
+    b2, b3 = [(3, 3, 10, 9)], [(8, 8, 10, 8)]
+    d2 = np.concatenate([W.make_descs([a * R], [b * R], w * R, h * R, 1 / n / R, 1 / n / R, dom) for a, b, w, h in b2])
+    d3 = np.concatenate([W.make_descs([a * R], [b * R], w * R, h * R, 1 / n / R / R, 1 / n / R / R, dom)
+                         for a, b, w, h in b3])
+    o.set_level(2, d2, W.random_ic(d2, 1))
+    o.set_level(3, d3, W.random_ic(d3, 2))
+    q2, q3 = o.read(2, 0), o.read(3, 0)
+    o.regrid(1, b2, R)
+    assert len(o.descs(3)) == 0
+    o.regrid(2, b3, R)
+    assert np.array_equal(o.read(2, 0), q2) and np.array_equal(o.read(3, 0), q3)
+    o.regrid(1, b2, R)
+    o.fill_ghost(1, 0.0)
+    o.advance_level(1, 0.0)                 # time moves (dt = 0): the discarded level 3 is dropped
+    o.regrid(2, b3, R)
+    assert not np.array_equal(o.read(3, 0), q3)
