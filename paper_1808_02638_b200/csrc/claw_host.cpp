@@ -354,6 +354,7 @@ struct claw_ctx {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_free;  // event pool
   uint8_t* h_stage = nullptr;  // pinned staging for flag maps (regrid)
   size_t h_stage_bytes = 0;
+  std::vector<int32_t> sat_scratch;  // clustering table, kept across regrids
   // CUDA graphs of the hierarchy's coarse step
   std::vector<HierGraph> graphs;
   uint64_t epoch = 0;          // bumped whenever levels are (re)defined
@@ -959,8 +960,56 @@ int plan_level(claw_ctx* c, int level, Level& L) {
   for (int p = 0; p < np; ++p)
     if (rc_p[p]) return fail(c, rc_p[p], "%s", msg_p[p].c_str());
   std::vector<Pending> pend;
-  for (int p = 0; p < np; ++p) pend.insert(pend.end(), pend_p[p].begin(), pend_p[p].end());
+  if (world > 1)
+    for (int p = 0; p < np; ++p) pend.insert(pend.end(), pend_p[p].begin(), pend_p[p].end());
   lap("ghosts");
+  // coarse donors of a frame slot: centre, x-, x+, y-, y+ (coarse composite
+  // via clamp/wrap)
+  auto make_spec = [&](const Pending& pd, int64_t slot, DevInterp& sp, std::string& emsg) -> int {
+    sp = DevInterp{};
+    const int64_t cI[5] = {pd.Ic, map_axis(pd.Ic - 1, C->nx, cfg.bc[0], cfg.bc[1]),
+                           map_axis(pd.Ic + 1, C->nx, cfg.bc[0], cfg.bc[1]), pd.Ic, pd.Ic};
+    const int64_t cJ[5] = {pd.Jc, pd.Jc, pd.Jc, map_axis(pd.Jc - 1, C->ny, cfg.bc[2], cfg.bc[3]),
+                           map_axis(pd.Jc + 1, C->ny, cfg.bc[2], cfg.bc[3])};
+    for (int d = 0; d < 5; ++d) {
+      const int q = C->find(cI[d], cJ[d]);
+      if (q < 0 || C->local[q] < 0) {
+        char b[200];
+        std::snprintf(b, sizeof b, "level %d: coarse cell (%lld,%lld) needed for interpolation is not on level %d",
+                      level, (long long)cI[d], (long long)cJ[d], level - 1);
+        emsg = b;
+        return CLAW_ENEST;
+      }
+      const int lq = C->local[q];
+      sp.off[d] = C->off[lq] + (cJ[d] - C->j0[q]) * C->desc[q].mx + (cI[d] - C->i0[q]);
+      sp.cs[d] = static_cast<int64_t>(C->desc[q].mx) * C->desc[q].my;
+    }
+    const int R = L.ratio;
+    sp.xi = (static_cast<double>(pd.I % R) + 0.5) / static_cast<double>(R) - 0.5;
+    sp.eta = (static_cast<double>(pd.J % R) + 0.5) / static_cast<double>(R) - 0.5;
+    sp.dst = L.coarse_frame_off + slot;
+    return CLAW_OK;
+  };
+  if (world == 1) {
+    // one rank: every frame cell is coarse-interpolated; slots in patch order,
+    // specs built per patch in parallel
+    std::vector<int64_t> cstart(np + 1, 0);
+    for (int p = 0; p < np; ++p) cstart[p + 1] = cstart[p] + static_cast<int64_t>(pend_p[p].size());
+    L.coarse_frame_off = 0;
+    L.ncoarse = cstart[np];
+    L.frame_elems = 3 * L.ncoarse;
+    L.hinterp.assign(static_cast<size_t>(L.ncoarse), DevInterp{});
+    parallel_for(host_threads(np), np, [&](int p) {
+      for (size_t k = 0; k < pend_p[p].size() && !rc_p[p]; ++k) {
+        const Pending& pd = pend_p[p][k];
+        const int64_t slot = cstart[p] + static_cast<int64_t>(k);
+        cells[pd.lp][pd.cellidx] = Src{1, slot, L.ncoarse};
+        rc_p[p] = make_spec(pd, slot, L.hinterp[static_cast<size_t>(slot)], msg_p[p]);
+      }
+    });
+    for (int p = 0; p < np; ++p)
+      if (rc_p[p]) return fail(c, rc_p[p], "%s", msg_p[p].c_str());
+  } else {
   // frame layout: [peer 0 segment][peer 1 segment]...[coarse segment], each [3][n]
   // (band mode: planned above, full halo rows per source rank)
   int64_t fo = L.band ? L.frame_elems : 0;
@@ -986,29 +1035,14 @@ int plan_level(claw_ctx* c, int level, Level& L) {
     } else {
       const int64_t k = ck++;
       cells[pd.lp][pd.cellidx] = Src{1, L.coarse_frame_off + k, L.ncoarse};
-      // coarse donors: centre, x-, x+, y-, y+ (coarse composite via clamp/wrap)
-      DevInterp sp{};
-      const int64_t cI[5] = {pd.Ic, map_axis(pd.Ic - 1, C->nx, cfg.bc[0], cfg.bc[1]),
-                             map_axis(pd.Ic + 1, C->nx, cfg.bc[0], cfg.bc[1]), pd.Ic, pd.Ic};
-      const int64_t cJ[5] = {pd.Jc, pd.Jc, pd.Jc, map_axis(pd.Jc - 1, C->ny, cfg.bc[2], cfg.bc[3]),
-                             map_axis(pd.Jc + 1, C->ny, cfg.bc[2], cfg.bc[3])};
-      for (int d = 0; d < 5; ++d) {
-        const int q = C->find(cI[d], cJ[d]);
-        if (q < 0 || C->local[q] < 0)
-          return fail(c, CLAW_ENEST, "level %d: coarse cell (%lld,%lld) needed for interpolation is not on level %d",
-                      level, (long long)cI[d], (long long)cJ[d], level - 1);
-        const int lq = C->local[q];
-        sp.off[d] = C->off[lq] + (cJ[d] - C->j0[q]) * C->desc[q].mx + (cI[d] - C->i0[q]);
-        sp.cs[d] = static_cast<int64_t>(C->desc[q].mx) * C->desc[q].my;
-      }
-      const int R = L.ratio;
-      sp.xi = (static_cast<double>(pd.I % R) + 0.5) / static_cast<double>(R) - 0.5;
-      sp.eta = (static_cast<double>(pd.J % R) + 0.5) / static_cast<double>(R) - 0.5;
-      sp.dst = L.coarse_frame_off + k;
+      DevInterp sp;
+      std::string emsg;
+      if (int rc = make_spec(pd, k, sp, emsg)) return fail(c, rc, "%s", emsg.c_str());
       L.hinterp.push_back(sp);
     }
   }
 
+  }
   lap("frame");
   // rectangles (per patch, in parallel) and device patch records
   std::vector<std::vector<DevRect>> rects_p(L.owned.size());
@@ -1127,7 +1161,7 @@ int plan_level(claw_ctx* c, int level, Level& L) {
   // tiles of patches that read remote (other-rank) ghost cells go last, so a
   // step can run the others while the halo is in flight
   std::vector<char> remote(L.owned.size(), 0);
-  for (size_t lp = 0; lp < L.owned.size(); ++lp)
+  for (size_t lp = 0; lp < L.owned.size() && world > 1; ++lp)
     for (const int64_t code : L.dbg_src[lp])
       if (code == -2) {
         remote[lp] = 1;
@@ -2212,13 +2246,17 @@ namespace {
 // sides; no admissible cut: accept.  Low part before high part.
 struct Clusterer {
   int64_t nx, ny;
-  std::vector<int32_t> sat;  // (ny+1) x (nx+1) prefix counts (maps < 2^31 cells)
+  std::vector<int32_t> own;
+  std::vector<int32_t>& sat;  // (ny+1) x (nx+1) prefix counts (maps < 2^31 cells)
   double cutoff;
   int maxd, mind;
   std::vector<int32_t> out;  // (x0, y0, w, h) quadruples
 
-  Clusterer(const uint8_t* f, int64_t nx_, int64_t ny_, double c, int mx, int mn)
-      : nx(nx_), ny(ny_), sat(static_cast<size_t>((nx_ + 1) * (ny_ + 1))), cutoff(c), maxd(mx), mind(mn) {
+  // scratch: a caller-kept buffer for the table (no fresh pages per regrid)
+  Clusterer(const uint8_t* f, int64_t nx_, int64_t ny_, double c, int mx, int mn,
+            std::vector<int32_t>* scratch = nullptr)
+      : nx(nx_), ny(ny_), sat(scratch ? *scratch : own), cutoff(c), maxd(mx), mind(mn) {
+    sat.resize(static_cast<size_t>((nx + 1) * (ny + 1)));
     const int64_t W = nx + 1;
     const int nt = host_threads(static_cast<int>(std::min<int64_t>(ny, 1 << 20)) * 4);
     // row prefix sums (rows in parallel), then running sums down each column
@@ -2507,6 +2545,7 @@ int claw_regrid(claw_ctx* ctx, int32_t level, int32_t nbox, const int32_t* boxes
     d[b].K = C.desc[0].K;
   }
   Level& L = ctx->lev[level + 1];
+  L.hinterp.swap(old.hinterp);  // reuse the old table's pages (plan_level reassigns it)
   int rc = build_geometry(ctx, level + 1, nbox, d.data(), L);
   if (!rc) rc = plan_level(ctx, level + 1, L);
   if (rc) {
@@ -2617,7 +2656,7 @@ int claw_regrid_auto(claw_ctx* ctx, int32_t level, double tol, int32_t buffer, d
     if (!(cutoff > 0.0) || cutoff > 1.0 || max_dim < 1 || min_dim < 1 || 2 * min_dim > max_dim)
       return fail(ctx, CLAW_EINVAL, "cluster: cutoff=%g max_dim=%d min_dim=%d", cutoff, max_dim, min_dim);
     if (n >= (1ll << 31)) return fail(ctx, CLAW_EINVAL, "regrid_auto: flag map of %lld cells", (long long)n);
-    Clusterer cl(f, C.nx, C.ny, cutoff, max_dim, min_dim);
+    Clusterer cl(f, C.nx, C.ny, cutoff, max_dim, min_dim, &ctx->sat_scratch);
     cl.run();
     // nesting: split each box into row-run rectangles of the nesting mask M
     // (runs identical in consecutive rows merge), drop pieces without flags;
