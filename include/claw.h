@@ -287,11 +287,13 @@ int claw_debug_halo_send(const claw_ctx* ctx, int32_t level, int32_t peer,
                          int64_t k, int32_t* patch, int32_t* i, int32_t* j);
 
 /* The process-wide device memory pool every context allocates from (the
- * paper's GPU memory pool): requests served from cached blocks
- * (hits) or cudaMalloc (misses), and the bytes cached for reuse.  Released
- * blocks are cached per device and size class up to CLAW_POOL_LIMIT_MB
- * (environment, default 16384).  claw_pool_trim returns every cached block
- * to the driver (call with no kernel of the library in flight). */
+ * paper's GPU memory pool): per device, chunks of >= 256 MiB from
+ * cudaMalloc carved best-fit with coalescing frees.  hits = requests served
+ * from free ranges, misses = requests that needed a new chunk, cached_bytes =
+ * free bytes held.  Wholly free chunks beyond CLAW_POOL_LIMIT_MB (environment,
+ * default 16384) of free memory are returned to the driver; claw_pool_trim
+ * returns every wholly free chunk (call with no kernel of the library in
+ * flight). */
 int claw_pool_stats(int64_t* hits, int64_t* misses, int64_t* cached_bytes);
 int claw_pool_trim(void);
 

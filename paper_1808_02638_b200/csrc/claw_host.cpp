@@ -87,39 +87,58 @@ Nccl g_nccl;
 
 // ---------------------------------------------------------------------------
 // Device memory pool (the paper's GPU memory pool: cudaMalloc per
-// patch "can even dominate" with small patches).  Every device buffer of the
-// library comes from here.  Blocks are rounded up to size classes (8 per
-// power of two, >= 4 KiB) and cached per device on release; a request reuses
-// the smallest cached block of its class or up to two classes above (<= 25%
-// slack), so a regrid (which frees one level and allocates a similar one) or
-// a re-set level does not call cudaMalloc.  Releases happen only after the
+// patch "can even dominate" with small patches; the paper's pool "allocates a
+// huge chunk of memory at a time and allocates more chunks when needed").
+// Every device buffer of the library comes from here: per device, chunks of
+// >= 256 MiB from cudaMalloc, carved best-fit (512-byte granules) with free
+// ranges coalesced on release, so regrids and re-set levels of varying sizes
+// reuse memory without calling cudaMalloc.  Releases happen only after the
 // owning context's stream is synchronised (set_level, regrid, destroy), so a
-// block is never reused while a kernel may still touch it.  Cached bytes are
-// capped (CLAW_POOL_LIMIT_MB, default 16384); a failing cudaMalloc first
-// returns the device's cached blocks to the driver and retries.
+// range is never reused while a kernel may still touch it.  Wholly free chunks
+// beyond CLAW_POOL_LIMIT_MB (default 16384) of free memory go back to the
+// driver, and a failing cudaMalloc first returns every free chunk and retries.
 // ---------------------------------------------------------------------------
 struct Pool {
+  static constexpr size_t kGrain = 512;
+  static constexpr size_t kChunk = size_t{256} << 20;
+  struct Dev {
+    std::map<char*, size_t> chunks;        // start -> size
+    std::map<char*, size_t> free_at;       // free ranges by address
+    std::multimap<size_t, char*> free_sz;  // the same by size (best fit)
+    size_t free_bytes = 0;
+  };
   std::mutex mu;
-  std::multimap<std::pair<int, size_t>, void*> cache;  // (device, class bytes) -> block
+  std::map<int, Dev> devs;
   std::unordered_map<void*, std::pair<int, size_t>> live;
-  size_t cached = 0, limit = 0;
+  size_t limit = 0;
   int64_t hits = 0, misses = 0;
   Pool() {
     const char* s = std::getenv("CLAW_POOL_LIMIT_MB");
     limit = static_cast<size_t>(s ? std::atoll(s) : 16384) << 20;
   }
-  static size_t size_class(size_t bytes) {
-    size_t b = std::max<size_t>(bytes, 4096);
-    int e = 63 - __builtin_clzll(b);  // 2^e <= b < 2^(e+1)
-    const size_t step = (size_t{1} << e) / 8;
-    return (b + step - 1) / step * step;
+  static bool is_chunk_start(const Dev& d, char* p) { return d.chunks.count(p) != 0; }
+  void erase_free(Dev& d, char* p, size_t n) {
+    d.free_at.erase(p);
+    auto r = d.free_sz.equal_range(n);
+    for (auto it = r.first; it != r.second; ++it)
+      if (it->second == p) {
+        d.free_sz.erase(it);
+        break;
+      }
+    d.free_bytes -= n;
   }
-  void trim_locked(int dev) {
-    for (auto it = cache.begin(); it != cache.end();) {
-      if (it->first.first == dev) {
-        cudaFree(it->second);
-        cached -= it->first.second;
-        it = cache.erase(it);
+  void insert_free(Dev& d, char* p, size_t n) {
+    d.free_at[p] = n;
+    d.free_sz.emplace(n, p);
+    d.free_bytes += n;
+  }
+  void release_free_chunks(Dev& d, size_t keep) {
+    for (auto it = d.chunks.begin(); it != d.chunks.end() && d.free_bytes > keep;) {
+      auto f = d.free_at.find(it->first);
+      if (f != d.free_at.end() && f->second == it->second) {  // chunk entirely free
+        erase_free(d, it->first, it->second);
+        cudaFree(it->first);
+        it = d.chunks.erase(it);
       } else {
         ++it;
       }
@@ -129,49 +148,75 @@ struct Pool {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
-    const size_t cls = size_class(bytes);
+    const size_t n = (std::max<size_t>(bytes, 1) + kGrain - 1) / kGrain * kGrain;
     std::lock_guard<std::mutex> g(mu);
-    auto it = cache.lower_bound({dev, cls});
-    if (it != cache.end() && it->first.first == dev && it->first.second <= cls + cls / 4) {
-      *out = it->second;
-      live[it->second] = it->first;
-      cached -= it->first.second;
-      cache.erase(it);
+    Dev& d = devs[dev];
+    auto it = d.free_sz.lower_bound(n);
+    if (it == d.free_sz.end()) {
+      const size_t cs = std::max(n, kChunk);
+      void* c = nullptr;
+      e = cudaMalloc(&c, cs);
+      if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        release_free_chunks(d, 0);
+        e = cudaMalloc(&c, cs);
+      }
+      if (e != cudaSuccess) {
+        *out = nullptr;
+        return e;
+      }
+      d.chunks[static_cast<char*>(c)] = cs;
+      insert_free(d, static_cast<char*>(c), cs);
+      ++misses;
+      it = d.free_sz.lower_bound(n);
+    } else {
       ++hits;
-      return cudaSuccess;
     }
-    e = cudaMalloc(out, cls);
-    if (e == cudaErrorMemoryAllocation) {
-      cudaGetLastError();
-      trim_locked(dev);
-      e = cudaMalloc(out, cls);
-    }
-    if (e != cudaSuccess) {
-      *out = nullptr;
-      return e;
-    }
-    live[*out] = {dev, cls};
-    ++misses;
+    char* p = it->second;
+    const size_t fs = it->first;
+    erase_free(d, p, fs);
+    if (fs > n) insert_free(d, p + n, fs - n);
+    live[p] = {dev, n};
+    *out = p;
     return cudaSuccess;
   }
-  void release(void* p) {
+  void release(void* vp) {
     std::lock_guard<std::mutex> g(mu);
-    auto it = live.find(p);
-    if (it == live.end()) return;
-    const auto key = it->second;
-    live.erase(it);
-    if (cached + key.second > limit) {
-      cudaFree(p);
-      return;
+    auto lv = live.find(vp);
+    if (lv == live.end()) return;
+    Dev& d = devs[lv->second.first];
+    char* p = static_cast<char*>(vp);
+    size_t n = lv->second.second;
+    live.erase(lv);
+    // coalesce with the free neighbours inside the same chunk
+    auto nx = d.free_at.find(p + n);
+    if (nx != d.free_at.end() && !is_chunk_start(d, p + n)) {
+      const size_t m = nx->second;
+      erase_free(d, p + n, m);
+      n += m;
     }
-    cache.emplace(key, p);
-    cached += key.second;
+    auto pv = d.free_at.lower_bound(p);
+    if (pv != d.free_at.begin() && !is_chunk_start(d, p)) {
+      --pv;
+      if (pv->first + pv->second == p) {
+        char* q = pv->first;
+        const size_t m = pv->second;
+        erase_free(d, q, m);
+        p = q;
+        n += m;
+      }
+    }
+    insert_free(d, p, n);
+    if (d.free_bytes > limit) release_free_chunks(d, limit);
   }
   void trim_all() {
     std::lock_guard<std::mutex> g(mu);
-    for (auto& kv : cache) cudaFree(kv.second);
-    cache.clear();
-    cached = 0;
+    for (auto& kv : devs) release_free_chunks(kv.second, 0);
+  }
+  size_t cached() {
+    size_t c = 0;
+    for (auto& kv : devs) c += kv.second.free_bytes;
+    return c;
   }
 };
 Pool& pool() {
@@ -2726,7 +2771,7 @@ int claw_pool_stats(int64_t* hits, int64_t* misses, int64_t* cached_bytes) {
   std::lock_guard<std::mutex> g(P.mu);
   if (hits) *hits = P.hits;
   if (misses) *misses = P.misses;
-  if (cached_bytes) *cached_bytes = static_cast<int64_t>(P.cached);
+  if (cached_bytes) *cached_bytes = static_cast<int64_t>(P.cached());
   return CLAW_OK;
 }
 
