@@ -155,16 +155,18 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU oracle on a bounded sample (cpu_baseline / --impl reference)
 # ---------------------------------------------------------------------------
-def oracle_sample(wl: W.Workload, budget_s: float = 12.0, steps_cap: int | None = None, reflux: bool = False):
+def oracle_sample(wl: W.Workload, budget_s: float = 12.0, steps_cap: int | None = None, reflux: bool = False,
+                  threads: int | None = None):
     """Time the oracle as it stands on a sub-level of the same workload shape
-    (same patch size, same scheme) for ~budget_s of CPU work.  Returns
+    (same patch size, same scheme) for ~budget_s of CPU work, with `threads`
+    OpenMP threads over patches (default: every host core).  Returns
     (cell-updates/s, cores, description)."""
     import oracle
     d0 = wl.levels[0].descs
     mx, my = int(d0["mx"][0]), int(d0["my"][0])
     uniform = len(wl.levels) == 1 and not wl.extra.get("ratios") and (d0["mx"] == mx).all() and \
         (d0["my"] == my).all()
-    cores = host_cores()
+    cores = threads or host_cores()
     if uniform:
         side = max(1, min(int(math.sqrt(len(d0))), max(1, 1024 // mx)))  # ~1024^2 cells max
         dx = float(d0["dx"][0])
@@ -535,8 +537,10 @@ def main():
         import oracle
         oracle.build()
         v, cores, desc = oracle_sample(wl, budget_s=12.0, reflux=args.reflux)
+        v1, _, desc1 = oracle_sample(wl, budget_s=4.0, reflux=args.reflux, threads=1)
         cpu = {"value": v, "unit": "cell-updates/s", "cores": cores, "kind": "oracle", "sample": desc,
-               "cpu": cpu_model()}
+               "cpu": cpu_model(),
+               "single_thread": {"value": v1, "cores": 1, "sample": desc1}}
 
     clk = clocks.summary()
     gpu_launches = st["step_launches"] + st["ghost_launches"]
