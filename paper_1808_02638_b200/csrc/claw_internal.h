@@ -93,6 +93,9 @@ struct StepParams {
   int32_t tile_offset;            // generic tiles: first tile index of this launch
   int64_t hoff[4];                // band halo rows Y0-2, Y0-1, Y1, Y1+1: frame offset of
   int64_t hcs[4];                 // column 0 (-1: the row is local) and component stride
+  double* side;                   // generic kernel: per-tile side records (side_stride()
+                                  // doubles per tile), filled by a side_kernel launched
+                                  // ahead of the step kernel; null: computed in the kernel
 };
 
 // Launchers (claw_kernels.cu).  All return cudaError_t as int.
@@ -186,6 +189,7 @@ struct RegridParams {
 };
 int launch_regrid(const RegridParams& p, int32_t nnew, void* stream);
 int max_tile_rows();
+int side_stride();
 int grid_strip();
 
 }  // namespace claw
