@@ -109,3 +109,38 @@ def test_full_size_hierarchy_covers_every_flag():
     cfl = g.advance_hierarchy(0.0, wl.dt0(), update=True)
     assert abs(cfl - wl.cfl) < 1e-12
     g.close()
+
+
+def test_dynamic_run_with_conservation_fix_conserves_and_matches():
+    """Dynamic hierarchy + updating + the conservation fix (periodic BCs):
+    regrids re-create levels 2-3 (their registers rebuilt empty), and the
+    level-1 totals of p, u, v stay constant to round-off through the steps
+    and the regrids; GPU = oracle throughout."""
+    wl = W.paper(n1=64, npx=4)
+    wl.bc = W.PERIODIC
+    R = wl.extra["ratios"]
+    nlev = 1 + len(R)
+    d1 = wl.levels[0].descs
+    q1 = W.ring_ic(d1)
+    g = binding.Claw(wl.domain, wl.bc, wl.limiter, wl.order_trans, device=0, reflux=True)
+    o = oracle.Oracle(wl.domain, wl.bc, wl.limiter, wl.order_trans, reflux=True)
+    for h in (g, o):
+        h.set_level(1, d1, q1)
+    regrid_both(g, o, wl, 0.0, nlev)
+    dt = wl.dt0()
+    totals = [g.read_level(1).reshape(len(d1), 3, -1).sum(axis=(0, 2))]
+    for n in range(6):
+        g.advance_hierarchy(n * dt, dt, update=True)
+        bo_oracle(o, 1, n * dt, dt, R, nlev)
+        for L in range(1, nlev + 1):
+            qg, qo = g.read_level(L), o.read_level(L)
+            assert np.abs(qg - qo).max() <= TOL * np.abs(qo).max(), (n, L)
+        totals.append(g.read_level(1).reshape(len(d1), 3, -1).sum(axis=(0, 2)))
+        if (n + 1) % 2 == 0:
+            for L in range(1, nlev + 1):
+                g.write_level(L, o.read_level(L))
+            regrid_both(g, o, wl, (n + 1) * dt, nlev)
+    scale = np.abs(g.read_level(1)).sum()
+    drift = np.abs(np.array(totals[1:]) - totals[0]).max()
+    assert drift <= 1e-13 * scale, (drift, scale)
+    g.close()
