@@ -1567,6 +1567,10 @@ int claw_create(const claw_config* cfg, claw_ctx** out) {
   ctx->tile_rows = cfg->tile_rows > 0 ? cfg->tile_rows : claw::max_tile_rows();
   ctx->host_only = cfg->device < 0;
   {
+    const char* pd = std::getenv("CLAW_PDL");  // programmatic dependent launches (default on)
+    claw::set_pdl(pd ? std::atoi(pd) : 1);
+  }
+  {
     // opt-in (CLAW_GRAPH=1): measured slower than the asynchronous launch
     // sequence, which never starves the GPU inside a coarse step
     const char* gv = std::getenv("CLAW_GRAPH");

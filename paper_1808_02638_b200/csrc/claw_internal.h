@@ -188,6 +188,9 @@ struct RegridParams {
   int32_t* err;
 };
 int launch_regrid(const RegridParams& p, int32_t nnew, void* stream);
+// programmatic dependent launches of the step-sequence kernels (default on)
+extern int g_pdl;
+void set_pdl(int on);
 int max_tile_rows();
 int side_stride();
 int grid_strip();
