@@ -162,7 +162,9 @@ int claw_patch_cfl(claw_ctx* ctx, int32_t level, int32_t patch, double* cfl);
 
 int claw_owner(const claw_ctx* ctx, int32_t level, int32_t patch, int32_t* rank);
 /* Kernel path chosen for a level: 0 generic ghost-table kernel, 1 grid kernel
- * (see claw_config.path). */
+ * (see claw_config.path), 2 grid kernel on a sparse lattice (a finer level of
+ * equal, lattice-aligned patches: one rank, one medium; coarse ghost values are
+ * kept in the lattice's empty slots). */
 int claw_level_mode(const claw_ctx* ctx, int32_t level, int32_t* mode);
 
 /* Updating: every level-(level-1) cell whose R x R

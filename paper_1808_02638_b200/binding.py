@@ -300,7 +300,7 @@ class Claw:
     def level_mode(self, level: int) -> str:
         m = ctypes.c_int32()
         self._check(load().claw_level_mode(self._h, level, ctypes.byref(m)))
-        return "grid" if m.value == 1 else "generic"
+        return {1: "grid", 2: "sparse"}.get(m.value, "generic")
 
     def advance_hierarchy(self, t: float, dt: float, update: bool = False) -> float:
         """One coarse step of every level with subcycling (and, with update,

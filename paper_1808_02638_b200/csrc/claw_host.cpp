@@ -12,6 +12,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <climits>
 #include <chrono>
 #include <array>
 #include <cmath>
@@ -349,6 +350,13 @@ struct Level {
   int64_t ngrid_blocks = 0;   // row blocks of the band (grid mode)
   int grid_th = 0;            // rows per grid tile (> my: tiles span patch rows)
   bool use_side = false;      // generic kernel: side records by a side_kernel ahead of the step
+  bool sparse = false;        // grid kernel on a sparse lattice of equal patches
+  std::vector<int32_t> hslots;  // lattice slot -> patch (>= 0) or -1-v (virtual slot v)
+  int32_t nvirt = 0;
+  std::vector<int4> hgtile;   // sparse lattice: (strip, row block) tiles
+  DevBuf<int32_t> dslots;
+  DevBuf<int4> dgtile;
+  int64_t frame_cs = 0;       // component stride of the coarse frame cells (interp_kernel)
   DevBuf<double> side;
   int64_t ntile_interior = 0; // generic tiles [0, n) read no remote ghost cell
   bool halo_pending = false;  // NCCL halo in flight on the comm stream
@@ -993,6 +1001,35 @@ int plan_level(claw_ctx* c, int level, Level& L) {
       }
       return CLAW_OK;
   };
+  // sparse lattice (grid kernel on a level of equal, lattice-aligned patches
+  // that does not cover the domain, e.g. C3's level 3): one rank, one medium,
+  // level > 1; the frame is laid out as the lattice's empty slots ("virtual
+  // patches"), so coarse ghost values sit where the grid kernel's arithmetic
+  // addressing looks for them (CLAW_SPARSE=0 disables)
+  L.sparse = false;
+  L.hslots.clear();
+  {
+    const char* e = std::getenv("CLAW_SPARSE");
+    bool ok = !(e && e[0] == '0') && world == 1 && cfg.path == 0 && level > 1 && np > 0 && L.gapless;
+    const int mx = np ? L.desc[0].mx : 0, my = np ? L.desc[0].my : 0;
+    if (ok) ok = L.nx % mx == 0 && L.ny % my == 0 && L.nx < (1ll << 30) && L.ny < (1ll << 30);
+    for (int p = 0; ok && p < np; ++p)
+      ok = L.desc[p].mx == mx && L.desc[p].my == my && L.i0[p] % mx == 0 && L.j0[p] % my == 0 &&
+           L.desc[p].rho == L.desc[0].rho && L.desc[p].K == L.desc[0].K &&
+           L.off[L.local[p]] == static_cast<int64_t>(L.local[p]) * 3 * mx * my;
+    const int64_t npx = ok ? L.nx / mx : 0, npy = ok ? L.ny / my : 0;
+    ok = ok && npx * npy > np && npx * npy <= 4ll * np && npx * npy < (1ll << 30);
+    if (ok) {
+      L.sparse = true;
+      L.npx = static_cast<int>(npx);
+      L.hslots.assign(static_cast<size_t>(npx * npy), INT32_MIN);
+      for (int p = 0; p < np; ++p) L.hslots[(L.j0[p] / my) * npx + L.i0[p] / mx] = L.local[p];
+      int32_t v = 0;
+      for (auto& x : L.hslots)
+        if (x == INT32_MIN) x = -1 - v++;
+      L.nvirt = v;
+    }
+  }
   lap("pre");
   // per patch; in parallel on one rank (every patch is owned, nothing is
   // sent), the pending frame cells concatenated in patch order afterwards
@@ -1045,13 +1082,28 @@ int plan_level(claw_ctx* c, int level, Level& L) {
     L.coarse_frame_off = 0;
     L.ncoarse = cstart[np];
     L.frame_elems = 3 * L.ncoarse;
+    L.frame_cs = L.ncoarse;
+    const int smx = np ? L.desc[0].mx : 1, smy = np ? L.desc[0].my : 1;
+    if (L.sparse) {  // frame = the lattice's virtual slots, [slot][3][my][mx]
+      L.frame_elems = static_cast<int64_t>(L.nvirt) * 3 * smx * smy;
+      L.frame_cs = static_cast<int64_t>(smx) * smy;
+    }
     L.hinterp.assign(static_cast<size_t>(L.ncoarse), DevInterp{});
     parallel_for(host_threads(np), np, [&](int p) {
       for (size_t k = 0; k < pend_p[p].size() && !rc_p[p]; ++k) {
         const Pending& pd = pend_p[p][k];
         const int64_t slot = cstart[p] + static_cast<int64_t>(k);
-        cells[pd.lp][pd.cellidx] = Src{1, slot, L.ncoarse};
-        rc_p[p] = make_spec(pd, slot, L.hinterp[static_cast<size_t>(slot)], msg_p[p]);
+        DevInterp& sp = L.hinterp[static_cast<size_t>(slot)];
+        rc_p[p] = make_spec(pd, slot, sp, msg_p[p]);
+        if (L.sparse) {
+          const int32_t sl = L.hslots[(pd.J / smy) * L.npx + pd.I / smx];
+          if (sl >= 0) {
+            rc_p[p] = CLAW_EINVAL;
+            msg_p[p] = "sparse lattice: a coarse ghost cell inside a patch slot";
+          }
+          sp.dst = static_cast<int64_t>(-1 - sl) * 3 * smx * smy + (pd.J % smy) * smx + pd.I % smx;
+        }
+        cells[pd.lp][pd.cellidx] = Src{1, sp.dst, L.frame_cs};
       }
     });
     for (int p = 0; p < np; ++p)
@@ -1073,6 +1125,7 @@ int plan_level(claw_ctx* c, int level, Level& L) {
   for (const Pending& pd : pend)
     if (pd.kind == 2) L.ncoarse++;
   L.frame_elems = fo + 3 * L.ncoarse;
+  L.frame_cs = L.ncoarse;
   std::vector<int64_t> rk(world, 0);
   int64_t ck = 0;
   for (const Pending& pd : pend) {
@@ -1149,7 +1202,30 @@ int plan_level(claw_ctx* c, int level, Level& L) {
   }
   // grid mode: whole domain tiled by equal patches in row-major order, gapless
   L.grid = false;
-  if (L.uniform && c->cfg.path == 0 && (world == 1 || L.band) && L.gapless && !L.owned.empty()) {
+  if (L.sparse && L.uniform) {
+    // sparse lattice: the grid kernel over listed (strip, row block) tiles that
+    // hold at least one patch cell; tiles stay inside one patch row
+    const int mx = L.desc[0].mx, my = L.desc[0].my;
+    L.grid = true;
+    L.Y0 = 0;
+    L.Y1 = L.ny;
+    const int th = std::min(L.th, my);
+    L.grid_th = th;
+    const int nbr = (my + th - 1) / th;
+    const int64_t npy = L.ny / my, nstrip = (L.nx + claw::grid_strip() - 1) / claw::grid_strip();
+    L.hgtile.clear();
+    for (int64_t pr = 0; pr < npy; ++pr)
+      for (int rb = 0; rb < nbr; ++rb)
+        for (int64_t st = 0; st < nstrip; ++st) {
+          const int64_t c0 = st * claw::grid_strip(), c1 = std::min<int64_t>(L.nx, c0 + claw::grid_strip());
+          bool any = false;
+          for (int64_t pc = c0 / mx; pc <= (c1 - 1) / mx && !any; ++pc) any = L.hslots[pr * L.npx + pc] >= 0;
+          if (any) L.hgtile.push_back(make_int4(static_cast<int>(st), static_cast<int>(pr * nbr + rb), 0, 0));
+        }
+    L.ngrid_tiles = static_cast<int64_t>(L.hgtile.size());
+    L.ngrid_blocks = npy * nbr;
+  } else if (L.uniform && c->cfg.path == 0 && (world == 1 || L.band) && L.gapless && !L.owned.empty() &&
+             !L.sparse) {
     const int mx = L.desc[0].mx, my = L.desc[0].my;
     bool ok = (L.nx % mx == 0) && (L.ny % my == 0) &&
               static_cast<int64_t>(np) == (L.nx / mx) * (L.ny / my);
@@ -1432,6 +1508,8 @@ int alloc_level(claw_ctx* ctx, int level, Level& L) {
   if (int r2 = upload(ctx, L.dinterp, L.hinterp)) return r2;
   if (int r2 = upload(ctx, L.du, L.hu)) return r2;
   if (int r2 = upload(ctx, L.dur, L.hur)) return r2;
+  if (int r2 = upload(ctx, L.dslots, L.hslots)) return r2;
+  if (int r2 = upload(ctx, L.dgtile, L.hgtile)) return r2;
   if (int r2 = upload(ctx, L.du_src, L.hu_src)) return r2;
   if (int r2 = upload(ctx, L.du_scs, L.hu_scs)) return r2;
   if (int r2 = upload(ctx, L.dreg, L.hreg)) return r2;
@@ -1719,7 +1797,7 @@ int claw_fill_ghost(claw_ctx* ctx, int32_t level, double t) {
     // DevInterp.dst is an absolute frame offset; components are ncoarse apart
     if (!ctx->dry)
       CUDA_TRY(static_cast<cudaError_t>(claw::launch_interp(C.q[1 - C.cur].p, C.q[C.cur].p, alpha, adev,
-                                                            L.dinterp.p, L.ncoarse, L.frame.p, L.ncoarse,
+                                                            L.dinterp.p, L.ncoarse, L.frame.p, L.frame_cs,
                                                             ctx->stream)));
     ctx->stats.ghost_launches++;
   }
@@ -1805,6 +1883,10 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
     P.per_x = ctx->cfg.bc[0] == CLAW_BC_PERIODIC;
     P.per_y = ctx->cfg.bc[2] == CLAW_BC_PERIODIC;
     P.ntiles = static_cast<int32_t>(L.ngrid_tiles);
+    if (L.sparse) {
+      P.slots = L.dslots.p;
+      P.tiles = L.dgtile.p;
+    }
     P.Y0 = static_cast<int32_t>(L.Y0);
     P.Y1 = static_cast<int32_t>(L.Y1);
     for (int k = 0; k < 4; ++k) {
@@ -2029,7 +2111,7 @@ int claw_owner(const claw_ctx* ctx, int32_t level, int32_t patch, int32_t* rank)
 
 int claw_level_mode(const claw_ctx* ctx, int32_t level, int32_t* mode) {
   if (!ctx || !mode || level < 1 || level > kMaxLevel || !ctx->lev[level].set) return CLAW_EINVAL;
-  *mode = ctx->lev[level].grid ? 1 : 0;
+  *mode = ctx->lev[level].grid ? (ctx->lev[level].sparse ? 2 : 1) : 0;
   return CLAW_OK;
 }
 

@@ -93,6 +93,10 @@ struct StepParams {
   int32_t tile_offset;            // generic tiles: first tile index of this launch
   int64_t hoff[4];                // band halo rows Y0-2, Y0-1, Y1, Y1+1: frame offset of
   int64_t hcs[4];                 // column 0 (-1: the row is local) and component stride
+  const int32_t* slots;           // grid kernel on a sparse lattice of equal patches: per
+                                  // lattice slot (row-major, npx per row) the patch index
+                                  // (>= 0) or -1-v for virtual slot v of the frame (coarse
+                                  // ghost values); P.tiles then lists (strip, row block)
   double* side;                   // generic kernel: per-tile side records (side_stride()
                                   // doubles per tile), filled by a side_kernel launched
                                   // ahead of the step kernel; null: computed in the kernel

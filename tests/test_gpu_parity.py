@@ -454,3 +454,42 @@ def test_grid_tiles_spanning_patch_rows(npx, npy, mx, my, th, bc, monkeypatch):
         res.append((g.read_level(1), c))
         g.close()
     assert np.array_equal(res[0][0], res[1][0]) and res[0][1] == res[1][1]
+
+
+@pytest.mark.parametrize("case", ["c3", "r2_periodic", "r4_extrap"])
+def test_sparse_lattice_grid_kernel_bitwise_equals_generic(case):
+    """A finer level of equal, lattice-aligned patches (not covering the
+    domain) runs the grid kernel on a sparse lattice, its coarse ghost values
+    in the lattice's empty slots: bitwise equal to the generic kernel, through
+    hierarchy steps with updating."""
+    if case == "c3":
+        wl = W.c3()
+        levels = [lv.descs for lv in wl.levels]
+        q0s = W.hierarchy_ic(wl)
+        dom, bc, nsteps = wl.domain, wl.bc, 2
+    else:
+        dom, nsteps = W.DOMAIN, 4
+        if case == "r2_periodic":
+            n1, R, mx, bc = 32, 2, 8, W.PERIODIC
+            slots = [(x, y) for x in range(8) for y in range(8) if 2 <= x + y <= 11 and (3 * x + y) % 4 != 0]
+        else:
+            n1, R, mx, bc = 16, 4, 16, W.EXTRAP
+            slots = [(0, 0), (1, 0), (1, 1), (2, 1), (3, 2), (3, 3)]
+        d1 = W.uniform_level(2, 2, n1 // 2, n1 // 2, dom)
+        dxf = (dom[1] - dom[0]) / n1 / R
+        d2 = np.concatenate([W.make_descs([x * mx], [y * mx], mx, mx, dxf, dxf, dom) for x, y in slots])
+        levels = [d1, d2]
+        q0s = [W.random_ic(d1, 3), W.random_ic(d2, 4)]
+    res = []
+    for path in (0, 1):
+        g = binding.Claw(dom, bc, 4, 2, device=0, path=path)
+        for L, (d, q) in enumerate(zip(levels, q0s), start=1):
+            g.set_level(L, d, q)
+        assert g.level_mode(len(levels)) == ("sparse" if path == 0 else "generic")
+        dt = 0.9 * float(levels[0]["dx"][0])
+        cfl = [g.advance_hierarchy(n * dt, dt, update=True) for n in range(nsteps)]
+        res.append(([g.read_level(L) for L in range(1, len(levels) + 1)], cfl))
+        g.close()
+    assert res[0][1] == res[1][1]
+    for x, y in zip(res[0][0], res[1][0]):
+        assert np.array_equal(x, y)
