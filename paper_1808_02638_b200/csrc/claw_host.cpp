@@ -349,6 +349,7 @@ struct Level {
   int64_t ngrid_tiles = 0;
   int64_t ngrid_blocks = 0;   // row blocks of the band (grid mode)
   int grid_th = 0;            // rows per grid tile (> my: tiles span patch rows)
+  int grid_wide = 0;          // grid mode runs the wide kernel (two columns per lane)
   bool use_side = false;      // generic kernel: side records by a side_kernel ahead of the step
   bool sparse = false;        // grid kernel on a sparse lattice of equal patches
   std::vector<int32_t> hslots;  // lattice slot -> patch (>= 0) or -1-v (virtual slot v)
@@ -423,6 +424,16 @@ struct claw_ctx {
 };
 
 namespace {
+
+// the wide grid kernel (two columns per lane) is opt-in (CLAW_GRID_WIDE=1):
+// 15% fewer instructions but 12 instead of 16 resident warps per SM, measured
+// 2.5% (C5) / 7% (C4) slower than the 32-lane kernel (profiles/README.md).
+// It needs even patch widths, so a lane's column pair never straddles patches.
+int grid_wide_ok(int mx) {
+  const char* e = std::getenv("CLAW_GRID_WIDE");
+  if (!e || e[0] != '1') return 0;
+  return mx % 2 == 0 ? 1 : 0;
+}
 
 int fail(claw_ctx* c, int code, const char* fmt, ...) {
   if (c) {
@@ -1212,12 +1223,14 @@ int plan_level(claw_ctx* c, int level, Level& L) {
     const int th = std::min(L.th, my);
     L.grid_th = th;
     const int nbr = (my + th - 1) / th;
-    const int64_t npy = L.ny / my, nstrip = (L.nx + claw::grid_strip() - 1) / claw::grid_strip();
+    L.grid_wide = grid_wide_ok(mx);
+    const int64_t npy = L.ny / my, nstrip = claw::grid_nstrip(L.nx, L.grid_wide);
     L.hgtile.clear();
     for (int64_t pr = 0; pr < npy; ++pr)
       for (int rb = 0; rb < nbr; ++rb)
         for (int64_t st = 0; st < nstrip; ++st) {
-          const int64_t c0 = st * claw::grid_strip(), c1 = std::min<int64_t>(L.nx, c0 + claw::grid_strip());
+          int64_t c0, c1;
+          claw::grid_strip_cols(st, L.grid_wide, L.nx, c0, c1);
           bool any = false;
           for (int64_t pc = c0 / mx; pc <= (c1 - 1) / mx && !any; ++pc) any = L.hslots[pr * L.npx + pc] >= 0;
           if (any) L.hgtile.push_back(make_int4(static_cast<int>(st), static_cast<int>(pr * nbr + rb), 0, 0));
@@ -1250,7 +1263,8 @@ int plan_level(claw_ctx* c, int level, Level& L) {
       // patch-row boundaries), which halves the per-tile prologue on 32-row
       // patches; CLAW_GRID_TH overrides (tuning)
       int th = std::min(L.th, my);
-      const int64_t nstrip0 = (L.nx + claw::grid_strip() - 1) / claw::grid_strip();
+      L.grid_wide = grid_wide_ok(mx);
+      const int64_t nstrip0 = claw::grid_nstrip(L.nx, L.grid_wide);
       auto span_ok = [&](int w) { return w > my && w % my == 0 && my % 4 == 0 && my >= 8 && w <= 512; };
       if (const char* e = std::getenv("CLAW_GRID_TH")) {
         if (span_ok(std::atoi(e))) th = std::atoi(e);
@@ -1267,7 +1281,7 @@ int plan_level(claw_ctx* c, int level, Level& L) {
           }
       }
       L.grid_th = th;
-      const int64_t nstrip = (L.nx + claw::grid_strip() - 1) / claw::grid_strip();
+      const int64_t nstrip = claw::grid_nstrip(L.nx, L.grid_wide);
       L.ngrid_blocks = th > my ? ((L.Y1 - L.Y0) + th - 1) / th : ((L.Y1 - L.Y0) / my) * ((my + th - 1) / th);
       L.ngrid_tiles = nstrip * L.ngrid_blocks;
     }
@@ -1880,6 +1894,7 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
     P.my = L.desc[0].my;
     P.npx = L.npx;
     P.th = L.grid_th;
+    P.wide = L.grid_wide;
     P.per_x = ctx->cfg.bc[0] == CLAW_BC_PERIODIC;
     P.per_y = ctx->cfg.bc[2] == CLAW_BC_PERIODIC;
     P.ntiles = static_cast<int32_t>(L.ngrid_tiles);
@@ -1901,7 +1916,7 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
     claw::StepParams Pi = P, Pe = P;
     int64_t n_int = 0, n_all = 0;
     if (L.grid) {
-      const int64_t nstrip = (L.nx + claw::grid_strip() - 1) / claw::grid_strip();
+      const int64_t nstrip = claw::grid_nstrip(L.nx, L.grid_wide);
       const int64_t nb = L.ngrid_blocks;
       if (nb >= 3) {
         Pi.blk_first = 1;
