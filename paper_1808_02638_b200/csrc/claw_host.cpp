@@ -295,6 +295,7 @@ struct Level {
   std::vector<DevPatch> hpatch;
   std::vector<DevRect> hrect;
   std::vector<int4> htile;
+  int lane_tiles = 0;         // generic tiles: 30-column strips for step_lane_kernel
   std::vector<DevInterp> hinterp;
   // debug: per owned patch, per padded cell, donor code
   std::vector<std::vector<int64_t>> dbg_src, dbg_remote;
@@ -1286,12 +1287,32 @@ int plan_level(claw_ctx* c, int level, Level& L) {
       L.ngrid_tiles = nstrip * L.ngrid_blocks;
     }
   }
+  // generic tiles: strips of 30 columns for the halo-lane kernel (default;
+  // CLAW_LANE=0 selects the side-pass kernel and 32-column strips)
+  // (auto: where 30-column strips need at most 20% more warps than 32-column
+  // ones -- measured 9% faster per coarse step on the paper workload's mixed
+  // widths and 13% on C2, but 21% slower on uniform 64-wide patches, which
+  // take 3 strips instead of 2; profiles/r01_lane_kernel.txt)
+  {
+    const char* e = std::getenv("CLAW_LANE");
+    if (e && (e[0] == '0' || e[0] == '1')) {
+      L.lane_tiles = e[0] == '1';
+    } else {
+      int64_t n30 = 0, n32 = 0;
+      for (size_t lp = 0; lp < L.owned.size(); ++lp) {
+        n30 += (L.hpatch[lp].mx + 29) / 30;
+        n32 += (L.hpatch[lp].mx + 31) / 32;
+      }
+      L.lane_tiles = 5 * n30 <= 6 * n32 ? 1 : 0;
+    }
+  }
+  const int tstrip = L.lane_tiles ? 30 : 32;
   L.htile.clear();
   for (size_t lp = 0; lp < L.owned.size(); ++lp) {
     const int mx = L.hpatch[lp].mx, my = L.hpatch[lp].my;
     for (int j0 = 0; j0 < my; j0 += L.th)
-      for (int i0 = 0; i0 < mx; i0 += 32) {
-        const int tw = std::min(32, mx - i0), th = std::min(L.th, my - j0);
+      for (int i0 = 0; i0 < mx; i0 += tstrip) {
+        const int tw = std::min(tstrip, mx - i0), th = std::min(L.th, my - j0);
         L.htile.push_back(make_int4(static_cast<int>(lp), i0, j0, tw | (th << 16)));
       }
   }
@@ -1554,7 +1575,7 @@ int alloc_level(claw_ctx* ctx, int level, Level& L) {
   {
     const char* e = std::getenv("CLAW_SIDE");
     const bool want = e ? e[0] == '1' : (L.htile.size() >= 1024 && L.th >= 64);
-    L.use_side = want && !L.grid && ctx->cfg.world == 1 && !L.htile.empty();
+    L.use_side = want && !L.grid && !L.lane_tiles && ctx->cfg.world == 1 && !L.htile.empty();
     if (L.use_side) CUDA_TRY(L.side.alloc(L.htile.size() * static_cast<size_t>(claw::side_stride())));
   }
   L.device_bytes = 2 * L.buf_elems * 8 + L.frame_elems * 8 +
@@ -1874,6 +1895,7 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
   P.rects = L.drect.p;
   P.tiles = L.dtile.p;
   P.ntiles = static_cast<int32_t>(L.htile.size());
+  P.lane_tiles = L.lane_tiles;
   P.limiter = ctx->cfg.limiter;
   P.order_trans = ctx->cfg.order_trans;
   P.dt = dt;

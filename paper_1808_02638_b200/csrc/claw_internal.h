@@ -79,7 +79,7 @@ struct StepParams {
   unsigned long long* level_cfl_reset;  // the other generation's slot, zeroed by the kernel
   unsigned long long* hier_cfl;   // coarse-step slot of claw_advance_hierarchy, or null
   int32_t uniform;                // 1: every patch uses `k` below
-  int32_t pad2;
+  int32_t lane_tiles;             // generic tiles are 30-column strips for step_lane_kernel
   StepConsts k;
   // grid mode (uniform tiling of the whole domain by equal patches in
   // row-major order, gapless buffer): level-index strips, no tables

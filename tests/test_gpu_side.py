@@ -20,6 +20,7 @@ def _gpu():
 
 def run_level(descs, q0, side, limiter, ot, tile_rows, bc, steps, monkeypatch):
     monkeypatch.setenv("CLAW_SIDE", "1" if side else "0")
+    monkeypatch.setenv("CLAW_LANE", "0")  # the side-pass kernel (not the halo-lane one)
     g = binding.Claw(W.DOMAIN, bc, limiter, ot, device=0, tile_rows=tile_rows, path=1)
     g.set_level(1, descs, q0)
     dt = (0.8 if ot else 0.4) * 2.0 / 40
@@ -50,6 +51,7 @@ def test_side_kernel_on_c3_hierarchy(monkeypatch):
     res = []
     for side in (True, False):
         monkeypatch.setenv("CLAW_SIDE", "1" if side else "0")
+        monkeypatch.setenv("CLAW_LANE", "0")  # the side-pass kernel (not the halo-lane one)
         g = binding.Claw(wl.domain, wl.bc, wl.limiter, wl.order_trans, device=0)
         for L, (lv, q) in enumerate(zip(wl.levels, q0s), start=1):
             g.set_level(L, lv.descs, q)
