@@ -12,6 +12,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <functional>
+#include <condition_variable>
 #include <climits>
 #include <chrono>
 #include <array>
@@ -91,7 +93,7 @@ Nccl g_nccl;
 // patch "can even dominate" with small patches; the paper's pool "allocates a
 // huge chunk of memory at a time and allocates more chunks when needed").
 // Every device buffer of the library comes from here: per device, chunks of
-// >= 256 MiB from cudaMalloc, carved best-fit (512-byte granules) with free
+// >= 256 MiB (growing geometrically up to 2 GiB) from cudaMalloc, carved best-fit (512-byte granules) with free
 // ranges coalesced on release, so regrids and re-set levels of varying sizes
 // reuse memory without calling cudaMalloc.  Releases happen only after the
 // owning context's stream is synchronised (set_level, regrid, destroy), so a
@@ -154,9 +156,20 @@ struct Pool {
     Dev& d = devs[dev];
     auto it = d.free_sz.lower_bound(n);
     if (it == d.free_sz.end()) {
-      const size_t cs = std::max(n, kChunk);
+      // geometric growth (a new chunk at least as large as all chunks so far):
+      // cudaMalloc of a few hundred MB costs 15-50 ms on B200, so a growing
+      // workload (the paper's regrids) misses O(log) times, not once per size
+      // (capped at 2 GiB; if that much is not free, just the request)
+      size_t have = 0;
+      for (const auto& ch : d.chunks) have += ch.second;
+      size_t cs = std::max({n, kChunk, std::min(have, size_t{2} << 30)});
       void* c = nullptr;
       e = cudaMalloc(&c, cs);
+      if (e == cudaErrorMemoryAllocation && cs > std::max(n, kChunk)) {
+        cudaGetLastError();
+        cs = std::max(n, kChunk);
+        e = cudaMalloc(&c, cs);
+      }
       if (e == cudaErrorMemoryAllocation) {
         cudaGetLastError();
         release_free_chunks(d, 0);
@@ -411,7 +424,6 @@ struct claw_ctx {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_free;  // event pool
   uint8_t* h_stage = nullptr;  // pinned staging for flag maps (regrid)
   size_t h_stage_bytes = 0;
-  std::vector<int32_t> sat_scratch;  // clustering table, kept across regrids
   // CUDA graphs of the hierarchy's coarse step
   std::vector<HierGraph> graphs;
   uint64_t epoch = 0;          // bumped whenever levels are (re)defined
@@ -765,6 +777,75 @@ struct PhaseTrace {
   }
 };
 
+// Persistent host workers for parallel_for: a regrid runs ~10 parallel loops
+// of the planner and clusterer, and creating and joining 16 std::threads per
+// loop cost milliseconds.  The caller takes part as thread 0; thread t runs
+// indices t, t + nthr, ...; jobs are serialised; a loop body that itself calls
+// parallel_for runs that loop serially.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool* p = new HostPool();  // never destroyed (workers detached at exit)
+    return *p;
+  }
+  static bool& in_worker() {
+    thread_local bool w = false;
+    return w;
+  }
+  void run(int nthr, int n, const std::function<void(int)>& f) {
+    std::lock_guard<std::mutex> one(run_mu_);
+    nthr = std::min(nthr, 1 + static_cast<int>(workers_.size()));
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      job_ = &f;
+      n_ = n;
+      nthr_ = nthr;
+      pending_ = nthr - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    in_worker() = true;
+    for (int k = 0; k < n; k += nthr) f(k);
+    in_worker() = false;
+    std::unique_lock<std::mutex> g(mu_);
+    done_.wait(g, [&] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  HostPool() {
+    const int nw = std::max(0, std::min(31, static_cast<int>(std::thread::hardware_concurrency()) - 1));
+    for (int t = 1; t <= nw; ++t) workers_.emplace_back([this, t] { loop(t); });
+    for (auto& w : workers_) w.detach();
+  }
+  void loop(int t) {
+    in_worker() = true;
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int)>* f;
+      int n, nthr;
+      {
+        std::unique_lock<std::mutex> g(mu_);
+        cv_.wait(g, [&] { return gen_ != seen; });
+        seen = gen_;
+        f = job_;
+        n = n_;
+        nthr = nthr_;
+      }
+      if (t >= nthr) continue;
+      for (int k = t; k < n; k += nthr) (*f)(k);
+      std::lock_guard<std::mutex> g(mu_);
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex run_mu_, mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* job_ = nullptr;
+  int n_ = 0, nthr_ = 0, pending_ = 0;
+  uint64_t gen_ = 0;
+};
+
 // Host threads for the planner's per-patch loops (results are assembled in
 // patch order, so they do not depend on the thread count).
 int host_threads(int nwork) {
@@ -778,16 +859,12 @@ int host_threads(int nwork) {
 
 template <class F>
 void parallel_for(int nthr, int n, F&& f) {
-  if (nthr <= 1) {
+  if (nthr <= 1 || HostPool::in_worker()) {
     for (int k = 0; k < n; ++k) f(k);
     return;
   }
-  std::vector<std::thread> th;
-  for (int t = 0; t < nthr; ++t)
-    th.emplace_back([&, t] {
-      for (int k = t; k < n; k += nthr) f(k);
-    });
-  for (auto& x : th) x.join();
+  const std::function<void(int)> fn = [&](int k) { f(k); };
+  HostPool::get().run(nthr, n, fn);
 }
 
 int plan_level(claw_ctx* c, int level, Level& L) {
@@ -2430,10 +2507,14 @@ struct Clusterer {
   int64_t nx, ny;
   std::vector<int32_t> own;
   std::vector<int32_t>& sat;  // (ny+1) x (nx+1) prefix counts (maps < 2^31 cells)
+  const int32_t* S = nullptr; // the table count() reads (sat's data, or a table built on the GPU)
   double cutoff;
   int maxd, mind;
   std::vector<int32_t> out;  // (x0, y0, w, h) quadruples
 
+  // a table computed elsewhere (launch_sat on the device, copied back)
+  Clusterer(const int32_t* table, int64_t nx_, int64_t ny_, double c, int mx, int mn)
+      : nx(nx_), ny(ny_), sat(own), S(table), cutoff(c), maxd(mx), mind(mn) {}
   // scratch: a caller-kept buffer for the table (no fresh pages per regrid)
   Clusterer(const uint8_t* f, int64_t nx_, int64_t ny_, double c, int mx, int mn,
             std::vector<int32_t>* scratch = nullptr)
@@ -2464,10 +2545,11 @@ struct Clusterer {
         for (int64_t I = a0; I < a1; ++I) r[I] += q[I];
       }
     });
+    S = sat.data();
   }
   int64_t count(int64_t x0, int64_t y0, int64_t x1, int64_t y1) const {  // [x0,x1) x [y0,y1)
     const int64_t W = nx + 1;
-    return static_cast<int64_t>(sat[y1 * W + x1]) - sat[y0 * W + x1] - sat[y1 * W + x0] + sat[y0 * W + x0];
+    return static_cast<int64_t>(S[y1 * W + x1]) - S[y0 * W + x1] - S[y1 * W + x0] + S[y0 * W + x0];
   }
   void emit(int64_t x0, int64_t y0, int64_t w, int64_t h) {
     out.push_back(static_cast<int32_t>(x0));
@@ -2821,24 +2903,36 @@ int claw_regrid_auto(claw_ctx* ctx, int32_t level, double tol, int32_t buffer, d
   int64_t nflag = 0;
   if (int rc = flag_device(ctx, level, tol, buffer, 2, out, on, &nflag)) return rc;
   lap("flag");
-  if (ctx->h_stage_bytes < static_cast<size_t>(2 * n)) {
+  // the clusterer reads only the flags' summed-area table: built on the
+  // device (launch_sat) and copied back with the nesting mask, instead of
+  // copying the flag map and summing it on the host (4 ms for 2000^2 cells)
+  const size_t satb = static_cast<size_t>((C.nx + 1) * (C.ny + 1)) * sizeof(int32_t);
+  const size_t need = satb + static_cast<size_t>(n);
+  if (ctx->h_stage_bytes < need) {
     if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
     ctx->h_stage = nullptr;
     ctx->h_stage_bytes = 0;
-    CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_stage), static_cast<size_t>(2 * n)));
-    ctx->h_stage_bytes = static_cast<size_t>(2 * n);
+    CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_stage), need));
+    ctx->h_stage_bytes = need;
   }
-  const uint8_t* f = ctx->h_stage;
-  const uint8_t* m = ctx->h_stage + n;
-  CUDA_TRY(cudaMemcpyAsync(ctx->h_stage, out.p, n, cudaMemcpyDeviceToHost, ctx->stream));
-  CUDA_TRY(cudaMemcpyAsync(ctx->h_stage + n, on.p, n, cudaMemcpyDeviceToHost, ctx->stream));
-  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  const int32_t* hsat = reinterpret_cast<const int32_t*>(ctx->h_stage);
+  const uint8_t* m = ctx->h_stage + satb;
+  {
+    DevBuf<int32_t> dsat;
+    if (nflag > 0) {
+      CUDA_TRY(dsat.alloc(static_cast<size_t>((C.nx + 1) * (C.ny + 1))));
+      CUDA_TRY(static_cast<cudaError_t>(claw::launch_sat(out.p, C.nx, C.ny, dsat.p, ctx->stream)));
+      CUDA_TRY(cudaMemcpyAsync(ctx->h_stage, dsat.p, satb, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    CUDA_TRY(cudaMemcpyAsync(ctx->h_stage + satb, on.p, n, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  }
   std::vector<int32_t> boxes;
   if (nflag > 0) {
     if (!(cutoff > 0.0) || cutoff > 1.0 || max_dim < 1 || min_dim < 1 || 2 * min_dim > max_dim)
       return fail(ctx, CLAW_EINVAL, "cluster: cutoff=%g max_dim=%d min_dim=%d", cutoff, max_dim, min_dim);
     if (n >= (1ll << 31)) return fail(ctx, CLAW_EINVAL, "regrid_auto: flag map of %lld cells", (long long)n);
-    Clusterer cl(f, C.nx, C.ny, cutoff, max_dim, min_dim, &ctx->sat_scratch);
+    Clusterer cl(hsat, C.nx, C.ny, cutoff, max_dim, min_dim);
     cl.run();
     // nesting: split each box into row-run rectangles of the nesting mask M
     // (runs identical in consecutive rows merge), drop pieces without flags;

@@ -165,6 +165,8 @@ int launch_flag(const StepParams& p, const int2* orig, int32_t nown, int64_t nx,
 int launch_dilate(const uint8_t* in, uint8_t* tmp, uint8_t* out, const uint8_t* mask, int64_t nx, int64_t ny, int b,
                   unsigned long long* count, void* stream);
 int launch_not(const uint8_t* in, uint8_t* out, int64_t n, void* stream);
+// summed-area table (ny+1) x (nx+1) int32 of a uint8 flag map (clustering)
+int launch_sat(const uint8_t* f, int64_t nx, int64_t ny, int32_t* sat, void* stream);
 // Patch-id map of a level's index space: map[J*nx + I] = owned patch index
 // or -1 (map memset to 0xff first); one CTA per patch paints its rectangle.
 int launch_paint(int32_t* map, int64_t nx, const int2* orig, const DevPatch* patches, int32_t npatch, void* stream);
