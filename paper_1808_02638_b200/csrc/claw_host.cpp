@@ -93,8 +93,8 @@ Nccl g_nccl;
 // patch "can even dominate" with small patches; the paper's pool "allocates a
 // huge chunk of memory at a time and allocates more chunks when needed").
 // Every device buffer of the library comes from here: per device, chunks of
-// >= 256 MiB (growing geometrically up to 2 GiB) from cudaMalloc, carved best-fit (512-byte granules) with free
-// ranges coalesced on release, so regrids and re-set levels of varying sizes
+// >= 1 GiB (growing geometrically up to 2 GiB) from cudaMalloc, carved
+// best-fit (512-byte granules) with free ranges coalesced on release, so regrids and re-set levels of varying sizes
 // reuse memory without calling cudaMalloc.  Releases happen only after the
 // owning context's stream is synchronised (set_level, regrid, destroy), so a
 // range is never reused while a kernel may still touch it.  Wholly free chunks
@@ -103,7 +103,7 @@ Nccl g_nccl;
 // ---------------------------------------------------------------------------
 struct Pool {
   static constexpr size_t kGrain = 512;
-  static constexpr size_t kChunk = size_t{256} << 20;
+  static constexpr size_t kChunk = size_t{1} << 30;  // first chunk (cudaMalloc of a chunk: 15-100 ms)
   struct Dev {
     std::map<char*, size_t> chunks;        // start -> size
     std::map<char*, size_t> free_at;       // free ranges by address
@@ -2559,14 +2559,70 @@ struct Clusterer {
   }
   bool admissible(int64_t k, int64_t n) const { return k >= mind && n - k >= mind; }
 
+  struct Box { int64_t x0, y0, x1, y1; };
+  // Berger-Rigoutsos, depth first with the low part of every cut first (the
+  // oracle's order).  The first cuts are expanded breadth first into an
+  // ordered frontier (a cut box is replaced by its low and high parts, so each
+  // entry's subtree output stays contiguous in the depth-first order) until
+  // it holds enough open boxes; their subtrees are then clustered by host
+  // workers and all outputs concatenated in frontier order: the result is the
+  // sequential one for any thread count.
   void run() {
-    struct Box { int64_t x0, y0, x1, y1; };
-    std::vector<Box> stack{{0, 0, nx, ny}};
+    struct Ent {
+      Box b;
+      bool open;
+      std::vector<int32_t> out;
+    };
     std::vector<int64_t> sig[2];
-    while (!stack.empty()) {
-      Box b = stack.back();
-      stack.pop_back();
-      if (count(b.x0, b.y0, b.x1, b.y1) == 0) continue;
+    const int nthr = host_threads(64 * 64);
+    const size_t want = static_cast<size_t>(4 * nthr);
+    std::vector<Ent> fr;
+    fr.push_back(Ent{Box{0, 0, nx, ny}, true, {}});
+    size_t nopen = 1;
+    std::vector<Box> st;
+    while (nthr > 1 && nopen > 0 && nopen < want) {
+      std::vector<Ent> nxt;
+      nopen = 0;
+      for (Ent& e : fr) {
+        if (!e.open) {
+          nxt.push_back(std::move(e));
+          continue;
+        }
+        st.clear();
+        std::vector<int32_t> o;
+        process(e.b, st, o, sig);
+        if (!o.empty()) nxt.push_back(Ent{e.b, false, std::move(o)});
+        if (st.size() == 2) {  // pushed hi, then lo
+          nxt.push_back(Ent{st[1], true, {}});
+          nxt.push_back(Ent{st[0], true, {}});
+          nopen += 2;
+        }
+      }
+      fr.swap(nxt);
+    }
+    parallel_for(nthr, static_cast<int>(fr.size()), [&](int i) {
+      Ent& e = fr[i];
+      if (!e.open) return;
+      std::vector<Box> stk{e.b};
+      std::vector<int64_t> sg[2];
+      while (!stk.empty()) {
+        Box bx = stk.back();
+        stk.pop_back();
+        process(bx, stk, e.out, sg);
+      }
+    });
+    for (auto& e : fr) out.insert(out.end(), e.out.begin(), e.out.end());
+  }
+  static void emit_to(std::vector<int32_t>& o, int64_t x0, int64_t y0, int64_t w, int64_t h) {
+    o.push_back(static_cast<int32_t>(x0));
+    o.push_back(static_cast<int32_t>(y0));
+    o.push_back(static_cast<int32_t>(w));
+    o.push_back(static_cast<int32_t>(h));
+  }
+  // one popped box: emit it, or push its two parts
+  void process(Box b, std::vector<Box>& stack, std::vector<int32_t>& o, std::vector<int64_t>* sig) const {
+    {
+      if (count(b.x0, b.y0, b.x1, b.y1) == 0) return;
       // shrink: first / last non-empty column and row
       while (count(b.x0, b.y0, b.x0 + 1, b.y1) == 0) ++b.x0;
       while (count(b.x1 - 1, b.y0, b.x1, b.y1) == 0) --b.x1;
@@ -2575,8 +2631,8 @@ struct Clusterer {
       const int64_t w = b.x1 - b.x0, h = b.y1 - b.y0;
       const int64_t nf = count(b.x0, b.y0, b.x1, b.y1);
       if (static_cast<double>(nf) / static_cast<double>(w * h) >= cutoff && w <= maxd && h <= maxd) {
-        emit(b.x0, b.y0, w, h);
-        continue;
+        emit_to(o, b.x0, b.y0, w, h);
+        return;
       }
       sig[0].resize(w);
       sig[1].resize(h);
@@ -2632,8 +2688,8 @@ struct Clusterer {
         cut = len[order[0]] / 2;
       }
       if (dir < 0) {
-        emit(b.x0, b.y0, w, h);
-        continue;
+        emit_to(o, b.x0, b.y0, w, h);
+        return;
       }
       Box lo = b, hi = b;
       if (dir == 0) lo.x1 = hi.x0 = b.x0 + cut;
@@ -2927,6 +2983,7 @@ int claw_regrid_auto(claw_ctx* ctx, int32_t level, double tol, int32_t buffer, d
     CUDA_TRY(cudaMemcpyAsync(ctx->h_stage + satb, on.p, n, cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   }
+  lap("sat+d2h");
   std::vector<int32_t> boxes;
   if (nflag > 0) {
     if (!(cutoff > 0.0) || cutoff > 1.0 || max_dim < 1 || min_dim < 1 || 2 * min_dim > max_dim)
@@ -2934,6 +2991,7 @@ int claw_regrid_auto(claw_ctx* ctx, int32_t level, double tol, int32_t buffer, d
     if (n >= (1ll << 31)) return fail(ctx, CLAW_EINVAL, "regrid_auto: flag map of %lld cells", (long long)n);
     Clusterer cl(hsat, C.nx, C.ny, cutoff, max_dim, min_dim);
     cl.run();
+    lap("BR");
     // nesting: split each box into row-run rectangles of the nesting mask M
     // (runs identical in consecutive rows merge), drop pieces without flags;
     // boxes in parallel, pieces concatenated in box order
@@ -2990,7 +3048,7 @@ int claw_regrid_auto(claw_ctx* ctx, int32_t level, double tol, int32_t buffer, d
     for (auto& pc : piece) boxes.insert(boxes.end(), pc.begin(), pc.end());
   }
   const int32_t nb = static_cast<int32_t>(boxes.size() / 4);
-  lap("cluster");
+  lap("nest-split");
   if (nbox_out) *nbox_out = nb;
   const int rc = claw_regrid(ctx, level, nb, boxes.data(), R);
   lap("regrid");

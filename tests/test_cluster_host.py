@@ -63,3 +63,29 @@ def test_cluster_argument_errors():
     for args in [(0.0, 16, 2), (1.5, 16, 2), (0.7, 3, 2), (0.7, 16, 0)]:
         with pytest.raises(binding.ClawError):
             binding.cluster(f, *args)
+
+
+@pytest.mark.parametrize("threads", ["1", "3", "8"])
+def test_cluster_parallel_subtrees_equal_oracle(threads):
+    """Large maps: after the first cuts the clusterer hands the stacked boxes'
+    subtrees to host workers and concatenates their outputs in pop order;
+    the boxes (and their order) must still be the oracle's, for any thread
+    count (CLAW_HOST_THREADS is read once per process, so the thread count is
+    varied in a subprocess)."""
+    import subprocess, sys, os
+    code = (
+        "import numpy as np, oracle\n"
+        "from paper_1808_02638_b200 import binding\n"
+        "Y, X = np.mgrid[0:400, 0:520]\n"
+        "r = np.hypot(X - 260.5, Y - 200.5) / 200\n"
+        "rng = np.random.default_rng(4)\n"
+        "f = ((np.abs(r - 0.5) < 0.06) | (np.abs(r - 0.8) < 0.03) | (rng.uniform(size=r.shape) > 0.999)).astype(np.uint8)\n"
+        "for c, M, m in [(0.7, 40, 4), (0.8, 16, 2), (0.6, 64, 8)]:\n"
+        "    got = binding.cluster(f, c, M, m); want = oracle.cluster(f, c, M, m)\n"
+        "    assert len(got) > 40, len(got)\n"
+        "    assert np.array_equal(got, want)\n"
+        "print('ok')\n")
+    env = dict(os.environ, CLAW_HOST_THREADS=threads)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
