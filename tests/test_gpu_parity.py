@@ -247,6 +247,50 @@ def test_sampled_patches_at_full_c4_size_one_step():
         assert rel_err(q1[pj * 256 + pi], ref) <= TOL, (pi, pj)
 
 
+def test_sampled_patches_at_full_c5_size_one_step():
+    """The default bench workload at full size (C5: 16384^2 cells, 65,536
+    patches of 64^2, 14.5 GB of state) in the bench's launch configuration
+    (grid kernel, 256-row tiles spanning patch rows): after 3 GPU steps, one
+    more step of sampled patches (corners, edges, random interior) is
+    recomputed by the oracle from the GPU's own state on the 3x3 block of
+    patches around each sample; patches are read one by one."""
+    wl = W.c5()
+    d = wl.levels[0].descs
+    g = binding.Claw(W.DOMAIN, W.EXTRAP, 4, 2, device=0)
+    g.set_level(1, d, W.random_ic(d, 55))
+    assert g.level_mode(1) == "grid"
+    dt = wl.dt0()
+    for s in range(3):
+        g.fill_ghost(1, s * dt)
+        g.advance_level(1, dt)
+    rng = np.random.default_rng(5)
+    samples = [tuple(x) for x in rng.integers(0, 256, (10, 2))] + [(0, 0), (255, 255), (0, 255), (255, 0), (3, 128)]
+    blocks = {}
+    for pj, pi in samples:
+        for b in range(max(pj - 1, 0), min(pj + 2, 256)):
+            for a in range(max(pi - 1, 0), min(pi + 2, 256)):
+                blocks[(a, b)] = g.read(1, b * 256 + a).copy()
+    g.fill_ghost(1, 3 * dt)
+    cfl = g.advance_level(1, dt)
+    assert cfl == (dt / float(d["dx"][0])) * 1.0
+    dx = float(d["dx"][0])
+    for pj, pi in samples:
+        js = range(max(pj - 1, 0), min(pj + 2, 256))
+        iis = range(max(pi - 1, 0), min(pi + 2, 256))
+        dom = (-1 + iis[0] * 64 * dx, -1 + (iis[-1] + 1) * 64 * dx,
+               -1 + js[0] * 64 * dx, -1 + (js[-1] + 1) * 64 * dx)
+        boxes = [(a, b) for b in js for a in iis]
+        sub = np.concatenate([W.make_descs([(a - iis[0]) * 64], [(b - js[0]) * 64], 64, 64, dx, dx, dom)
+                              for a, b in boxes])
+        o = oracle.Oracle(dom, W.EXTRAP, 4, 2, nthreads=1)
+        o.set_level(1, sub, np.concatenate([blocks[ab].ravel() for ab in boxes]))
+        o.fill_ghost(1, 0.0)
+        o.advance_level(1, dt)
+        ref = o.read(1, boxes.index((pi, pj)))
+        assert rel_err(g.read(1, pj * 256 + pi), ref) <= TOL, (pi, pj)
+    g.close()
+
+
 def run_hierarchy(wl, n_coarse, q0s, use_gpu, update=False):
     ratios = {L + 1: wl.levels[L + 1].ratio for L in range(len(wl.levels) - 1)}
     nlev = len(wl.levels)
