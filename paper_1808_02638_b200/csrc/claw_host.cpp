@@ -346,7 +346,8 @@ struct Level {
   std::vector<claw::DevUpdate> hu;
   std::vector<claw::DevUpdateRect> hur;  // rectangles of coarse cells inside one fine patch
   DevBuf<claw::DevUpdateRect> dur;
-  int32_t hur_max = 0;                   // largest rectangle (coarse cells)
+  DevBuf<int32_t> dur_chunk;
+  std::vector<int32_t> hur_chunk;        // work chunk -> rectangle (claw::kUpdChunk cells per chunk)
   std::vector<int64_t> hu_src, hu_scs;   // slow entries: R*R (offset, cs) each
   DevBuf<claw::DevUpdate> du;
   DevBuf<int64_t> du_src, du_scs;
@@ -1414,7 +1415,7 @@ int plan_level(claw_ctx* c, int level, Level& L) {
   // interior cells of this level
   L.hu.clear();
   L.hur.clear();
-  L.hur_max = 0;
+  L.hur_chunk.clear();
   L.hu_src.clear();
   L.hu_scs.clear();
   if (C && world == 1) {
@@ -1448,8 +1449,10 @@ int plan_level(claw_ctx* c, int level, Level& L) {
           r.fmx = L.desc[fp].mx;
           r.w = static_cast<int32_t>(x1 - x0);
           r.h = static_cast<int32_t>(y1 - y0);
+          r.chunk0 = static_cast<int32_t>(L.hur_chunk.size());
+          L.hur_chunk.insert(L.hur_chunk.end(), (r.w * r.h + claw::kUpdChunk - 1) / claw::kUpdChunk,
+                             static_cast<int32_t>(L.hur.size()));
           L.hur.push_back(r);
-          L.hur_max = std::max(L.hur_max, r.w * r.h);
         }
       }
       // the rest of the footprint (patches not aligned to the coarse cells):
@@ -1620,6 +1623,7 @@ int alloc_level(claw_ctx* ctx, int level, Level& L) {
   if (int r2 = upload(ctx, L.dinterp, L.hinterp)) return r2;
   if (int r2 = upload(ctx, L.du, L.hu)) return r2;
   if (int r2 = upload(ctx, L.dur, L.hur)) return r2;
+  if (int r2 = upload(ctx, L.dur_chunk, L.hur_chunk)) return r2;
   if (int r2 = upload(ctx, L.dslots, L.hslots)) return r2;
   if (int r2 = upload(ctx, L.dgtile, L.hgtile)) return r2;
   if (int r2 = upload(ctx, L.du_src, L.hu_src)) return r2;
@@ -2242,8 +2246,9 @@ int claw_update_level(claw_ctx* ctx, int32_t level) {
                 F.t_new, level - 1, C.t_new);
   const int64_t n = static_cast<int64_t>(F.hu.size());
   if (!ctx->dry) CUDA_TRY(static_cast<cudaError_t>(claw::launch_update_rects(C.q[C.cur].p, F.q[F.cur].p, F.dur.p,
-                                                              static_cast<int32_t>(F.hur.size()), F.ratio,
-                                                              F.hur_max, ctx->stream)));
+                                                              F.dur_chunk.p,
+                                                              static_cast<int32_t>(F.hur_chunk.size()), F.ratio,
+                                                              ctx->stream)));
   if (!ctx->dry) CUDA_TRY(static_cast<cudaError_t>(claw::launch_update(C.q[C.cur].p, F.q[F.cur].p, F.du.p, n, F.ratio,
                                                         F.du_src.p, F.du_scs.p, ctx->stream)));
   ctx->stats.ghost_launches += (F.hur.empty() ? 0 : 1) + (n > 0 ? 1 : 0);

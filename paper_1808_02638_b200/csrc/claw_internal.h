@@ -128,9 +128,12 @@ struct DevUpdateRect {
   int64_t dst, src;
   int64_t dcs, fcs;
   int32_t cmx, fmx, w, h;
+  int32_t chunk0, pad;  // first work chunk (kUpdChunk coarse cells each) of this rectangle
 };
-int launch_update_rects(double* q_coarse, const double* q_fine, const DevUpdateRect* rects, int32_t n, int R,
-                        int32_t max_cells, void* stream);
+constexpr int kUpdChunk = 128;
+// nchunk work chunks; chunk_rect[k] = the rectangle chunk k belongs to
+int launch_update_rects(double* q_coarse, const double* q_fine, const DevUpdateRect* rects,
+                        const int32_t* chunk_rect, int32_t nchunk, int R, void* stream);
 int launch_update(double* q_coarse, const double* q_fine, const DevUpdate* tab, int64_t n, int R,
                   const int64_t* slow_off, const int64_t* slow_cs, void* stream);
 // Conservation-fix register of a fine level (NEXT-2, R17): coarse
