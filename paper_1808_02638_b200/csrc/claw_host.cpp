@@ -1376,12 +1376,16 @@ int plan_level(claw_ctx* c, int level, Level& L) {
     if (e && (e[0] == '0' || e[0] == '1')) {
       L.lane_tiles = e[0] == '1';
     } else {
-      int64_t n30 = 0, n32 = 0;
+      int64_t n30 = 0, n32 = 0, t30 = 0;
       for (size_t lp = 0; lp < L.owned.size(); ++lp) {
         n30 += (L.hpatch[lp].mx + 29) / 30;
         n32 += (L.hpatch[lp].mx + 31) / 32;
+        t30 += static_cast<int64_t>((L.hpatch[lp].mx + 29) / 30) * ((L.hpatch[lp].my + L.th - 1) / L.th);
       }
-      L.lane_tiles = 5 * n30 <= 6 * n32 ? 1 : 0;
+      // a level whose lane tiles fit in one wave of resident warps (148 SMs x
+      // 16) is latency-bound: the extra warps are free and the march without
+      // side passes is shorter
+      L.lane_tiles = (5 * n30 <= 6 * n32 || t30 <= 148 * 16) ? 1 : 0;
     }
   }
   const int tstrip = L.lane_tiles ? 30 : 32;
