@@ -1279,13 +1279,15 @@ int plan_level(claw_ctx* c, int level, Level& L) {
   for (size_t lp = 1; lp < L.hpatch.size(); ++lp)
     if (L.hpatch[lp].c != L.hpatch[0].c || L.hpatch[lp].Z != L.hpatch[0].Z) L.uniform = false;
   // rows per tile: the configured value, or (auto) the largest power of two
-  // <= 64 that still gives ~one tile per resident warp of the GPU (148 SMs x
-  // 16 warps); small, latency-bound levels get short tiles (>= 8) so the
-  // serial row march of each warp stays short
+  // <= 64 that still gives ~half a tile per resident warp of the GPU (148 SMs
+  // x 16 warps); small, latency-bound levels get short tiles (>= 8) so the
+  // serial row march of each warp stays short (measured: C3's level 3 runs
+  // 2.5% faster with 32-row tiles at 0.7 tiles per warp than with 16-row
+  // ones, C1/C2 fastest at 8; profiles/r01_tile_rows_c123.txt)
   if (c->cfg.tile_rows > 0) {
     L.th = c->tile_rows;
   } else {
-    const int64_t want = 148 * 16;
+    const int64_t want = 148 * 8;
     int th = 64;
     while (th > 8 && L.cells_owned / (32ll * th) < want) th /= 2;
     L.th = th;
