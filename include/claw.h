@@ -289,8 +289,9 @@ int claw_debug_halo_send(const claw_ctx* ctx, int32_t level, int32_t peer,
                          int64_t k, int32_t* patch, int32_t* i, int32_t* j);
 
 /* The process-wide device memory pool every context allocates from (the
- * paper's GPU memory pool): per device, chunks of >= 256 MiB from
- * cudaMalloc carved best-fit with coalescing frees.  hits = requests served
+ * paper's GPU memory pool): per device, chunks from cudaMalloc (the
+ * first 1 GiB, each new one at least the size of all chunks so far, up to
+ * 2 GiB, or the request if larger) carved best-fit with coalescing frees.  hits = requests served
  * from free ranges, misses = requests that needed a new chunk, cached_bytes =
  * free bytes held.  Wholly free chunks beyond CLAW_POOL_LIMIT_MB (environment,
  * default 16384) of free memory are returned to the driver; claw_pool_trim
