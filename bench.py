@@ -307,14 +307,19 @@ def main():
     from paper_1808_02638_b200 import binding
 
     host_x = args.exchange == "host" and world > 1
-    device = local_rank % max(1, torch.cuda.device_count()) if host_x else local_rank
+    # TEST MODE: CLAW_NCCL_LIB points libclaw at a stand-in NCCL that runs
+    # between processes sharing one GPU (tests/nccl_shim); torch's plumbing
+    # then uses gloo, since real NCCL refuses two ranks on one GPU
+    shim_x = world > 1 and not host_x and bool(os.environ.get("CLAW_NCCL_LIB"))
+    test_x = host_x or shim_x
+    device = local_rank % max(1, torch.cuda.device_count()) if test_x else local_rank
     torch.cuda.set_device(device)
     if world > 1:
-        if host_x:
+        if test_x:
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    red_dev = "cpu" if host_x else "cuda"
+    red_dev = "cpu" if test_x else "cuda"
     wl = workload(args.config)
     dyn = bool(wl.extra.get("ratios"))
     rat = hierarchy_ratios(wl)
@@ -547,6 +552,9 @@ def main():
     if rank == 0:
         if host_x:
             line_note = "TEST MODE --exchange host (halos through host memory): not a benchmark number"
+        if shim_x:
+            line_note = ("TEST MODE CLAW_NCCL_LIB (libclaw's NCCL path through a stand-in NCCL between processes "
+                         "on one GPU): not a benchmark number")
         line = {"metric": "fp64 cell-updates/s", "value": value, "unit": "cell-updates/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -570,7 +578,7 @@ def main():
                 "per_gpu_value": value / world}
         if cpu is not None:
             line["cpu_baseline"] = cpu
-        if host_x:
+        if test_x:
             line["test_mode"] = line_note
         print(json.dumps(line), flush=True)
     g.close()

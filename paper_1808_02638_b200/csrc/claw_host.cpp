@@ -59,12 +59,21 @@ struct Nccl {
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   bool load(std::string& err) {
     if (h) return true;
+    // CLAW_NCCL_LIB: an explicit library (tests load a stand-in that runs
+    // the same calls between processes sharing one GPU, which NCCL refuses)
+    if (const char* lib = std::getenv("CLAW_NCCL_LIB")) {
+      h = dlopen(lib, RTLD_NOW | RTLD_LOCAL);
+      if (!h) {
+        err = std::string("CLAW_NCCL_LIB=") + lib + " could not be loaded";
+        return false;
+      }
+    }
     // prefer the NCCL already in the process (torch's), else load one locally
     // so it cannot interpose on another library's NCCL symbols
     const char* names[] = {"libnccl.so.2", "libnccl.so"};
     for (const char* n : names) {
-      h = dlopen(n, RTLD_NOW | RTLD_NOLOAD);
       if (h) break;
+      h = dlopen(n, RTLD_NOW | RTLD_NOLOAD);
     }
     for (const char* n : names) {
       if (h) break;

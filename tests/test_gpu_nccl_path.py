@@ -1,0 +1,100 @@
+"""The library's NCCL code path with several PROCESSES on one GPU.
+
+Real NCCL refuses two ranks on one GPU ("Duplicate GPU detected",
+profiles/r01_nccl_dup_probe.txt), so libclaw is pointed (CLAW_NCCL_LIB) at a
+test stand-in (tests/nccl_shim/ncclshim.c) that implements the calls libclaw
+makes -- unique id, communicator init/destroy, grouped send/recv, float64 max
+all-reduce -- between processes through a memory-mapped file with synchronous
+device<->host copies.  Everything else is the production multi-rank path:
+claw_create with world > 1 and the NCCL exchange, the partition, the pack
+kernel on the comm stream, receives straight into the frame, the event that
+gates the edge tiles after the interior tiles, and the CFL all-reduce inside
+claw_advance_level.  Each rank's owned patches after several steps must be
+bitwise equal to a one-rank run, and every rank must return the global CFL."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from paper_1808_02638_b200 import binding, workloads as W
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SHIM_SRC = os.path.join(ROOT, "tests", "nccl_shim", "ncclshim.c")
+
+WORKER = r'''
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_1808_02638_b200 import binding, workloads as W
+rank, world, idhex, name, bcs, out = int(sys.argv[2]), int(sys.argv[3]), sys.argv[4], sys.argv[5], sys.argv[6], sys.argv[7]
+bc = tuple(int(x) for x in bcs.split(","))
+d = W.c5(patches_per_side=6, mx=32).levels[0].descs if name == "uniform" else W.ragged_level(6, 90, 70, 30)
+q0 = W.random_ic(d, 77)
+offs = W.level_offsets(d)
+owners = binding.partition(d, world)
+g = binding.Claw(W.DOMAIN, bc, 4, 2, device=0, rank=rank, world=world, nccl_id=bytes.fromhex(idhex))
+g.set_level(1, d, np.concatenate([q0[offs[p]:offs[p + 1]] for p in range(len(d)) if owners[p] == rank]))
+dt = 0.9 * float(d["dx"][0])
+cfl = []
+for n in range(5):
+    g.fill_ghost(1, n * dt)
+    cfl.append(g.advance_level(1, dt))
+np.save(out, g.read_level(1))
+np.save(out + ".cfl.npy", np.array(cfl))
+print("mode", g.level_mode(1))
+g.close()
+'''
+
+
+@pytest.fixture(scope="module")
+def shim(tmp_path_factory):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    out = str(tmp_path_factory.mktemp("shim") / "libncclshim.so")
+    subprocess.run(["gcc", "-O2", "-shared", "-fPIC", "-o", out, SHIM_SRC, "-ldl"], check=True)
+    return out
+
+
+@pytest.mark.parametrize("world,name,bc", [(2, "uniform", W.EXTRAP), (3, "uniform", W.PERIODIC),
+                                           (2, "ragged", W.PERIODIC), (4, "ragged", (1, 1, 2, 2))])
+def test_nccl_path_processes_bitwise_equal_single_rank(shim, tmp_path, world, name, bc):
+    env = dict(os.environ, CLAW_NCCL_LIB=shim)
+    # the unique id comes from the same library call rank 0 would make
+    gen = subprocess.run([sys.executable, "-c",
+                          "import sys; sys.path.insert(0, sys.argv[1]); "
+                          "from paper_1808_02638_b200 import binding; print(binding.nccl_unique_id().hex())", ROOT],
+                         env=env, capture_output=True, text=True, check=True)
+    idhex = gen.stdout.strip().splitlines()[-1]
+    script = tmp_path / "worker.py"
+    script.write_text(WORKER)
+    bcs = ",".join(str(x) for x in bc)
+    procs = [subprocess.Popen([sys.executable, str(script), ROOT, str(r), str(world), idhex, name, bcs,
+                               str(tmp_path / f"rank{r}.npy")], env=env, stdout=subprocess.PIPE,
+                              stderr=subprocess.PIPE, text=True) for r in range(world)]
+    outs = [p.communicate(timeout=600) for p in procs]
+    for p, (so, se) in zip(procs, outs):
+        assert p.returncode == 0, se[-3000:]
+    modes = {so.strip().splitlines()[-1] for so, _ in outs}
+    assert modes == {"mode grid" if name == "uniform" else "mode generic"}, modes
+    # the one-rank reference
+    d = W.c5(patches_per_side=6, mx=32).levels[0].descs if name == "uniform" else W.ragged_level(6, 90, 70, 30)
+    q0 = W.random_ic(d, 77)
+    offs = W.level_offsets(d)
+    owners = binding.partition(d, world)
+    ref = binding.Claw(W.DOMAIN, bc, 4, 2, device=0)
+    ref.set_level(1, d, q0)
+    dt = 0.9 * float(d["dx"][0])
+    cfl = []
+    for n in range(5):
+        ref.fill_ghost(1, n * dt)
+        cfl.append(ref.advance_level(1, dt))
+    full = ref.read_level(1)
+    ref.close()
+    for r in range(world):
+        mine = np.concatenate([full[offs[p]:offs[p + 1]] for p in range(len(d)) if owners[p] == r])
+        assert np.array_equal(np.load(tmp_path / f"rank{r}.npy"), mine), r
+        assert np.load(tmp_path / f"rank{r}.npy.cfl.npy").tolist() == cfl
