@@ -146,3 +146,24 @@ def test_partition_ragged_morton_balanced(world):
     cells = np.bincount(own2, weights=d2["mx"] * d2["my"], minlength=world)
     assert cells.max() <= cells.sum() / world + (d2["mx"] * d2["my"]).max()
     assert np.array_equal(own2, binding.partition(d2, world))
+
+
+def test_nccl_stand_in_loads_through_claw_nccl_lib(tmp_path):
+    """CPU: the test-only stand-in NCCL (tests/nccl_shim) compiles, exports the
+    nine calls libclaw uses, and libclaw loads it through CLAW_NCCL_LIB (the
+    unique id is the stand-in's); the GPU test runs the multi-process path."""
+    import os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    so = str(tmp_path / "libncclshim.so")
+    subprocess.run(["gcc", "-O2", "-shared", "-fPIC", "-o", so, os.path.join(root, "tests", "nccl_shim", "ncclshim.c"),
+                    "-ldl"], check=True)
+    syms = subprocess.run(["nm", "-D", so], capture_output=True, text=True, check=True).stdout
+    for f in ["GetUniqueId", "CommInitRank", "CommDestroy", "AllReduce", "Send", "Recv", "GroupStart", "GroupEnd",
+              "GetErrorString"]:
+        assert f" T nccl{f}" in syms, f
+    code = ("import sys; sys.path.insert(0, sys.argv[1]); from paper_1808_02638_b200 import binding; "
+            "print(binding.nccl_unique_id().split(b'\\0')[0].decode())")
+    r = subprocess.run([sys.executable, "-c", code, root], env=dict(os.environ, CLAW_NCCL_LIB=so),
+                       capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.strip().splitlines()[-1].startswith("/tmp/claw_ncclshim_")
