@@ -2998,12 +2998,16 @@ int claw_regrid_auto(claw_ctx* ctx, int32_t level, double tol, int32_t buffer, d
     if (nflag > 0) {
       CUDA_TRY(dsat.alloc(static_cast<size_t>((C.nx + 1) * (C.ny + 1))));
       CUDA_TRY(static_cast<cudaError_t>(claw::launch_sat(out.p, C.nx, C.ny, dsat.p, ctx->stream)));
+      if (lap.on) {
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        lap("sat");
+      }
       CUDA_TRY(cudaMemcpyAsync(ctx->h_stage, dsat.p, satb, cudaMemcpyDeviceToHost, ctx->stream));
     }
     CUDA_TRY(cudaMemcpyAsync(ctx->h_stage + satb, on.p, n, cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   }
-  lap("sat+d2h");
+  lap("d2h");
   std::vector<int32_t> boxes;
   if (nflag > 0) {
     if (!(cutoff > 0.0) || cutoff > 1.0 || max_dim < 1 || min_dim < 1 || 2 * min_dim > max_dim)
