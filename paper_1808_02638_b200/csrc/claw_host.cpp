@@ -9,6 +9,7 @@
 // a level max P:417-420.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <unistd.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -795,7 +796,16 @@ struct PhaseTrace {
 class HostPool {
  public:
   static HostPool& get() {
-    static HostPool* p = new HostPool();  // never destroyed (workers detached at exit)
+    // never destroyed (workers detached at exit); a forked child has none of
+    // the parent's workers, so it starts its own pool
+    static HostPool* p = nullptr;
+    static pid_t owner = 0;
+    static std::mutex mk;
+    std::lock_guard<std::mutex> g(mk);
+    if (!p || owner != getpid()) {
+      p = new HostPool();
+      owner = getpid();
+    }
     return *p;
   }
   static bool& in_worker() {

@@ -89,3 +89,21 @@ def test_cluster_parallel_subtrees_equal_oracle(threads):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_host_worker_pool_after_fork():
+    """The planner's persistent host workers do not survive fork(): a child
+    process starts its own pool and clusters like the parent."""
+    import os
+    import sys
+    if not hasattr(os, "fork") or sys.platform != "linux":
+        pytest.skip("fork")
+    Y, X = np.mgrid[0:300, 0:300]
+    f = (np.abs(np.hypot(X - 150, Y - 150) / 150 - 0.5) < 0.05).astype(np.uint8)
+    a = binding.cluster(f, 0.7, 40, 4)
+    pid = os.fork()
+    if pid == 0:
+        ok = np.array_equal(binding.cluster(f, 0.7, 40, 4), a)
+        os._exit(0 if ok else 3)
+    _, st = os.waitpid(pid, 0)
+    assert os.WEXITSTATUS(st) == 0 and len(a) > 4
