@@ -327,6 +327,8 @@ struct Level {
   std::vector<std::vector<int64_t>> send_dbg;  // patch<<32 | j<<16 | i
   std::vector<int64_t> nrecv, recv_frame_off;
   int64_t frame_elems = 0;
+  int nslice = 1;                // frame slices (the R substeps of a fine level inside a coarse step)
+  int fsel = 0;                  // slice the next step reads
   int64_t coarse_frame_off = 0, ncoarse = 0;
   // device
   DevBuf<double> q[2];
@@ -1641,7 +1643,11 @@ int alloc_level(claw_ctx* ctx, int level, Level& L) {
       return fail(ctx, CLAW_ENOMEM, "level %d: cannot allocate %lld bytes of device pool", level, bytes);
     }
   }
-  CUDA_TRY(L.frame.alloc(std::max<int64_t>(L.frame_elems, 1)));
+  // a fine level's coarse ghost values for all R substeps of a coarse step
+  // are interpolated by one launch into R slices (claw_advance_hierarchy)
+  L.nslice = (level > 1 && L.ncoarse > 0 && ctx->cfg.world == 1 && L.ratio >= 2 &&
+              L.ratio <= claw::kMaxInterpAlphas) ? L.ratio : 1;
+  CUDA_TRY(L.frame.alloc(std::max<int64_t>(L.frame_elems, 1) * L.nslice));
   if (int r2 = upload(ctx, L.dpatch, L.hpatch)) return r2;
   if (int r2 = upload(ctx, L.drect, L.hrect)) return r2;
   if (int r2 = upload(ctx, L.dtile, L.htile)) return r2;
@@ -1911,37 +1917,52 @@ int claw_set_level(claw_ctx* ctx, int32_t level, int32_t npatch, const claw_patc
   return CLAW_OK;
 }
 
+namespace {
+// Coarse-to-fine interpolation (R10) of level `level`'s frame cells at
+// the times ts[0..nts) into frame slices 0..nts-1, one launch; slice 0 is
+// what the next step reads.
+int interp_frames(claw_ctx* ctx, int32_t level, const double* ts, int nts) {
+  Level& L = ctx->lev[level];
+  L.fsel = 0;
+  if (!(level > 1 && L.ncoarse > 0)) return CLAW_OK;
+  const Level& C = ctx->lev[level - 1];
+  const double span = C.t_new - C.t_old;
+  const double tol = 1e-12 * std::max(1.0, std::fabs(C.t_new));
+  double alpha[claw::kMaxInterpAlphas];
+  for (int k = 0; k < nts; ++k) {
+    const double t = ts[k];
+    if (t < C.t_old - tol || t > C.t_new + tol)
+      return fail(ctx, CLAW_ESTATE, "fill_ghost(level %d, t=%.17g): outside level %d's [%.17g, %.17g]", level, t,
+                  level - 1, C.t_old, C.t_new);
+    alpha[k] = (span > 0) ? (t - C.t_old) / span : 0.0;
+  }
+  // inside claw_advance_hierarchy's graph path alpha goes through device
+  // memory, so a replayed graph interpolates at this step's times
+  const double* adev = nullptr;
+  if (ctx->in_hier) {
+    if (ctx->alpha_n + nts > kMaxAlpha) return fail(ctx, CLAW_EINVAL, "more than %d interpolations per coarse step", kMaxAlpha);
+    for (int k = 0; k < nts; ++k) ctx->h_alpha[ctx->alpha_n + k] = alpha[k];
+    adev = ctx->d_alpha.p + ctx->alpha_n;
+    ctx->alpha_n += nts;
+  }
+  // C.q[C.cur] holds t_new, the other buffer t_old; DevInterp.dst is a frame
+  // offset inside a slice, components are frame_cs apart
+  if (!ctx->dry)
+    CUDA_TRY(static_cast<cudaError_t>(claw::launch_interp(C.q[1 - C.cur].p, C.q[C.cur].p, alpha, nts, adev,
+                                                          L.dinterp.p, L.ncoarse, L.frame.p, L.frame_cs,
+                                                          L.frame_elems, ctx->stream)));
+  ctx->stats.ghost_launches++;
+  return CLAW_OK;
+}
+}  // namespace
+
 int claw_fill_ghost(claw_ctx* ctx, int32_t level, double t) {
   if (int rc = check_ctx(ctx)) return rc;
   if (int rc = check_level(ctx, level)) return rc;
   if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
   Level& L = ctx->lev[level];
   record(ctx, ctx->ev_ghost, true);
-  if (level > 1 && L.ncoarse > 0) {
-    const Level& C = ctx->lev[level - 1];
-    const double span = C.t_new - C.t_old;
-    const double tol = 1e-12 * std::max(1.0, std::fabs(C.t_new));
-    if (t < C.t_old - tol || t > C.t_new + tol)
-      return fail(ctx, CLAW_ESTATE, "fill_ghost(level %d, t=%.17g): outside level %d's [%.17g, %.17g]", level, t,
-                  level - 1, C.t_old, C.t_new);
-    const double alpha = (span > 0) ? (t - C.t_old) / span : 0.0;
-    // inside claw_advance_hierarchy alpha goes through device memory, so a
-    // replayed graph interpolates at this step's time
-    const double* adev = nullptr;
-    if (ctx->in_hier) {
-      if (ctx->alpha_n >= kMaxAlpha) return fail(ctx, CLAW_EINVAL, "more than %d interpolations per coarse step", kMaxAlpha);
-      ctx->h_alpha[ctx->alpha_n] = alpha;
-      adev = ctx->d_alpha.p + ctx->alpha_n;
-      ctx->alpha_n++;
-    }
-    // C.q[C.cur] holds t_new, the other buffer t_old
-    // DevInterp.dst is an absolute frame offset; components are ncoarse apart
-    if (!ctx->dry)
-      CUDA_TRY(static_cast<cudaError_t>(claw::launch_interp(C.q[1 - C.cur].p, C.q[C.cur].p, alpha, adev,
-                                                            L.dinterp.p, L.ncoarse, L.frame.p, L.frame_cs,
-                                                            ctx->stream)));
-    ctx->stats.ghost_launches++;
-  }
+  if (int rc = interp_frames(ctx, level, &t, 1)) return rc;
   if (ctx->cfg.world > 1 && ctx->cfg.exchange == 0) {
     // halo on the comm stream: starts when q^n is complete on the main
     // stream; claw_advance_level runs the interior tiles meanwhile and waits
@@ -1996,7 +2017,7 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
   claw::StepParams P{};
   P.q = L.q[L.cur].p;
   P.qn = L.q[1 - L.cur].p;
-  P.frame = L.frame.p;
+  P.frame = L.frame.p + static_cast<int64_t>(L.fsel) * L.frame_elems;
   P.patches = L.dpatch.p;
   P.rects = L.drect.p;
   P.tiles = L.dtile.p;
@@ -2219,7 +2240,7 @@ int claw_read_padded(claw_ctx* ctx, int32_t level, int32_t patch, double* q_out)
   const int64_t n = 3ll * (L.hpatch[lp].mx + 4) * (L.hpatch[lp].my + 4);
   DevBuf<double> tmp;
   CUDA_TRY(tmp.alloc(n));
-  CUDA_TRY(static_cast<cudaError_t>(claw::launch_gather_padded(L.q[L.cur].p, L.frame.p, L.dpatch.p, L.drect.p, lp,
+  CUDA_TRY(static_cast<cudaError_t>(claw::launch_gather_padded(L.q[L.cur].p, L.frame.p + static_cast<int64_t>(L.fsel) * L.frame_elems, L.dpatch.p, L.drect.p, lp,
                                                                tmp.p, ctx->stream)));
   CUDA_TRY(cudaMemcpyAsync(q_out, tmp.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
@@ -2316,14 +2337,33 @@ int claw_reflux_registers(claw_ctx* ctx, int32_t level, int64_t* n, int32_t* edg
 
 // Recursive subcycled advance without host synchronisation; every
 // step kernel also folds its Courant number into the coarse-step slot.
-static int advance_rec(claw_ctx* ctx, int level, double t, double dt, int nlev, int flags) {
-  if (int rc = claw_fill_ghost(ctx, level, t)) return rc;
+// sub_ts / sub_k / sub_n: this level is substep sub_k of sub_n at the times
+// sub_ts (set by the parent); a level with that many frame slices gets the
+// coarse ghost values of all its substeps from one interpolation launch at
+// substep 0, and later substeps only select their slice
+static int advance_rec(claw_ctx* ctx, int level, double t, double dt, int nlev, int flags,
+                       const double* sub_ts = nullptr, int sub_k = 0, int sub_n = 1) {
+  Level& L = ctx->lev[level];
+  if (sub_ts && sub_n > 1 && L.nslice >= sub_n && L.ncoarse > 0) {
+    if (sub_k == 0) {
+      if (int rc = check_ctx(ctx)) return rc;
+      record(ctx, ctx->ev_ghost, true);
+      if (int rc = interp_frames(ctx, level, sub_ts, sub_n)) return rc;
+      record(ctx, ctx->ev_ghost, false);
+    }
+    L.fsel = sub_k;
+  } else {
+    if (int rc = claw_fill_ghost(ctx, level, t)) return rc;
+  }
   if (int rc = claw_advance_level_async(ctx, level, dt)) return rc;
   if (level < nlev) {
     const int R = ctx->lev[level + 1].ratio;
     const double dtf = dt / R;
+    double ts[claw::kMaxInterpAlphas];
+    const bool multi = R <= claw::kMaxInterpAlphas;
+    for (int k = 0; k < R && multi; ++k) ts[k] = t + k * dtf;
     for (int k = 0; k < R; ++k)
-      if (int rc = advance_rec(ctx, level + 1, t + k * dtf, dtf, nlev, flags)) return rc;
+      if (int rc = advance_rec(ctx, level + 1, t + k * dtf, dtf, nlev, flags, multi ? ts : nullptr, k, R)) return rc;
     if (flags & CLAW_HIER_UPDATE)
       if (int rc = claw_update_level(ctx, level + 1)) return rc;
   }
@@ -2797,7 +2837,7 @@ int flag_device(claw_ctx* ctx, int level, double tol, int buffer, int clip, DevB
   CUDA_TRY(cudaMemsetAsync(cnt.p, 0, 8, ctx->stream));
   claw::StepParams P{};
   P.q = L.q[L.cur].p;
-  P.frame = L.frame.p;
+  P.frame = L.frame.p + static_cast<int64_t>(L.fsel) * L.frame_elems;
   P.patches = L.dpatch.p;
   P.rects = L.drect.p;
   CUDA_TRY(static_cast<cudaError_t>(claw::launch_flag(P, orig.p, static_cast<int32_t>(L.owned.size()), L.nx, tol,

@@ -105,8 +105,14 @@ struct StepParams {
 // Launchers (claw_kernels.cu).  All return cudaError_t as int.
 int launch_step(const StepParams& p, void* stream);
 // alpha_dev (may be null): read alpha from device memory instead (graph replay)
-int launch_interp(const double* q_old, const double* q_new, double alpha, const double* alpha_dev,
-                  const DevInterp* spec, int64_t n, double* frame, int64_t fcs, void* stream);
+// nal time levels (alphas, or alpha_dev[k] when non-null) into frame slices
+// k * slice apart (the R substeps of a fine level at once; nal = 1 otherwise)
+constexpr int kMaxInterpAlphas = 8;
+struct InterpAlphas {
+  double a[kMaxInterpAlphas];
+};
+int launch_interp(const double* q_old, const double* q_new, const double* alphas, int nal, const double* alpha_dev,
+                  const DevInterp* spec, int64_t n, double* frame, int64_t fcs, int64_t slice, void* stream);
 int launch_pack(const double* q, const int64_t* off, const int64_t* cs, int64_t n,
                 double* out, void* stream);
 int launch_gather_padded(const double* q, const double* frame, const DevPatch* patches,
