@@ -1412,12 +1412,17 @@ int plan_level(claw_ctx* c, int level, Level& L) {
     }
   }
   const int tstrip = L.lane_tiles ? 30 : 32;
+  // halo-lane tiles take at most 32 rows: measured 1.3% faster per coarse
+  // step on the paper workload's fine levels than 64 (more, shorter marches
+  // over its ragged patches; profiles/r01_lane_kernel.txt); an equal split of
+  // a patch's rows (50 + 50 instead of 64 + 36) measured no better
+  const int gth = (L.lane_tiles && c->cfg.tile_rows == 0) ? std::min(L.th, 32) : L.th;
   L.htile.clear();
   for (size_t lp = 0; lp < L.owned.size(); ++lp) {
     const int mx = L.hpatch[lp].mx, my = L.hpatch[lp].my;
-    for (int j0 = 0; j0 < my; j0 += L.th)
+    for (int j0 = 0; j0 < my; j0 += gth)
       for (int i0 = 0; i0 < mx; i0 += tstrip) {
-        const int tw = std::min(tstrip, mx - i0), th = std::min(L.th, my - j0);
+        const int tw = std::min(tstrip, mx - i0), th = std::min(gth, my - j0);
         L.htile.push_back(make_int4(static_cast<int>(lp), i0, j0, tw | (th << 16)));
       }
   }
