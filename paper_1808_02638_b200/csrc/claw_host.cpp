@@ -1452,7 +1452,16 @@ int plan_level(claw_ctx* c, int level, Level& L) {
   L.hu_scs.clear();
   if (C && world == 1) {
     const int R = L.ratio;
-    for (int fp = 0; fp < np; ++fp) {
+    // per fine patch in parallel (host workers), concatenated in patch order:
+    // the tables are the sequential ones
+    struct UpdPart {
+      std::vector<claw::DevUpdateRect> rects;
+      std::vector<claw::DevUpdate> cells;
+      std::vector<int64_t> so, sc;  // slow entries (src = index into this part's R*R groups)
+    };
+    std::vector<UpdPart> parts(np);
+    parallel_for(host_threads(np), np, [&](int fp) {
+      UpdPart& P = parts[fp];
       const int64_t ic0 = L.i0[fp] / R, ic1 = (L.i0[fp] + L.desc[fp].mx - 1) / R;
       const int64_t jc0 = L.j0[fp] / R, jc1 = (L.j0[fp] + L.desc[fp].my - 1) / R;
       const int64_t fi0 = L.i0[fp], fi1 = L.i0[fp] + L.desc[fp].mx, fj0 = L.j0[fp], fj1 = L.j0[fp] + L.desc[fp].my;
@@ -1481,10 +1490,7 @@ int plan_level(claw_ctx* c, int level, Level& L) {
           r.fmx = L.desc[fp].mx;
           r.w = static_cast<int32_t>(x1 - x0);
           r.h = static_cast<int32_t>(y1 - y0);
-          r.chunk0 = static_cast<int32_t>(L.hur_chunk.size());
-          L.hur_chunk.insert(L.hur_chunk.end(), (r.w * r.h + claw::kUpdChunk - 1) / claw::kUpdChunk,
-                             static_cast<int32_t>(L.hur.size()));
-          L.hur.push_back(r);
+          P.rects.push_back(r);
         }
       }
       // the rest of the footprint (patches not aligned to the coarse cells):
@@ -1527,13 +1533,29 @@ int plan_level(claw_ctx* c, int level, Level& L) {
             u.fmx = L.desc[fp].mx;
             u.slow = 0;
           } else {
-            u.src = static_cast<int64_t>(L.hu_src.size()) / (R * R);
+            u.src = static_cast<int64_t>(P.so.size()) / (R * R);
             u.slow = 1;
-            L.hu_src.insert(L.hu_src.end(), so.begin(), so.end());
-            L.hu_scs.insert(L.hu_scs.end(), sc.begin(), sc.end());
+            P.so.insert(P.so.end(), so.begin(), so.end());
+            P.sc.insert(P.sc.end(), sc.begin(), sc.end());
           }
-          L.hu.push_back(u);
+          P.cells.push_back(u);
         }
+    });
+    for (int fp = 0; fp < np; ++fp) {
+      UpdPart& P = parts[fp];
+      for (claw::DevUpdateRect r : P.rects) {
+        r.chunk0 = static_cast<int32_t>(L.hur_chunk.size());
+        L.hur_chunk.insert(L.hur_chunk.end(), (r.w * r.h + claw::kUpdChunk - 1) / claw::kUpdChunk,
+                           static_cast<int32_t>(L.hur.size()));
+        L.hur.push_back(r);
+      }
+      const int64_t base = static_cast<int64_t>(L.hu_src.size()) / (R * R);
+      for (claw::DevUpdate u : P.cells) {
+        if (u.slow) u.src += base;
+        L.hu.push_back(u);
+      }
+      L.hu_src.insert(L.hu_src.end(), P.so.begin(), P.so.end());
+      L.hu_scs.insert(L.hu_scs.end(), P.sc.begin(), P.sc.end());
     }
   }
   lap("update");
