@@ -129,3 +129,85 @@ def test_coarse_interp_is_conservative_r2():
     for k in range(2):                  # coarse rows 3, 4
         blk = qp[:, 2 + 2 * k:4 + 2 * k, 0:2]
         assert np.allclose(blk.mean(axis=(1, 2)), C[:, 3 + k, 2], atol=1e-15)
+
+
+# ---------------------------------------------------------------------------
+# Pin of the coarse-interpolation slope (reading R10 of P:131, "interpolated
+# from underlying coarse grid patches"): minmod of the two one-sided coarse
+# differences, 0 at a coarse local extremum.  The fields are separable, so each
+# slope is read off the coarse sequences by hand (below); every value is dyadic,
+# so the comparisons are exact.  An unlimited central slope, a `max` in place of
+# the `min`, a dropped extremum test or an x/y (or component) mix-up changes at
+# least one hand-derived number here.
+#
+#   a(Ic) = [0, 0, 1, 3, 4, 4.5, 8, 8]     (x sequence, Ic = 0..7)
+#   b(Jc) = [0, 0, 2, 2.5, 2, 1, 0, 0]     (y sequence, Jc = 0..7)
+#   p = a(Ic) + b(Jc),  u = a(Ic),  v = b(Jc)
+#
+# Hand-derived minmod slopes (one-sided differences d- = f(k)-f(k-1), d+ = f(k+1)-f(k)):
+#   x, Ic=2: d-=1,   d+=2     -> +1      (central would be 1.5, max 2)
+#   x, Ic=3: d-=2,   d+=1     -> +1
+#   x, Ic=4: d-=1,   d+=0.5   -> +0.5
+#   x, Ic=5: d-=0.5, d+=3.5   -> +0.5    (central 2, max 3.5)
+#   y, Jc=2: d-=2,   d+=0.5   -> +0.5
+#   y, Jc=3: d-=0.5, d+=-0.5  -> 0       (local maximum; central would be 0)
+#   y, Jc=4: d-=-0.5, d+=-1   -> -0.5    (central -0.75, max -1)
+#   y, Jc=5: d-=-1,  d+=-1    -> -1
+SLOPE_X = {2: 1.0, 3: 1.0, 4: 0.5, 5: 0.5}
+SLOPE_Y = {2: 0.5, 3: 0.0, 4: -0.5, 5: -1.0}
+A_SEQ = [0, 0, 1, 3, 4, 4.5, 8, 8]
+B_SEQ = [0, 0, 2, 2.5, 2, 1, 0, 0]
+
+
+def _minmod_field():
+    Jc, Ic = np.mgrid[0:8, 0:8]
+    a = np.asarray(A_SEQ, float)[Ic]
+    b = np.asarray(B_SEQ, float)[Jc]
+    return np.stack([a + b, a, b])
+
+
+def _hand_value(I, J, R=2):
+    """Fine value at fine global (I, J), R = 2: offsets xi, eta = -1/4 or +1/4."""
+    Ic, Jc = I // R, J // R
+    xi = -0.25 if I % R == 0 else 0.25
+    eta = -0.25 if J % R == 0 else 0.25
+    sx, sy = SLOPE_X[Ic], SLOPE_Y[Jc]
+    a, b = A_SEQ[Ic], B_SEQ[Jc]
+    return np.array([a + b + sx * xi + sy * eta, a + sx * xi, b + sy * eta])
+
+
+def test_coarse_interp_minmod_slope_hand_values():
+    """Ghost frame of a fine patch over coarse cells (3..4)^2, R = 2 (fine
+    cells 6..9): every ghost cell equals the hand-derived minmod value."""
+    o, cd, fd, dxc, dxf = two_level(2, [(6, 6, 4, 4)])
+    o.set_level(1, cd, _minmod_field().ravel())
+    o.set_level(2, fd, np.zeros(3 * 16))
+    o.fill_ghost(2, 0.0)
+    qp = o.read_padded(2, 0)
+    # spot values written out in full
+    assert list(qp[:, 2, 0]) == [3.25, 0.75, 2.5]      # fine (4,6): coarse (2,3), xi=-1/4, eta=-1/4, sy=0
+    assert list(qp[:, 4, 1]) == [3.375, 1.25, 2.125]   # fine (5,8): coarse (2,4), xi=+1/4, eta=-1/4, sy=-1/2
+    assert list(qp[:, 0, 0]) == [2.625, 0.75, 1.875]   # fine (4,4): corner, coarse (2,2)
+    assert list(qp[:, 7, 7]) == [5.375, 4.625, 0.75]   # fine (11,11): coarse (5,5), xi=eta=+1/4, sx=1/2, sy=-1
+    n = 0
+    for jj in range(8):
+        for ii in range(8):
+            if 2 <= ii < 6 and 2 <= jj < 6:
+                continue
+            I, J = 6 + ii - 2, 6 + jj - 2
+            assert np.array_equal(qp[:, jj, ii], _hand_value(I, J)), (I, J, qp[:, jj, ii])
+            n += 1
+    assert n == 48
+
+
+def test_regrid_interp_minmod_slope_hand_values():
+    """The same rule in the regrid interpolation (new fine cells with no old fine
+    data, alpha = 1): a new box over coarse cells 2..5 x 2..5."""
+    o = oracle.Oracle((0.0, 1.0, 0.0, 1.0), W.EXTRAP, 4, 2)
+    o.set_level(1, W.uniform_level(1, 1, 8, 8, (0.0, 1.0, 0.0, 1.0)), _minmod_field().ravel())
+    o.regrid(1, [(2, 2, 4, 4)], 2)
+    q = o.read(2, 0)
+    assert list(q[:, 2, 2]) == [5.25, 2.75, 2.5]       # fine (6,6): coarse (3,3), xi=-1/4, sx=1, sy=0
+    for jj in range(8):
+        for ii in range(8):
+            assert np.array_equal(q[:, jj, ii], _hand_value(4 + ii, 4 + jj))
