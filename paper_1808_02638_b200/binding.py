@@ -125,10 +125,45 @@ def load() -> ctypes.CDLL:
 
 
 def _dptr(a):
-    if hasattr(a, "data_ptr"):  # torch tensor (pinned host or device)
+    if hasattr(a, "data_ptr"):  # torch tensor (host memory; checked by _host_f64)
         return ctypes.cast(ctypes.c_void_p(a.data_ptr()), ctypes.POINTER(ctypes.c_double))
-    assert a.dtype == np.float64 and a.flags["C_CONTIGUOUS"], "need C-contiguous float64"
     return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _host_f64(a, n: int, what: str, writable: bool = False):
+    """Check that `a` is a C-contiguous float64 HOST buffer of exactly n
+    elements (numpy array or CPU torch tensor, pinned or not) before its raw
+    pointer crosses the C-ABI, which copies n doubles from / to it: an
+    undersized, float32, strided or device buffer raises ClawError(EINVAL)
+    instead of reading or writing out of bounds."""
+    if hasattr(a, "data_ptr"):
+        import torch
+        if a.dtype != torch.float64:
+            raise ClawError(CLAW_EINVAL, f"{what}: dtype {a.dtype}, need torch.float64")
+        if a.device.type != "cpu":
+            raise ClawError(CLAW_EINVAL, f"{what}: tensor on {a.device}, need a host (CPU) tensor")
+        if not a.is_contiguous():
+            raise ClawError(CLAW_EINVAL, f"{what}: tensor is not contiguous")
+        size = a.numel()
+    else:
+        if not isinstance(a, np.ndarray):
+            raise ClawError(CLAW_EINVAL, f"{what}: need a numpy array or torch tensor, got {type(a).__name__}")
+        if a.dtype != np.float64:
+            raise ClawError(CLAW_EINVAL, f"{what}: dtype {a.dtype}, need float64")
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ClawError(CLAW_EINVAL, f"{what}: array is not C-contiguous")
+        if writable and not a.flags["WRITEABLE"]:
+            raise ClawError(CLAW_EINVAL, f"{what}: array is read-only")
+        size = a.size
+    if size != n:
+        raise ClawError(CLAW_EINVAL, f"{what}: {size} elements, need {n}")
+    return _dptr(a)
+
+
+def _as_f64(q):
+    """numpy input -> C-contiguous float64 copy if needed; torch tensors pass
+    through unchanged (and are then checked, never silently converted)."""
+    return q if hasattr(q, "data_ptr") else np.ascontiguousarray(q, dtype=np.float64)
 
 
 def _descs(descs) -> np.ndarray:
@@ -230,10 +265,22 @@ class Claw:
 
     # -- the five calls of north_star -----------------------------------
     def set_level(self, level: int, descs, q0=None):
+        """q0: the owned patches' level array (3 * owned cells doubles), or None
+        (zeros).  With world > 1 ownership is known only once the level is
+        planned, so the level is set with zeros and q0 written after the size
+        check."""
         d = _descs(descs)
         self._descs[level] = d
+        if q0 is not None:
+            q0 = _as_f64(q0)
+        if q0 is None or self.world > 1:
+            self._check(load().claw_set_level(self._h, level, len(d), d.ctypes.data, None))
+            if q0 is not None:
+                self.write_level(level, q0)
+            return
+        n = 3 * int((d["mx"].astype(np.int64) * d["my"].astype(np.int64)).sum())
         self._check(load().claw_set_level(self._h, level, len(d), d.ctypes.data,
-                                          None if q0 is None else _dptr(q0)))
+                                          _host_f64(q0, n, "set_level q0")))
 
     def fill_ghost(self, level: int, t: float = 0.0):
         self._check(load().claw_fill_ghost(self._h, level, float(t)))
@@ -254,12 +301,14 @@ class Claw:
     def read(self, level: int, patch: int) -> np.ndarray:
         d = self._descs[level][patch]
         out = np.empty((3, int(d["my"]), int(d["mx"])))
-        self._check(load().claw_read(self._h, level, patch, _dptr(out)))
+        self._check(load().claw_read(self._h, level, patch, _host_f64(out, out.size, "read", True)))
         return out
 
     def write(self, level: int, patch: int, q):
-        q = np.ascontiguousarray(q, dtype=np.float64)
-        self._check(load().claw_write(self._h, level, patch, _dptr(q)))
+        d = self._descs[level][patch]
+        q = _as_f64(q)
+        self._check(load().claw_write(self._h, level, patch,
+                                      _host_f64(q, 3 * int(d["mx"]) * int(d["my"]), "write")))
 
     # -- level-wide I/O --------------------------------------------------
     def owned_patches(self, level: int) -> np.ndarray:
@@ -271,20 +320,20 @@ class Claw:
         return 3 * cells
 
     def read_level(self, level: int, out=None):
+        n = self.level_size(level)
         if out is None:
-            out = np.empty(self.level_size(level))
-        self._check(load().claw_read_level(self._h, level, _dptr(out)))
+            out = np.empty(n)
+        self._check(load().claw_read_level(self._h, level, _host_f64(out, n, "read_level out", True)))
         return out
 
     def write_level(self, level: int, q):
-        if not hasattr(q, "data_ptr"):
-            q = np.ascontiguousarray(q, dtype=np.float64)
-        self._check(load().claw_write_level(self._h, level, _dptr(q)))
+        q = _as_f64(q)
+        self._check(load().claw_write_level(self._h, level, _host_f64(q, self.level_size(level), "write_level")))
 
     def read_padded(self, level: int, patch: int) -> np.ndarray:
         d = self._descs[level][patch]
         out = np.empty((3, int(d["my"]) + 4, int(d["mx"]) + 4))
-        self._check(load().claw_read_padded(self._h, level, patch, _dptr(out)))
+        self._check(load().claw_read_padded(self._h, level, patch, _host_f64(out, out.size, "read_padded", True)))
         return out
 
     def patch_cfl(self, level: int, patch: int) -> float:
@@ -393,13 +442,14 @@ class Claw:
         ns, _ = self.debug_halo_counts(level, peer)
         out = np.empty(3 * ns)
         if ns:
-            self._check(load().claw_halo_pack(self._h, level, peer, _dptr(out)))
+            self._check(load().claw_halo_pack(self._h, level, peer, _host_f64(out, 3 * ns, "halo_pack", True)))
         return out
 
     def halo_unpack(self, level: int, peer: int, buf: np.ndarray):
         buf = np.ascontiguousarray(buf, dtype=np.float64)
-        if buf.size:
-            self._check(load().claw_halo_unpack(self._h, level, peer, _dptr(buf)))
+        _, nr = self.debug_halo_counts(level, peer)
+        if buf.size or nr:
+            self._check(load().claw_halo_unpack(self._h, level, peer, _host_f64(buf, 3 * nr, "halo_unpack")))
 
     def debug_halo_counts(self, level: int, peer: int):
         s, r = ctypes.c_int64(), ctypes.c_int64()

@@ -167,3 +167,28 @@ def test_nccl_stand_in_loads_through_claw_nccl_lib(tmp_path):
                        capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stderr[-2000:]
     assert r.stdout.strip().splitlines()[-1].startswith("/tmp/claw_ncclshim_")
+
+
+def test_binding_rejects_bad_host_buffers_before_the_c_call():
+    """every raw pointer the binding passes (set_level q0, write,
+    write_level, read_level out=) is checked for dtype, contiguity, host
+    residency and exact size; nothing reaches the C-ABI otherwise."""
+    import torch
+    d = W.uniform_level(2, 2, 4, 4)            # 4 patches of 4x4 -> 192 doubles
+    n = 3 * 64
+    g = host_ctx()
+    # (numpy INPUTS of another dtype or stride are copied to float64 first;
+    # torch tensors are never converted, and outputs never)
+    bad = [np.zeros(n - 1), np.zeros(n + 3), np.zeros((n + 1, 2), np.float32)[:, 0],
+           torch.zeros(n, dtype=torch.float32), torch.zeros(2 * n, dtype=torch.float64)[::2],
+           torch.zeros(n - 1, dtype=torch.float64), [0.0] * (n - 1)]
+    for q in bad:
+        with pytest.raises(binding.ClawError) as e:
+            g.set_level(1, d, q)
+        assert e.value.code == binding.CLAW_EINVAL, q
+    for out in (np.broadcast_to(np.zeros(1), (8,)), np.zeros(8, np.float32), np.zeros(16)[::2], np.zeros(7)):
+        with pytest.raises(binding.ClawError) as e:  # output buffers: read-only, float32, strided, short
+            binding._host_f64(out, 8, "out", writable=True)
+        assert e.value.code == binding.CLAW_EINVAL
+    for q in (np.zeros(n), torch.zeros(n, dtype=torch.float64)):
+        assert binding._host_f64(q, n, "ok") is not None
