@@ -364,7 +364,8 @@ def main():
             if L > 1:
                 g.fill_ghost(L, t)
             tol, buf, cut, mxd, mnd, R = regrid_params(wl, L, float(g.descs(L)["dx"][0]), dx1, args.regrid_tol)
-            g.regrid_auto(L, tol, buf, cut, mxd, mnd, R)
+            if g.regrid_auto(L, tol, buf, cut, mxd, mnd, R) == 0:
+                break  # nothing flagged: level L+1 (and finer) removed; the next regrid may re-create them
         regrid_ms.append(1000.0 * (time.perf_counter() - t0))
 
     if dyn:

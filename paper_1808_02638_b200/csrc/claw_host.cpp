@@ -376,7 +376,6 @@ struct Level {
   int64_t ngrid_tiles = 0;
   int64_t ngrid_blocks = 0;   // row blocks of the band (grid mode)
   int grid_th = 0;            // rows per grid tile (> my: tiles span patch rows)
-  int grid_wide = 0;          // grid mode runs the wide kernel (two columns per lane)
   bool use_side = false;      // generic kernel: side records by a side_kernel ahead of the step
   bool sparse = false;        // grid kernel on a sparse lattice of equal patches
   std::vector<int32_t> hslots;  // lattice slot -> patch (>= 0) or -1-v (virtual slot v)
@@ -430,6 +429,7 @@ struct claw_ctx {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_step, ev_ghost, ev_pool;
   claw_stats stats{};
   int tile_rows = 64;
+  int nsm = 148;            // SM count of the device (queried at create; B200: 148)
   unsigned long long* hier_slot = nullptr;  // set while claw_advance_hierarchy runs
   cudaStream_t comm_stream = nullptr;       // world > 1: halo pack + NCCL send/recv
   cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
@@ -450,16 +450,6 @@ struct claw_ctx {
 };
 
 namespace {
-
-// the wide grid kernel (two columns per lane) is opt-in (CLAW_GRID_WIDE=1):
-// 15% fewer instructions but 12 instead of 16 resident warps per SM, measured
-// 2.5% (C5) / 7% (C4) slower than the 32-lane kernel (profiles/README.md).
-// It needs even patch widths, so a lane's column pair never straddles patches.
-int grid_wide_ok(int mx) {
-  const char* e = std::getenv("CLAW_GRID_WIDE");
-  if (!e || e[0] != '1') return 0;
-  return mx % 2 == 0 ? 1 : 0;
-}
 
 int fail(claw_ctx* c, int code, const char* fmt, ...) {
   if (c) {
@@ -1300,7 +1290,7 @@ int plan_level(claw_ctx* c, int level, Level& L) {
   for (size_t lp = 1; lp < L.hpatch.size(); ++lp)
     if (L.hpatch[lp].c != L.hpatch[0].c || L.hpatch[lp].Z != L.hpatch[0].Z) L.uniform = false;
   // rows per tile: the configured value, or (auto) the largest power of two
-  // <= 64 that still gives ~half a tile per resident warp of the GPU (148 SMs
+  // <= 64 that still gives ~half a tile per resident warp of the GPU (SMs
   // x 16 warps); small, latency-bound levels get short tiles (>= 8) so the
   // serial row march of each warp stays short (measured: C3's level 3 runs
   // 2.5% faster with 32-row tiles at 0.7 tiles per warp than with 16-row
@@ -1308,7 +1298,7 @@ int plan_level(claw_ctx* c, int level, Level& L) {
   if (c->cfg.tile_rows > 0) {
     L.th = c->tile_rows;
   } else {
-    const int64_t want = 148 * 8;
+    const int64_t want = static_cast<int64_t>(c->nsm) * 8;
     int th = 64;
     while (th > 8 && L.cells_owned / (32ll * th) < want) th /= 2;
     L.th = th;
@@ -1325,14 +1315,13 @@ int plan_level(claw_ctx* c, int level, Level& L) {
     const int th = std::min(L.th, my);
     L.grid_th = th;
     const int nbr = (my + th - 1) / th;
-    L.grid_wide = grid_wide_ok(mx);
-    const int64_t npy = L.ny / my, nstrip = claw::grid_nstrip(L.nx, L.grid_wide);
+    const int64_t npy = L.ny / my, nstrip = claw::grid_nstrip(L.nx);
     L.hgtile.clear();
     for (int64_t pr = 0; pr < npy; ++pr)
       for (int rb = 0; rb < nbr; ++rb)
         for (int64_t st = 0; st < nstrip; ++st) {
           int64_t c0, c1;
-          claw::grid_strip_cols(st, L.grid_wide, L.nx, c0, c1);
+          claw::grid_strip_cols(st, L.nx, c0, c1);
           bool any = false;
           for (int64_t pc = c0 / mx; pc <= (c1 - 1) / mx && !any; ++pc) any = L.hslots[pr * L.npx + pc] >= 0;
           if (any) L.hgtile.push_back(make_int4(static_cast<int>(st), static_cast<int>(pr * nbr + rb), 0, 0));
@@ -1365,8 +1354,7 @@ int plan_level(claw_ctx* c, int level, Level& L) {
       // patch-row boundaries), which halves the per-tile prologue on 32-row
       // patches; CLAW_GRID_TH overrides (tuning)
       int th = std::min(L.th, my);
-      L.grid_wide = grid_wide_ok(mx);
-      const int64_t nstrip0 = claw::grid_nstrip(L.nx, L.grid_wide);
+      const int64_t nstrip0 = claw::grid_nstrip(L.nx);
       auto span_ok = [&](int w) { return w > my && w % my == 0 && my % 4 == 0 && my >= 8 && w <= 512; };
       if (const char* e = std::getenv("CLAW_GRID_TH")) {
         if (span_ok(std::atoi(e))) th = std::atoi(e);
@@ -1374,16 +1362,16 @@ int plan_level(claw_ctx* c, int level, Level& L) {
         if (span_ok(c->cfg.tile_rows)) th = c->cfg.tile_rows;
       } else if (L.th == 64) {
         // large level: the tallest tile (<= 256 rows) that still gives two
-        // waves of warps (148 SMs x 16 resident warps x 2); measured C5 +3.6%,
+        // waves of warps (SMs x 16 resident warps x 2); measured C5 +3.6%,
         // C4 +7% over one-patch-row tiles (profiles/r01_grid_tile_rows.txt)
         for (int w = 256; w > my; w /= 2)
-          if (span_ok(w) && nstrip0 * ((L.Y1 - L.Y0 + w - 1) / w) >= 148 * 16 * 2) {
+          if (span_ok(w) && nstrip0 * ((L.Y1 - L.Y0 + w - 1) / w) >= static_cast<int64_t>(c->nsm) * 16 * 2) {
             th = w;
             break;
           }
       }
       L.grid_th = th;
-      const int64_t nstrip = claw::grid_nstrip(L.nx, L.grid_wide);
+      const int64_t nstrip = claw::grid_nstrip(L.nx);
       L.ngrid_blocks = th > my ? ((L.Y1 - L.Y0) + th - 1) / th : ((L.Y1 - L.Y0) / my) * ((my + th - 1) / th);
       L.ngrid_tiles = nstrip * L.ngrid_blocks;
     }
@@ -1399,16 +1387,18 @@ int plan_level(claw_ctx* c, int level, Level& L) {
     if (e && (e[0] == '0' || e[0] == '1')) {
       L.lane_tiles = e[0] == '1';
     } else {
+      // lane tiles take the rows the tile loop below gives them (gth)
+      const int lth = c->cfg.tile_rows == 0 ? std::min(L.th, 32) : L.th;
       int64_t n30 = 0, n32 = 0, t30 = 0;
       for (size_t lp = 0; lp < L.owned.size(); ++lp) {
         n30 += (L.hpatch[lp].mx + 29) / 30;
         n32 += (L.hpatch[lp].mx + 31) / 32;
-        t30 += static_cast<int64_t>((L.hpatch[lp].mx + 29) / 30) * ((L.hpatch[lp].my + L.th - 1) / L.th);
+        t30 += static_cast<int64_t>((L.hpatch[lp].mx + 29) / 30) * ((L.hpatch[lp].my + lth - 1) / lth);
       }
-      // a level whose lane tiles fit in one wave of resident warps (148 SMs x
+      // a level whose lane tiles fit in one wave of resident warps (SMs x
       // 16) is latency-bound: the extra warps are free and the march without
       // side passes is shorter
-      L.lane_tiles = (5 * n30 <= 6 * n32 || t30 <= 148 * 16) ? 1 : 0;
+      L.lane_tiles = (5 * n30 <= 6 * n32 || t30 <= static_cast<int64_t>(c->nsm) * 16) ? 1 : 0;
     }
   }
   const int tstrip = L.lane_tiles ? 30 : 32;
@@ -1831,6 +1821,7 @@ int claw_create(const claw_config* cfg, claw_ctx** out) {
   *out = ctx;
   if (ctx->host_only) return CLAW_OK;
   CUDA_TRY(cudaSetDevice(cfg->device));
+  CUDA_TRY(cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, cfg->device));
   if (cfg->stream) {
     ctx->stream = static_cast<cudaStream_t>(cfg->stream);
   } else {
@@ -2070,7 +2061,6 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
     P.my = L.desc[0].my;
     P.npx = L.npx;
     P.th = L.grid_th;
-    P.wide = L.grid_wide;
     P.per_x = ctx->cfg.bc[0] == CLAW_BC_PERIODIC;
     P.per_y = ctx->cfg.bc[2] == CLAW_BC_PERIODIC;
     P.ntiles = static_cast<int32_t>(L.ngrid_tiles);
@@ -2092,7 +2082,7 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
     claw::StepParams Pi = P, Pe = P;
     int64_t n_int = 0, n_all = 0;
     if (L.grid) {
-      const int64_t nstrip = claw::grid_nstrip(L.nx, L.grid_wide);
+      const int64_t nstrip = claw::grid_nstrip(L.nx);
       const int64_t nb = L.ngrid_blocks;
       if (nb >= 3) {
         Pi.blk_first = 1;

@@ -72,7 +72,6 @@ struct StepParams {
   const int4* tiles;
   int32_t ntiles;
   int32_t limiter, order_trans;
-  int32_t wide;                   // grid mode: the wide kernel (two columns per lane, 62-column strips)
   double dt;
   unsigned long long* patch_cfl;  // per owned patch, bits of a non-negative double (plain stores)
   unsigned long long* level_cfl;  // level slot of this step (atomicMax)
@@ -210,7 +209,7 @@ int max_tile_rows();
 int side_stride();
 int grid_strip();
 // grid-mode strips: count over nx level columns, output columns of strip s
-int64_t grid_nstrip(int64_t nx, int wide);
-void grid_strip_cols(int64_t s, int wide, int64_t nx, int64_t& c0, int64_t& c1);
+int64_t grid_nstrip(int64_t nx);
+void grid_strip_cols(int64_t s, int64_t nx, int64_t& c0, int64_t& c1);
 
 }  // namespace claw
