@@ -102,34 +102,79 @@ def cpu_model():
 # clocks during the timed region (B200_PROFILING.md clocks line)
 # ---------------------------------------------------------------------------
 class ClockSampler:
+    """SM clock, power and clock-event reasons sampled every 5 ms through NVML
+    (nvidia-ml-py) while the timed region runs, so even a ~0.1 s region gets
+    tens of samples; falls back to `nvidia-smi -lms 100`."""
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80}
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, device: int):
+    def __init__(self, device: int, period_s: float = 0.005):
         self.device = device
-        self.rows = []
+        self.period = period_s
+        self.rows = []       # (sm_mhz, max_mhz, power_w, reasons-set)
         self.proc = None
         self.thread = None
+        self.stop_ev = threading.Event()
+        self.source = None
+        self.nv = None
+        try:
+            import pynvml as nv
+            import torch
+            nv.nvmlInit()
+            uuid = str(torch.cuda.get_device_properties(device).uuid)
+            self.h = nv.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+            self.nv = nv
+            self.source = f"nvml every {period_s * 1000:.0f} ms"
+        except Exception:  # noqa: BLE001 -- any NVML problem: use nvidia-smi
+            self.nv = None
+
+    def _nvml_loop(self):
+        nv = self.nv
+        get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        while not self.stop_ev.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                pw = nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0
+                bits = get_r(self.h)
+                self.rows.append((float(sm), float(mx), pw, {k for k, b in self.BITS.items() if bits & b}))
+            except Exception:  # noqa: BLE001
+                pass
+            self.stop_ev.wait(self.period)
 
     def start(self):
+        if self.nv is not None:
+            self.thread = threading.Thread(target=self._nvml_loop, daemon=True)
+            self.thread.start()
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.source = "nvidia-smi -lms 100"
         except OSError:
             self.proc = None
             return
-        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread = threading.Thread(target=self._smi_loop, daemon=True)
         self.thread.start()
 
-    def _read(self):
+    def _smi_loop(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self.proc.stdout:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 9:
-                self.rows.append(parts)
+            r = [x.strip() for x in line.split(",")]
+            if len(r) >= 9:
+                try:
+                    self.rows.append((float(r[1]), float(r[2]), float(r[3]),
+                                      {names[k] for k in range(4) if r[5 + k].lower() == "active"}))
+                except ValueError:
+                    pass
 
     def stop(self):
+        self.stop_ev.set()
         if self.proc:
             self.proc.terminate()
             try:
@@ -142,14 +187,9 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[5 + k].lower() == "active"})
-        pw = [float(r[3]) for r in self.rows if r[3].replace(".", "").isdigit()]
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows),
-                "power_w_max": max(pw) if pw else None}
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": sorted(set().union(*(r[3] for r in self.rows))), "samples": len(self.rows),
+                "power_w_max": max(r[2] for r in self.rows), "source": self.source}
 
 
 # ---------------------------------------------------------------------------
@@ -239,27 +279,117 @@ def oracle_sample(wl: W.Workload, budget_s: float = 12.0, steps_cap: int | None 
     return counted[0] / el, cores, f"{desc}, {n} coarse steps (with updating), {el:.1f} s"
 
 
+def mem_available_bytes() -> int:
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+def oracle_workload_stepper(wl: W.Workload, cores: int, reflux: bool):
+    """The oracle holding the WHOLE workload (C4/C5: every patch at full size,
+    when the host has the memory; fixed hierarchies: every level), and a
+    function that runs one of its steps (a level step of the uniform level, a
+    Berger-Oliger coarse step with updating of a hierarchy).  Returns (step,
+    cell-updates per step, description) or None when the full size does not
+    fit the host memory."""
+    import oracle
+    d0 = wl.levels[0].descs
+    if len(wl.levels) == 1:
+        cells = int((d0["mx"].astype(np.int64) * d0["my"]).sum())
+        need = 24 * int(((d0["mx"].astype(np.int64) + 4) * (d0["my"] + 4)).sum()) + 2 * 24 * cells
+        if need * 1.5 > mem_available_bytes():
+            return None
+        o = oracle.Oracle(wl.domain, wl.bc, wl.limiter, wl.order_trans, nthreads=cores)
+        o.set_level(1, d0, W.ring_ic(d0))
+        dt = wl.dt0()
+        n = [0]
+
+        def step():
+            o.fill_ghost(1, n[0] * dt)
+            o.advance_level(1, dt)
+            n[0] += 1
+        return step, cells, f"the full {wl.name} level ({len(d0)} patches, {cells} cells), one level step per step"
+    o = oracle.Oracle(wl.domain, wl.bc, wl.limiter, wl.order_trans, nthreads=cores, reflux=reflux)
+    for L, (lv, q) in enumerate(zip(wl.levels, W.hierarchy_ic(wl)), start=1):
+        o.set_level(L, lv.descs, q)
+    rat = hierarchy_ratios(wl)
+    nlev = 1 + len(rat)
+    dt = wl.dt0()
+    n = [0]
+
+    def bo(level, t, dtl):
+        o.fill_ghost(level, t)
+        o.advance_level(level, dtl)
+        if level < nlev:
+            R = rat[level - 1]
+            for k in range(R):
+                bo(level + 1, t + k * dtl / R, dtl / R)
+            o.update_level(level + 1)
+
+    def step():
+        bo(1, n[0] * dt, dt)
+        n[0] += 1
+    cells = sum(int((lv.descs["mx"].astype(np.int64) * lv.descs["my"]).sum()) * int(np.prod(rat[:L]))
+                for L, lv in enumerate(wl.levels))
+    return step, cells, f"the full {wl.name} hierarchy, one coarse step (with updating) per step"
+
+
 def run_reference(args, rank):
+    """The reference arm of this paper-only build: the CPU oracle as it stands,
+    on the host cores, on the same workload.  Each step is one step of the
+    WHOLE workload (C5: all 268 M cells) when the host memory holds it and K
+    of them fit a few minutes; otherwise each step is a bounded sample of it
+    (said in cpu_baseline.sample)."""
     if rank != 0:
         return 0
     import oracle
     oracle.build()
     wl = workload(args.config)
-    vals = []
-    desc = ""
     cores = host_cores()
-    for _ in range(args.warmup):
-        oracle_sample(wl, budget_s=2.0, steps_cap=1, reflux=args.reflux)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        v, cores, desc = oracle_sample(wl, budget_s=max(1.0, 60.0 / max(args.steps, 1)), steps_cap=None,
-                                       reflux=args.reflux)
-        vals.append(v)
-    el = time.perf_counter() - t0
-    value = statistics.median(vals)
+    budget_s = 240.0
+    t_setup = time.perf_counter()
+    st = None if wl.extra.get("ratios") else oracle_workload_stepper(wl, cores, args.reflux)
+    setup_s = time.perf_counter() - t_setup
+    times = []
+    if st is not None:
+        step, cells, desc = st
+        t0 = time.perf_counter()
+        step()                                   # first warm-up step sizes the run
+        first = time.perf_counter() - t0
+        if first * (args.steps + max(args.warmup - 1, 0)) > budget_s:
+            st = None                            # too slow for K full steps: bounded samples instead
+            del step
+        else:
+            for _ in range(max(args.warmup - 1, 0)):
+                step()
+            for _ in range(args.steps):
+                t0 = time.perf_counter()
+                step()
+                times.append(time.perf_counter() - t0)
+            value = cells * len(times) / sum(times)
+            ms_per_step = 1000.0 * sum(times) / len(times)
+            desc = f"{desc}; {len(times)} timed steps after {args.warmup} warm-up, setup {setup_s:.1f} s"
+    if st is None:
+        vals, desc = [], ""
+        for _ in range(args.warmup):
+            oracle_sample(wl, budget_s=2.0, steps_cap=1, reflux=args.reflux)
+        for _ in range(args.steps):
+            v, cores, desc = oracle_sample(wl, budget_s=max(1.0, 60.0 / max(args.steps, 1)), steps_cap=None,
+                                           reflux=args.reflux)
+            vals.append(v)
+        value = statistics.median(vals)
+        cells = wl.levels[0].cells if len(wl.levels) == 1 else None
+        # one step of the workload at the sampled rate (not a measured step)
+        ms_per_step = 1000.0 * cells / value if cells else None
+        desc = f"bounded samples per step: {desc} (median of {args.steps})"
     line = {"impl": "reference", "metric": "fp64 cell-updates/s", "value": value, "unit": "cell-updates/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000.0 * el / max(args.steps, 1), "higher_is_better": True,
+            "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": wl.name, "note": wl.note,
                        "conservation_fix": bool(args.reflux and len(wl.levels) > 1)},
@@ -268,6 +398,20 @@ def run_reference(args, rank):
             "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` without a launcher: start N ranks of this same
+    command through torch.distributed.run (one process per GPU, rendezvous on
+    127.0.0.1); rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    print(f"[bench] spawning {n} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.run(cmd).returncode
 
 
 # ---------------------------------------------------------------------------
@@ -295,7 +439,12 @@ def main():
                          "(claw exchange=1), ranks may share one GPU; never a bench number")
     args = ap.parse_args()
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus))
     world = env_int("WORLD_SIZE", 1)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but {world} rank(s) were launched (WORLD_SIZE); "
+                         "launch N ranks with --gpus N, or omit the launcher and let --gpus N spawn them")
     rank = env_int("RANK", 0)
     local_rank = env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
@@ -340,6 +489,17 @@ def main():
     g = binding.Claw(wl.domain, wl.bc, wl.limiter, wl.order_trans, device=device, rank=rank,
                      world=world, nccl_id=nccl_id, stream=stream.cuda_stream, tile_rows=args.tile_rows,
                      path=args.path, exchange=1 if host_x else 0, reflux=args.reflux and nlev > 1)
+    comm = None
+    if world > 1:
+        ci = g.comm_info()   # the communicator as NCCL reports it (None: external exchange)
+        comm = {"rank": rank, "world": world, "cuda_device": device,
+                "nccl_nranks": ci[0] if ci else None, "nccl_rank": ci[1] if ci else None,
+                "nccl_cuda_device": ci[2] if ci else None}
+        print(f"[bench] rank {rank}/{world} cuda:{device}: libclaw NCCL communicator "
+              + (f"nranks={ci[0]} rank={ci[1]} cudaDev={ci[2]}" if ci else "none (external exchange)"),
+              file=sys.stderr, flush=True)
+        if ci and (ci[0] != world or ci[1] != rank):
+            raise SystemExit(f"rank {rank}: NCCL communicator reports nranks={ci[0]} rank={ci[1]}")
 
     # inputs: host-side synthetic data of the workload's shape, uploaded once
     # through the API; pinned so the e2e leg measures the real H2D path
@@ -448,10 +608,19 @@ def main():
         total_cells_per_step = st["cells_advanced"] / args.steps
         cells_per_step_rank = total_cells_per_step
     g.set_profiling(False)
+    per_rank = None
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        # every rank's device time of the K steps and its step-kernel busy
+        # time; value uses the max over ranks
+        mine = torch.tensor([ms, st["step_ms"]], dtype=torch.float64, device=red_dev)
+        allr = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(allr, mine)
+        per_rank = {"ms": [float(x[0]) for x in allr], "step_kernel_busy_ms": [float(x[1]) for x in allr]}
+        ms = max(per_rank["ms"])
+        per_rank["max_ms"] = ms
+        comms = [None] * world
+        dist.all_gather_object(comms, comm)
+        per_rank["comm"] = comms
     value = total_cells_per_step * args.steps / (ms / 1000.0)
 
     # ---- roofline of the dominant kernel (the fused step kernel)
@@ -592,6 +761,8 @@ def main():
                            if total_cells_per_step * 24 > 126e6 else "state fits L2 (latency-bound config)"},
                 "roofline": roof, "clocks": clk, "e2e": e2e, "gpu_launches": gpu_launches,
                 "per_gpu_value": value / world}
+        if per_rank is not None:
+            line["per_rank"] = per_rank
         if cpu is not None:
             line["cpu_baseline"] = cpu
         if test_x:

@@ -310,6 +310,13 @@ int claw_synchronize(claw_ctx* ctx);
  * NCCL cannot be loaded. */
 int claw_nccl_unique_id(void* out128);
 
+/* The context's NCCL communicator as NCCL itself reports it (ncclCommCount,
+ * ncclCommUserRank, ncclCommCuDevice): multi-GPU runs log it so the rank
+ * count and device mapping are checked, not assumed.  ESTATE if the context
+ * has no NCCL communicator (world = 1 or exchange = 1) or the loaded NCCL
+ * lacks these calls; ENCCL if NCCL fails. */
+int claw_comm_info(const claw_ctx* ctx, int32_t* nranks, int32_t* rank, int32_t* cuda_device);
+
 /* Library version / build string (host-only). */
 const char* claw_version(void);
 

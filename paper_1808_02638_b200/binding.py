@@ -35,7 +35,7 @@ EXPORTS = [
     "claw_level_mode", "claw_advance_hierarchy", "claw_halo_pack", "claw_halo_unpack",
     "claw_update_level", "claw_reflux_registers", "claw_level_extent", "claw_level_count",
     "claw_level_descs", "claw_flag", "claw_cluster", "claw_regrid", "claw_regrid_auto",
-    "claw_pool_stats", "claw_pool_trim",
+    "claw_pool_stats", "claw_pool_trim", "claw_comm_info",
 ]
 CLAW_HIER_UPDATE = 1
 
@@ -118,6 +118,8 @@ def load() -> ctypes.CDLL:
     L.claw_regrid.argtypes = [vp, i32, i32, vp, i32]
     L.claw_regrid_auto.argtypes = [vp, i32, d, i32, d, i32, i32, i32, ctypes.POINTER(ctypes.c_int32)]
     L.claw_pool_stats.argtypes = [i64, i64, i64]
+    L.claw_comm_info.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                                 ctypes.POINTER(ctypes.c_int32)]
     L.claw_halo_pack.argtypes = [vp, i32, i32, dp]
     L.claw_halo_unpack.argtypes = [vp, i32, i32, dp]
     _lib = L
@@ -461,6 +463,16 @@ class Claw:
         self._check(load().claw_debug_halo_send(self._h, level, peer, k, ctypes.byref(p),
                                                 ctypes.byref(i), ctypes.byref(j)))
         return p.value, i.value, j.value
+
+    def comm_info(self):
+        """(nranks, rank, cuda_device) of the context's NCCL communicator as
+        NCCL reports it, or None when there is none (world 1 / external)."""
+        n, r, d = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        rc = load().claw_comm_info(self._h, ctypes.byref(n), ctypes.byref(r), ctypes.byref(d))
+        if rc == CLAW_ESTATE:
+            return None
+        self._check(rc)
+        return n.value, r.value, d.value
 
     def set_profiling(self, on: bool = True):
         self._check(load().claw_set_profiling(self._h, int(on)))

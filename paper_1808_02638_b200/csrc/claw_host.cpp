@@ -58,6 +58,10 @@ struct Nccl {
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  // optional (introspection only): the communicator's own view
+  ncclResult_t (*CommCount)(const ncclComm_t, int*) = nullptr;
+  ncclResult_t (*CommUserRank)(const ncclComm_t, int*) = nullptr;
+  ncclResult_t (*CommCuDevice)(const ncclComm_t, int*) = nullptr;
   bool load(std::string& err) {
     if (h) return true;
     // CLAW_NCCL_LIB: an explicit library (tests load a stand-in that runs
@@ -93,6 +97,9 @@ struct Nccl {
     SYM(GetUniqueId) SYM(CommInitRank) SYM(CommDestroy) SYM(AllReduce) SYM(Send) SYM(Recv)
     SYM(GroupStart) SYM(GroupEnd) SYM(GetErrorString)
 #undef SYM
+    CommCount = reinterpret_cast<decltype(CommCount)>(dlsym(h, "ncclCommCount"));
+    CommUserRank = reinterpret_cast<decltype(CommUserRank)>(dlsym(h, "ncclCommUserRank"));
+    CommCuDevice = reinterpret_cast<decltype(CommCuDevice)>(dlsym(h, "ncclCommCuDevice"));
     return true;
   }
 };
@@ -1844,6 +1851,19 @@ int claw_create(const claw_config* cfg, claw_ctx** out) {
     ncclResult_t r = g_nccl.CommInitRank(&ctx->comm, cfg->world, id, cfg->rank);
     if (r != ncclSuccess) return nccl_fail(ctx, r, "ncclCommInitRank");
   }
+  return CLAW_OK;
+}
+
+int claw_comm_info(const claw_ctx* ctx, int32_t* nranks, int32_t* rank, int32_t* cuda_device) {
+  if (!ctx || !nranks || !rank || !cuda_device) return CLAW_EINVAL;
+  if (!ctx->comm || !g_nccl.CommCount || !g_nccl.CommUserRank || !g_nccl.CommCuDevice) return CLAW_ESTATE;
+  int n = 0, r = 0, d = 0;
+  if (g_nccl.CommCount(ctx->comm, &n) != ncclSuccess || g_nccl.CommUserRank(ctx->comm, &r) != ncclSuccess ||
+      g_nccl.CommCuDevice(ctx->comm, &d) != ncclSuccess)
+    return CLAW_ENCCL;
+  *nranks = n;
+  *rank = r;
+  *cuda_device = d;
   return CLAW_OK;
 }
 

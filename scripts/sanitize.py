@@ -1,0 +1,76 @@
+"""Small runs of every kernel family for compute-sanitizer (memcheck, racecheck,
+synccheck, initcheck); see scripts/gpu_sanitize.sh.
+
+  grid     step_grid_kernel (dense): C1 and a reduced C4 (8x8 patches of 32^2,
+           spanning tiles), both BCs
+  generic  step_lane_kernel and step_kernel (+ side_kernel) on a ragged level
+  hier     C3-shaped hierarchy (sparse-lattice grid kernel, interp_kernel,
+           update kernels, reflux kernels) on a reduced C2 with reflux
+  regrid   flag / dilate / sat / regrid kernels (claw_regrid_auto)
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1808_02638_b200 import binding, workloads as W  # noqa: E402
+
+what = sys.argv[1:] or ["grid", "generic", "hier", "regrid"]
+
+if "grid" in what:
+    for d, bc in ((W.c1().levels[0].descs, W.EXTRAP), (W.uniform_level(8, 8, 32, 32), W.PERIODIC)):
+        g = binding.Claw(W.DOMAIN, bc, 4, 2, device=0, tile_rows=128 if len(d) > 1 else 0)
+        g.set_level(1, d, W.random_ic(d, 1))
+        for n in range(3):
+            g.fill_ghost(1, 0.0)
+            g.advance_level(1, 0.9 * float(d["dx"][0]))
+        g.read_level(1)
+        g.close()
+    print("grid ok")
+
+if "generic" in what:
+    d = W.ragged_level(3, 70, 66, 40)
+    for lane in ("1", "0"):
+        os.environ["CLAW_LANE"] = lane
+        g = binding.Claw(W.DOMAIN, W.EXTRAP, 3, 2, device=0)
+        g.set_level(1, d, W.random_ic(d, 2))
+        for n in range(3):
+            g.fill_ghost(1, 0.0)
+            g.advance_level(1, 0.8 * 2 / 70)
+        g.read_level(1)
+        g.close()
+    os.environ.pop("CLAW_LANE")
+    print("generic ok")
+
+if "hier" in what:
+    wl = W.c2()
+    g = binding.Claw(wl.domain, wl.bc, 4, 2, device=0, reflux=True)
+    for L, (lv, q) in enumerate(zip(wl.levels, W.hierarchy_ic(wl)), start=1):
+        g.set_level(L, lv.descs, q)
+    dt = wl.dt0()
+    for n in range(2):
+        g.advance_hierarchy(n * dt, dt, update=True)
+    g.close()
+    wl = W.c3()
+    g = binding.Claw(wl.domain, wl.bc, 4, 2, device=0)
+    for L, (lv, q) in enumerate(zip(wl.levels, W.hierarchy_ic(wl)), start=1):
+        g.set_level(L, lv.descs, q)
+    assert g.level_mode(3) == "sparse"
+    g.advance_hierarchy(0.0, wl.dt0(), update=True)
+    g.close()
+    print("hier ok")
+
+if "regrid" in what:
+    wl = W.paper(n1=96, npx=2)
+    g = binding.Claw(wl.domain, wl.bc, wl.limiter, wl.order_trans, device=0)
+    g.set_level(1, wl.levels[0].descs, W.hierarchy_ic(wl)[0])
+    dx1 = float(wl.levels[0].descs["dx"][0])
+    import bench
+    for L in (1, 2):
+        if L > 1:
+            g.fill_ghost(L, 0.0)
+        n = g.regrid_auto(L, *bench.regrid_params(wl, L, float(g.descs(L)["dx"][0]), dx1, 0.02))
+        if n == 0:
+            break
+    g.advance_hierarchy(0.0, wl.dt0(), update=True)
+    g.close()
+    print("regrid ok")

@@ -128,6 +128,22 @@ ncclResult_t ncclCommInitRank(ncclComm_t* comm, int world, ncclUniqueId id, int 
   return ncclSuccess;
 }
 
+/* introspection (claw_comm_info); the stand-in has no device of its own: the
+ * caller's current device */
+ncclResult_t ncclCommCount(const ncclComm_t c, int* n) {
+  *n = c->world;
+  return ncclSuccess;
+}
+ncclResult_t ncclCommUserRank(const ncclComm_t c, int* r) {
+  *r = c->rank;
+  return ncclSuccess;
+}
+ncclResult_t ncclCommCuDevice(const ncclComm_t c, int* d) {
+  (void)c;
+  *d = -1;
+  return ncclSuccess;
+}
+
 ncclResult_t ncclCommDestroy(ncclComm_t c) {
   if (!c) return ncclSuccess;
   barrier(c);
