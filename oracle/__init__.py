@@ -88,6 +88,14 @@ def lib() -> ctypes.CDLL:
         L.oracle_rpn2.argtypes = [ctypes.c_int, dp, dp, ctypes.c_double, ctypes.c_double,
                                   dp, dp, dp, dp]
         L.oracle_rpt2.argtypes = [ctypes.c_int, dp, ctypes.c_double, ctypes.c_double, dp, dp]
+        L.oracle_set_aux.argtypes = [vp, ctypes.c_int, dp]
+        L.oracle_rpn2_vc.argtypes = [ctypes.c_int, dp, dp] + [ctypes.c_double] * 4 + [dp] * 4
+        L.oracle_rpn2_vc.restype = None
+        L.oracle_rpt2_vc.argtypes = [ctypes.c_int, dp] + [ctypes.c_double] * 6 + [dp, dp]
+        L.oracle_rpt2_vc.restype = None
+        L.oracle_step_patch_vc.argtypes = [ctypes.c_int, ctypes.c_int, dp, dp, ctypes.c_double,
+                                           ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                           ctypes.c_int, dp, dp]
         L.oracle_philim.argtypes = [ctypes.c_int, ctypes.c_double]
         L.oracle_philim.restype = ctypes.c_double
         _lib = L
@@ -137,6 +145,14 @@ class Oracle:
         self._descs[level] = d
         self._check(lib().oracle_set_level(self._h, level, len(d), d.ctypes.data,
                                            None if q is None else _dp(q)))
+
+    def set_aux(self, level: int, aux: np.ndarray):
+        """Variable media of the single level 1 (R20): aux =
+        [patch][2][my][mx] (rho, K) flat, every value finite and > 0."""
+        a = np.ascontiguousarray(aux, dtype=np.float64)
+        d = self._descs[level]
+        assert a.size == 2 * int((d["mx"].astype(np.int64) * d["my"]).sum())
+        self._check(lib().oracle_set_aux(self._h, level, _dp(a)))
 
     def fill_ghost(self, level: int, t: float = 0.0):
         self._check(lib().oracle_fill_ghost(self._h, level, float(t)))
@@ -234,6 +250,37 @@ def step_patch(qpad: np.ndarray, dx, dy, dt, rho=1.0, K=1.0, limiter=4, order_tr
     if rc != 0:
         raise OracleError("oracle_step_patch failed")
     return out, c.value
+
+
+def step_patch_vc(qpad: np.ndarray, auxpad: np.ndarray, dx, dy, dt, limiter=4, order_trans=2):
+    """One step with per-cell media: auxpad = [2][my+4][mx+4] (rho, K) with
+    its ghost frame set; returns (qout_pad, cfl)."""
+    qpad = np.ascontiguousarray(qpad, dtype=np.float64)
+    auxpad = np.ascontiguousarray(auxpad, dtype=np.float64)
+    _, py, px = qpad.shape
+    assert auxpad.shape == (2, py, px)
+    out = np.empty_like(qpad)
+    c = ctypes.c_double()
+    rc = lib().oracle_step_patch_vc(px - 4, py - 4, _dp(qpad), _dp(auxpad), dx, dy, dt,
+                                    limiter, order_trans, _dp(out), ctypes.byref(c))
+    if rc != 0:
+        raise OracleError("oracle_step_patch_vc failed")
+    return out, c.value
+
+
+def rpn2_vc(ixy, ql, qr, rhol, Kl, rhor, Kr):
+    ql = np.ascontiguousarray(ql, dtype=np.float64)
+    qr = np.ascontiguousarray(qr, dtype=np.float64)
+    wave = np.empty((2, 3)); s = np.empty(2); am = np.empty(3); ap = np.empty(3)
+    lib().oracle_rpn2_vc(ixy, _dp(ql), _dp(qr), rhol, Kl, rhor, Kr, _dp(wave), _dp(s), _dp(am), _dp(ap))
+    return wave, s, am, ap
+
+
+def rpt2_vc(ixy, asdq, rho_m, K_m, rho, K, rho_p, K_p):
+    a = np.ascontiguousarray(asdq, dtype=np.float64)
+    bm = np.empty(3); bp = np.empty(3)
+    lib().oracle_rpt2_vc(ixy, _dp(a), rho_m, K_m, rho, K, rho_p, K_p, _dp(bm), _dp(bp))
+    return bm, bp
 
 
 def rpn2(ixy, ql, qr, rho=1.0, K=1.0):

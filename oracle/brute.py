@@ -16,6 +16,14 @@ P:500 "corner transport"); rpn2/rpt2 are the eigen-splittings of A and B of
 P:457-466 (linear acoustics).  Ghost cells are made here with numpy padding
 (edge = zero-order extrapolation, wrap = periodic), independently of the
 oracle's ghost fill.
+
+Variable media (NEXT-4, R20): with a per-cell (rho, K) array every
+Riemann problem is re-solved as a 2x2 linear system (numpy.linalg.solve) in
+the eigenvectors of the two media involved -- the left-going wave in the
+left cell's medium, the right-going one in the right cell's; for the
+transverse split, the down-going part in the medium of the cell below, the
+up-going part in the medium of the cell above -- instead of the closed forms
+the C oracle uses.
 """
 from __future__ import annotations
 
@@ -75,12 +83,48 @@ def transverse(ixy, asdq, rho, K):
     return -c * b1 * r1, c * b2 * r2
 
 
+def riemann_vc(ixy, ql, qr, medl, medr):
+    """Waves and speeds at an interface between media medl, medr = (rho, K):
+    dq = a1 r1(left medium) + a2 r2(right medium) on the (p, normal) block."""
+    cl, _, mu, _, r1, _ = _eig(ixy, *medl)
+    cr, _, _, _, _, r2 = _eig(ixy, *medr)
+    dq = qr - ql
+    a = np.linalg.solve(np.array([[r1[0], r2[0]], [r1[mu], r2[mu]]]), np.array([dq[0], dq[mu]]))
+    return np.array([a[0] * r1, a[1] * r2]), np.array([-cl, cr])
+
+
+def transverse_vc(ixy, asdq, med_lo, med, med_hi):
+    """asdq entering a cell of medium `med`, split by the Riemann problems
+    across its low / high edges in the other direction (transmitted parts)."""
+    other = 2 if ixy == 1 else 1
+    c_lo, _, mu, _, r1_lo, _ = _eig(other, *med_lo)
+    _, _, _, _, r1_c, r2_c = _eig(other, *med)
+    c_hi, _, _, _, _, r2_hi = _eig(other, *med_hi)
+    rhs = np.array([asdq[0], asdq[mu]])
+    a_lo = np.linalg.solve(np.array([[r1_lo[0], r2_c[0]], [r1_lo[mu], r2_c[mu]]]), rhs)[0]
+    a_hi = np.linalg.solve(np.array([[r1_c[0], r2_hi[0]], [r1_c[mu], r2_hi[mu]]]), rhs)[1]
+    return -c_lo * a_lo * r1_lo, c_hi * a_hi * r2_hi
+
+
 class BruteStep:
-    def __init__(self, qpad, dx, dy, dt, rho, K, limiter, order_trans):
+    def __init__(self, qpad, dx, dy, dt, rho, K, limiter, order_trans, auxpad=None):
         self.Q = _Cell(qpad)
+        self.aux = auxpad            # [2][my+4][mx+4] (rho, K) or None
         self.dx, self.dy, self.dt = dx, dy, dt
         self.rho, self.K = rho, K
         self.lim, self.ot = limiter, order_trans
+
+    def med(self, i, j):
+        if self.aux is None:
+            return (self.rho, self.K)
+        return (float(self.aux[0, j + 1, i + 1]), float(self.aux[1, j + 1, i + 1]))
+
+    def _riemann(self, ixy, i, j):
+        ql, qr = self._states(ixy, i, j)
+        if self.aux is None:
+            return riemann(ixy, ql, qr, self.rho, self.K)
+        lo = (i - 1, j) if ixy == 1 else (i, j - 1)
+        return riemann_vc(ixy, ql, qr, self.med(*lo), self.med(i, j))
 
     def _states(self, ixy, i, j):
         """(left, right) states at interface (i,j) of direction ixy: the edge
@@ -90,11 +134,11 @@ class BruteStep:
         return self.Q(i, j - 1), self.Q(i, j)
 
     def fluct(self, ixy, i, j):
-        W, s = riemann(ixy, *self._states(ixy, i, j), self.rho, self.K)
+        W, s = self._riemann(ixy, i, j)
         return s[0] * W[0], s[1] * W[1]  # A-dQ, A+dQ
 
     def limited(self, ixy, i, j):
-        W, s = riemann(ixy, *self._states(ixy, i, j), self.rho, self.K)
+        W, s = self._riemann(ixy, i, j)
         if self.lim == 0:
             return W, s
         out = W.copy()
@@ -104,7 +148,7 @@ class BruteStep:
                 continue
             step = -1 if s[p] > 0 else 1  # upwind neighbour interface
             ii, jj = (i + step, j) if ixy == 1 else (i, j + step)
-            Wup, _ = riemann(ixy, *self._states(ixy, ii, jj), self.rho, self.K)
+            Wup, _ = self._riemann(ixy, ii, jj)
             out[p] = _phi(self.lim, float(Wup[p] @ W[p]) / nrm) * W[p]
         return out, s
 
@@ -134,7 +178,11 @@ class BruteStep:
         dtdn = self.dt / (self.dx if ixy == 1 else self.dy)
         tot = np.zeros(3)
         for a in self._split_in(ixy, i, j):
-            down, up = transverse(ixy, a, self.rho, self.K)
+            if self.aux is None:
+                down, up = transverse(ixy, a, self.rho, self.K)
+            else:
+                lo, hi = ((i, j - 1), (i, j + 1)) if ixy == 1 else ((i - 1, j), (i + 1, j))
+                down, up = transverse_vc(ixy, a, self.med(*lo), self.med(i, j), self.med(*hi))
             tot = tot - 0.5 * dtdn * (down if side == 0 else up)
         return tot
 
@@ -165,11 +213,13 @@ def pad(q: np.ndarray, bc: str = "edge") -> np.ndarray:
     return np.pad(q, ((0, 0), (2, 2), (2, 2)), mode=bc)
 
 
-def brute_step(q, dx, dy, dt, rho=1.0, K=1.0, limiter=4, order_trans=2, bc="edge"):
-    """One step on a single patch (= the whole domain) of shape [3][my][mx]."""
+def brute_step(q, dx, dy, dt, rho=1.0, K=1.0, limiter=4, order_trans=2, bc="edge", aux=None):
+    """One step on a single patch (= the whole domain) of shape [3][my][mx];
+    aux: per-cell media [2][my][mx] (rho, K) or None (constant rho, K)."""
     _, my, mx = q.shape
     assert mx <= 16 and my <= 16, "brute force is for tiny patches"
-    b = BruteStep(pad(q, bc), dx, dy, dt, rho, K, limiter, order_trans)
+    b = BruteStep(pad(q, bc), dx, dy, dt, rho, K, limiter, order_trans,
+                  None if aux is None else pad(aux, bc))
     out = np.empty_like(q)
     for j in range(1, my + 1):
         for i in range(1, mx + 1):

@@ -53,6 +53,7 @@ typedef struct {
   double** qpad;  /* current time level, padded [3][my+4][mx+4] */
   double** qold;  /* previous time level, interior [3][my][mx] */
   double* pcfl;   /* per-patch max Courant number of the last step */
+  double** auxpad; /* variable media (oracle_set_aux), padded [2][my+4][mx+4] rho, K; NULL: per-patch constants */
   double dx, dy;
   int64_t nx, ny; /* level index extent of the domain */
   int ratio_to_coarser; /* R_{L-1}; 0 for level 1 */
@@ -141,6 +142,65 @@ void oracle_rpt2(int ixy, const double* asdq, double rho, double K,
   bpasdq[mv] = cc * a2;
 }
 
+/* ------------------------------------------------------------------------ */
+/* Variable-coefficient acoustics (NEXT-4; heterogeneous media P:66;   */
+/* per-system normal/transverse solvers P:433-436; R20).  Each cell */
+/* has its own rho, K (an aux array), so A and B of P:457-466 differ between  */
+/* the two sides of an interface.  The interface Riemann problem is solved   */
+/* with the eigenvectors of each side's own matrix: the left-going wave lives */
+/* in the left medium (speed -c_l, eigenvector (-Z_l, 1, 0)), the right-going */
+/* one in the right medium (+c_r, (Z_r, 1, 0)), and qr - ql = W1 + W2.         */
+/* ------------------------------------------------------------------------ */
+
+void oracle_rpn2_vc(int ixy, const double* ql, const double* qr, double rhol, double Kl,
+                    double rhor, double Kr, double* wave, double* s, double* amdq, double* apdq) {
+  const double cl = sqrt(Kl / rhol), zl = rhol * cl;
+  const double cr = sqrt(Kr / rhor), zr = rhor * cr;
+  const int mu = (ixy == 1) ? 1 : 2;
+  const int mv = (ixy == 1) ? 2 : 1;
+  const double delta1 = qr[0] - ql[0];
+  const double delta2 = qr[mu] - ql[mu];
+  /* solve  -a1 zl + a2 zr = delta1,  a1 + a2 = delta2 */
+  const double a1 = (-delta1 + zr * delta2) / (zl + zr);
+  const double a2 = (delta1 + zl * delta2) / (zl + zr);
+  wave[0 * MEQN + 0] = -a1 * zl;
+  wave[0 * MEQN + mu] = a1;
+  wave[0 * MEQN + mv] = 0.0;
+  s[0] = -cl;
+  wave[1 * MEQN + 0] = a2 * zr;
+  wave[1 * MEQN + mu] = a2;
+  wave[1 * MEQN + mv] = 0.0;
+  s[1] = cr;
+  for (int m = 0; m < MEQN; ++m) {
+    amdq[m] = s[0] * wave[0 * MEQN + m];
+    apdq[m] = s[1] * wave[1 * MEQN + m];
+  }
+}
+
+/* Transverse split of asdq, which enters a cell with medium (rho, K), into a
+ * part going to the cell below it in the transverse direction (rho_m, K_m) and
+ * a part going to the cell above (rho_p, K_p).  Each part is the transmitted
+ * wave of the Riemann problem across that transverse edge with jump asdq:
+ * below:  asdq = a1 (-Z_m, 0, 1) + b (Z, 0, 1)    -> B-asdq = -c_m a1 (-Z_m, 0, 1)
+ * above:  asdq = b (-Z, 0, 1) + a2 (Z_p, 0, 1)    -> B+asdq = +c_p a2 (Z_p, 0, 1)
+ * (components written for ixy = 1, i.e. the transverse velocity is v). */
+void oracle_rpt2_vc(int ixy, const double* asdq, double rho_m, double K_m, double rho, double K,
+                    double rho_p, double K_p, double* bmasdq, double* bpasdq) {
+  const int mu = (ixy == 1) ? 1 : 2;
+  const int mv = (ixy == 1) ? 2 : 1;
+  const double cm = sqrt(K_m / rho_m), zm = rho_m * cm;
+  const double cc = sqrt(K / rho), zz = rho * cc;
+  const double cp = sqrt(K_p / rho_p), zp = rho_p * cp;
+  const double a1 = (-asdq[0] + zz * asdq[mv]) / (zm + zz);
+  const double a2 = (asdq[0] + zz * asdq[mv]) / (zz + zp);
+  bmasdq[0] = cm * a1 * zm;
+  bmasdq[mu] = 0.0;
+  bmasdq[mv] = -cm * a1;
+  bpasdq[0] = cp * a2 * zp;
+  bpasdq[mu] = 0.0;
+  bpasdq[mv] = cp * a2;
+}
+
 /* Wave limiter function phi(theta) (P:501 names van Leer; BASELINE configs use
  * MC and minmod).  Clawpack numbering. */
 double oracle_philim(int limiter, double r) {
@@ -167,7 +227,9 @@ double oracle_philim(int limiter, double r) {
 /*   gadd[k][m][i]              i = 0..n+1   (k=0: B^- part -> edge of cell  */
 /*                              i at the "low" transverse side, k=1: high)   */
 /* ------------------------------------------------------------------------ */
-static void flux2(int ixy, int n, const double* q1d, double dtdx, double rho,
+/* aux1d (variable media, else NULL): [r][k][i+1], r = 0 the slice below in the
+ * transverse direction, 1 this slice, 2 the slice above; k = 0 rho, 1 K. */
+static void flux2(int ixy, int n, const double* q1d, const double* aux1d, double dtdx, double rho,
                   double K, int limiter, int order_trans, double* faddm,
                   double* faddp, double* gadd, double* cfl1d) {
   const int W = n + 4; /* stride of every per-slice array */
@@ -185,6 +247,7 @@ static void flux2(int ixy, int n, const double* q1d, double dtdx, double rho,
 #define AM(m, i) amdq[(m) * W + (i) + 1]
 #define AP(m, i) apdq[(m) * W + (i) + 1]
 #define CQ(m, i) cqxx[(m) * W + (i) + 1]
+#define AUX(r, k, i) aux1d[((r) * 2 + (k)) * W + (i) + 1]
 
   for (int m = 0; m < MEQN; ++m)
     for (int i = -1; i <= n + 2; ++i) {
@@ -201,7 +264,11 @@ static void flux2(int ixy, int n, const double* q1d, double dtdx, double rho,
       ql[m] = Q1(m, i - 1);
       qr[m] = Q1(m, i);
     }
-    oracle_rpn2(ixy, ql, qr, rho, K, wv, sp, am, ap);
+    if (aux1d)
+      oracle_rpn2_vc(ixy, ql, qr, AUX(1, 0, i - 1), AUX(1, 1, i - 1), AUX(1, 0, i), AUX(1, 1, i),
+                     wv, sp, am, ap);
+    else
+      oracle_rpn2(ixy, ql, qr, rho, K, wv, sp, am, ap);
     for (int mw = 0; mw < MWAVES; ++mw) {
       S(mw, i) = sp[mw];
       for (int m = 0; m < MEQN; ++m) WAVE(mw, m, i) = wv[mw * MEQN + m];
@@ -274,13 +341,21 @@ static void flux2(int ixy, int n, const double* q1d, double dtdx, double rho,
     for (int i = 1; i <= n + 1; ++i) {
       double asdq[MEQN], bm[MEQN], bp[MEQN];
       for (int m = 0; m < MEQN; ++m) asdq[m] = AM(m, i);
-      oracle_rpt2(ixy, asdq, rho, K, bm, bp);
+      if (aux1d) /* A-dq enters cell i-1 */
+        oracle_rpt2_vc(ixy, asdq, AUX(0, 0, i - 1), AUX(0, 1, i - 1), AUX(1, 0, i - 1),
+                       AUX(1, 1, i - 1), AUX(2, 0, i - 1), AUX(2, 1, i - 1), bm, bp);
+      else
+        oracle_rpt2(ixy, asdq, rho, K, bm, bp);
       for (int m = 0; m < MEQN; ++m) {
         GADD(0, m, i - 1) = GADD(0, m, i - 1) - 0.5 * dtdx * bm[m];
         GADD(1, m, i - 1) = GADD(1, m, i - 1) - 0.5 * dtdx * bp[m];
       }
       for (int m = 0; m < MEQN; ++m) asdq[m] = AP(m, i);
-      oracle_rpt2(ixy, asdq, rho, K, bm, bp);
+      if (aux1d) /* A+dq enters cell i */
+        oracle_rpt2_vc(ixy, asdq, AUX(0, 0, i), AUX(0, 1, i), AUX(1, 0, i), AUX(1, 1, i),
+                       AUX(2, 0, i), AUX(2, 1, i), bm, bp);
+      else
+        oracle_rpt2(ixy, asdq, rho, K, bm, bp);
       for (int m = 0; m < MEQN; ++m) {
         GADD(0, m, i) = GADD(0, m, i) - 0.5 * dtdx * bm[m];
         GADD(1, m, i) = GADD(1, m, i) - 0.5 * dtdx * bp[m];
@@ -301,6 +376,7 @@ static void flux2(int ixy, int n, const double* q1d, double dtdx, double rho,
 #undef AM
 #undef AP
 #undef CQ
+#undef AUX
 }
 
 /* ------------------------------------------------------------------------ */
@@ -310,10 +386,12 @@ static void flux2(int ixy, int n, const double* q1d, double dtdx, double rho,
  * edge arrays fm, fp, gm, gp (each [3][my+4][mx+4], padded index = Clawpack
  * index + 1; the caller frees them) -- the conservation fix reads the ones on
  * coarse-fine interfaces ("can be saved ... for later use"). */
-static int step2(int mx, int my, const double* qpad, double dx, double dy,
+/* auxpad (variable media, else NULL): [2][my+4][mx+4] rho, K with the ghost
+ * frame filled (oracle_set_aux); then rho and K are not used. */
+static int step2(int mx, int my, const double* qpad, const double* auxpad, double dx, double dy,
                  double dt, double rho, double K, int limiter, int order_trans,
                  double* qout_pad, double* cfl_out, double** flux_out) {
-  if (mx < 1 || my < 1 || !(dx > 0.0) || !(dy > 0.0) || !(rho > 0.0) || !(K > 0.0))
+  if (mx < 1 || my < 1 || !(dx > 0.0) || !(dy > 0.0) || (!auxpad && (!(rho > 0.0) || !(K > 0.0))))
     return -1;
   const int PX = mx + 4, PY = my + 4;
   const size_t plane = (size_t)PX * PY;
@@ -332,6 +410,8 @@ static int step2(int mx, int my, const double* qpad, double dx, double dy,
   double* faddm = (double*)calloc((size_t)MEQN * NMAX, sizeof(double));
   double* faddp = (double*)calloc((size_t)MEQN * NMAX, sizeof(double));
   double* gadd = (double*)calloc((size_t)2 * MEQN * NMAX, sizeof(double));
+  double* aux1d = auxpad ? (double*)calloc((size_t)3 * 2 * NMAX, sizeof(double)) : NULL;
+#define AP_(k, i, j) auxpad[(k) * plane + (size_t)((j) + 1) * PX + (i) + 1]
   double cfl = 0.0, cfl1d;
 
   /* x-sweeps: rows j = 0..my+1 */
@@ -340,7 +420,11 @@ static int step2(int mx, int my, const double* qpad, double dx, double dy,
   for (int j = 0; j <= my + 1; ++j) {
     for (int m = 0; m < MEQN; ++m)
       for (int i = -1; i <= mx + 2; ++i) q1d[m * WX + i + 1] = QP(m, i, j);
-    flux2(1, mx, q1d, dtdx, rho, K, limiter, order_trans, faddm, faddp, gadd, &cfl1d);
+    if (aux1d) /* media of rows j-1, j, j+1 */
+      for (int r = 0; r < 3; ++r)
+        for (int k = 0; k < 2; ++k)
+          for (int i = -1; i <= mx + 2; ++i) aux1d[(r * 2 + k) * WX + i + 1] = AP_(k, i, j - 1 + r);
+    flux2(1, mx, q1d, aux1d, dtdx, rho, K, limiter, order_trans, faddm, faddp, gadd, &cfl1d);
     cfl = fmax(cfl, cfl1d);
     for (int i = 1; i <= mx + 1; ++i)
       for (int m = 0; m < MEQN; ++m) {
@@ -359,7 +443,11 @@ static int step2(int mx, int my, const double* qpad, double dx, double dy,
   for (int i = 0; i <= mx + 1; ++i) {
     for (int m = 0; m < MEQN; ++m)
       for (int j = -1; j <= my + 2; ++j) q1d[m * WY + j + 1] = QP(m, i, j);
-    flux2(2, my, q1d, dtdy, rho, K, limiter, order_trans, faddm, faddp, gadd, &cfl1d);
+    if (aux1d) /* media of columns i-1, i, i+1 */
+      for (int r = 0; r < 3; ++r)
+        for (int k = 0; k < 2; ++k)
+          for (int j = -1; j <= my + 2; ++j) aux1d[(r * 2 + k) * WY + j + 1] = AP_(k, i - 1 + r, j);
+    flux2(2, my, q1d, aux1d, dtdy, rho, K, limiter, order_trans, faddm, faddp, gadd, &cfl1d);
     cfl = fmax(cfl, cfl1d);
     for (int j = 1; j <= my + 1; ++j)
       for (int m = 0; m < MEQN; ++m) {
@@ -386,8 +474,9 @@ static int step2(int mx, int my, const double* qpad, double dx, double dy,
   } else {
     free(fm); free(fp); free(gm); free(gp);
   }
-  free(q1d); free(faddm); free(faddp); free(gadd);
+  free(q1d); free(faddm); free(faddp); free(gadd); free(aux1d);
   return 0;
+#undef AP_
 #undef QP
 #undef QN
 #undef FMA_
@@ -399,7 +488,14 @@ static int step2(int mx, int my, const double* qpad, double dx, double dy,
 int oracle_step_patch(int mx, int my, const double* qpad, double dx, double dy,
                       double dt, double rho, double K, int limiter,
                       int order_trans, double* qout_pad, double* cfl_out) {
-  return step2(mx, my, qpad, dx, dy, dt, rho, K, limiter, order_trans, qout_pad, cfl_out, NULL);
+  return step2(mx, my, qpad, NULL, dx, dy, dt, rho, K, limiter, order_trans, qout_pad, cfl_out, NULL);
+}
+
+int oracle_step_patch_vc(int mx, int my, const double* qpad, const double* auxpad, double dx,
+                         double dy, double dt, int limiter, int order_trans, double* qout_pad,
+                         double* cfl_out) {
+  if (!auxpad) return -1;
+  return step2(mx, my, qpad, auxpad, dx, dy, dt, 0.0, 0.0, limiter, order_trans, qout_pad, cfl_out, NULL);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -411,6 +507,9 @@ static void free_level(olevel* L) {
     for (int p = 0; p < L->npatch; ++p) free(L->qpad[p]);
   if (L->qold)
     for (int p = 0; p < L->npatch; ++p) free(L->qold[p]);
+  if (L->auxpad)
+    for (int p = 0; p < L->npatch; ++p) free(L->auxpad[p]);
+  free(L->auxpad);
   free(L->qpad); free(L->qold); free(L->desc); free(L->i0); free(L->j0);
   free(L->pcfl); free(L->bstart); free(L->blist);
   free(L->rcp); free(L->rli); free(L->rlj); free(L->rdir); free(L->rside);
@@ -550,6 +649,8 @@ static int set_level_impl(oracle_ctx* c, int level, int npatch, const oracle_pat
     return fail(c, -1, "bad arguments");
   if (level > 1 && c->lev[level - 1].npatch == 0)
     return fail(c, -2, "coarser level not set");
+  if (level > 1 && c->lev[1].auxpad)
+    return fail(c, -1, "variable media (oracle_set_aux) are single-level (DESIGN.md R20)");
   olevel* L = &c->lev[level];
   free_level(L);
   L->npatch = npatch;
@@ -730,6 +831,58 @@ int oracle_fill_ghost(oracle_ctx* c, int level, double t) {
   return 0;
 }
 
+/* Variable media (NEXT-4, R20): aux = [patch][2][my][mx] (rho, K per
+ * interior cell) for every patch of the single level 1.  The ghost frame of
+ * each patch's padded aux is filled once here by the same composite rule as q
+ * (BC map per axis, then the same-level cell); the medium does not
+ * change in time. */
+int oracle_set_aux(oracle_ctx* c, int level, const double* aux) {
+  if (!c || level != 1 || c->lev[1].npatch == 0 || !aux)
+    return fail(c, -1, "variable media need level 1 set and no finer level (DESIGN.md R20)");
+  if (c->lev[2].npatch != 0) return fail(c, -1, "variable media are single-level (DESIGN.md R20)");
+  olevel* L = &c->lev[1];
+  size_t off = 0;
+  for (int p = 0; p < L->npatch; ++p) {
+    const size_t n = (size_t)L->desc[p].mx * L->desc[p].my;
+    for (size_t k = 0; k < 2 * n; ++k)
+      if (!(aux[off + k] > 0.0) || !isfinite(aux[off + k])) return fail(c, -1, "rho, K must be finite and > 0");
+    off += 2 * n;
+  }
+  if (!L->auxpad) L->auxpad = (double**)calloc((size_t)(unsigned)L->npatch, sizeof(double*));
+  off = 0;
+  for (int p = 0; p < L->npatch; ++p) {
+    const int mx = L->desc[p].mx, my = L->desc[p].my;
+    const size_t plane = (size_t)(mx + 4) * (my + 4);
+    free(L->auxpad[p]);
+    L->auxpad[p] = (double*)calloc(2 * plane, sizeof(double));
+    for (int k = 0; k < 2; ++k)
+      for (int j = 0; j < my; ++j)
+        for (int i = 0; i < mx; ++i)
+          L->auxpad[p][k * plane + (size_t)(j + 2) * (mx + 4) + i + 2] = aux[off + ((size_t)k * my + j) * mx + i];
+    off += (size_t)2 * mx * my;
+  }
+  const int* bc = c->cfg.bc;
+  for (int p = 0; p < L->npatch; ++p) {
+    const int mx = L->desc[p].mx, my = L->desc[p].my;
+    const size_t plane = (size_t)(mx + 4) * (my + 4);
+    for (int j = -1; j <= my + 2; ++j)
+      for (int i = -1; i <= mx + 2; ++i) {
+        if (i >= 1 && i <= mx && j >= 1 && j <= my) continue;
+        const int64_t I = map_axis(L->i0[p] + i - 1, L->nx, bc[0], bc[1]);
+        const int64_t J = map_axis(L->j0[p] + j - 1, L->ny, bc[2], bc[3]);
+        const int src = find_patch(L, I, J);
+        if (src < 0) return fail(c, -6, "aux ghost cell with no same-level donor");
+        const oracle_patch_desc* sd = &L->desc[src];
+        const size_t splane = (size_t)(sd->mx + 4) * (sd->my + 4);
+        const int li = (int)(I - L->i0[src]), lj = (int)(J - L->j0[src]);
+        for (int k = 0; k < 2; ++k)
+          L->auxpad[p][k * plane + (size_t)(j + 1) * (mx + 4) + i + 1] =
+              L->auxpad[src][k * splane + (size_t)(lj + 2) * (sd->mx + 4) + li + 2];
+      }
+  }
+  return 0;
+}
+
 /* Edge-array entry (component m, Clawpack index i, j) of a patch's flux arrays. */
 static double edge(double* const* fl, int k, const oracle_patch_desc* d, int m, int i, int j) {
   const size_t plane = (size_t)(d->mx + 4) * (d->my + 4);
@@ -822,7 +975,7 @@ int oracle_advance_level(oracle_ctx* c, int level, double dt, double* cfl_max) {
     double* qn = (double*)malloc(MEQN * plane * sizeof(double));
     double cfl = 0.0;
     if (fl) fl[p] = (double**)calloc(4, sizeof(double*));
-    if (step2(mx, my, L->qpad[p], d->dx, d->dy, dt, d->rho, d->K,
+    if (step2(mx, my, L->qpad[p], L->auxpad ? L->auxpad[p] : NULL, d->dx, d->dy, dt, d->rho, d->K,
               c->cfg.limiter, c->cfg.order_trans, qn, &cfl, fl ? fl[p] : NULL) != 0) {
 #pragma omp atomic write
       status = -1;

@@ -155,6 +155,26 @@ void oracle_rpt2(int ixy, const double* asdq, double rho, double K,
                  double* bmasdq, double* bpasdq);
 double oracle_philim(int limiter, double r);
 
+/* Variable-coefficient acoustics (NEXT-4; heterogeneous media P:66, P:640;
+ * normal / transverse solvers per system P:433-436; R20).
+ * oracle_set_aux: per-cell media of the single level 1, aux =
+ *   [patch][2][my][mx] (rho, K), all > 0; ghost media by the composite rule
+ *   (BC map, same-level copy).  A finer level is then refused (-1).
+ * oracle_rpn2_vc: interface between a left cell (rhol, Kl) and a right cell
+ *   (rhor, Kr): W1 = a1 (-Z_l, 1, 0) at -c_l, W2 = a2 (Z_r, 1, 0) at +c_r
+ *   with qr - ql = W1 + W2.
+ * oracle_rpt2_vc: asdq entering a cell (rho, K) split into the transmitted
+ *   waves across its low (rho_m, K_m) and high (rho_p, K_p) transverse edges.
+ * oracle_step_patch_vc: one step with a padded aux [2][my+4][mx+4]. */
+int oracle_set_aux(oracle_ctx* ctx, int level, const double* aux);
+void oracle_rpn2_vc(int ixy, const double* ql, const double* qr, double rhol, double Kl,
+                    double rhor, double Kr, double* wave, double* s, double* amdq, double* apdq);
+void oracle_rpt2_vc(int ixy, const double* asdq, double rho_m, double K_m, double rho, double K,
+                    double rho_p, double K_p, double* bmasdq, double* bpasdq);
+int oracle_step_patch_vc(int mx, int my, const double* qpad, const double* auxpad, double dx,
+                         double dy, double dt, int limiter, int order_trans, double* qout_pad,
+                         double* cfl);
+
 #ifdef __cplusplus
 }
 #endif

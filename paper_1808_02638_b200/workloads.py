@@ -134,6 +134,83 @@ def level_offsets(descs: np.ndarray) -> np.ndarray:
 
 
 # ---------------------------------------------------------------------------
+# Heterogeneous media (NEXT-4 variable-coefficient acoustics, P:66, P:640;
+# DESIGN.md R20): per-cell (rho, K) arrays, [patch][2][my][mx] flat.
+# ---------------------------------------------------------------------------
+
+# Layers of the layered medium: (upper y bound, rho, K), bottom to top.  The
+# impedance jumps by up to 4x and the sound speed by 2x between layers.
+LAYERS = ((-0.5, 1.0, 1.0), (0.0, 2.0, 0.5), (0.5, 0.5, 2.0), (np.inf, 4.0, 4.0))
+
+
+def layered_medium(x, y):
+    """(rho, K) at points: horizontal layers LAYERS, plus a vertical inclusion
+    band 0.25 <= x < 0.5 with rho = 3, K = 0.75 (so the medium varies in both
+    directions)."""
+    y = np.asarray(y, dtype=np.float64) + np.zeros_like(x, dtype=np.float64)
+    x = np.asarray(x, dtype=np.float64) + np.zeros_like(y)
+    rho = np.empty_like(y)
+    K = np.empty_like(y)
+    lo = -np.inf
+    for top, r, k in LAYERS:
+        m = (y >= lo) & (y < top)
+        rho[m] = r
+        K[m] = k
+        lo = top
+    inc = (x >= 0.25) & (x < 0.5)
+    rho[inc] = 3.0
+    K[inc] = 0.75
+    return rho, K
+
+
+def media_field(descs: np.ndarray, fn=layered_medium, out: np.ndarray | None = None,
+                chunk: int = 4096) -> np.ndarray:
+    """(rho, K) = fn(x, y) at every cell centre of the level, flat
+    [patch][2][my][mx]."""
+    sizes = 2 * descs["mx"].astype(np.int64) * descs["my"]
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    if out is None:
+        out = np.zeros(int(offs[-1]))
+    uniform = (descs["mx"] == descs["mx"][0]).all() and (descs["my"] == descs["my"][0]).all()
+    if uniform:
+        mx, my = int(descs["mx"][0]), int(descs["my"][0])
+        view = out.reshape(len(descs), 2, my, mx)
+        ii = np.arange(mx) + 0.5
+        jj = np.arange(my) + 0.5
+        for s in range(0, len(descs), chunk):
+            d = descs[s:s + chunk]
+            x = d["xlower"][:, None, None] + ii[None, None, :] * d["dx"][:, None, None]
+            y = d["ylower"][:, None, None] + jj[None, :, None] * d["dy"][:, None, None]
+            view[s:s + chunk, 0], view[s:s + chunk, 1] = fn(x, y)
+    else:
+        for p, d in enumerate(descs):
+            mx, my = int(d["mx"]), int(d["my"])
+            X, Y = np.meshgrid(d["xlower"] + (np.arange(mx) + 0.5) * d["dx"],
+                               d["ylower"] + (np.arange(my) + 0.5) * d["dy"])
+            r, k = fn(X, Y)
+            out[offs[p]:offs[p + 1]] = np.concatenate([np.ravel(r), np.ravel(k)])
+    return out
+
+
+def random_media(descs: np.ndarray, seed: int, lo: float = 0.5, hi: float = 2.0) -> np.ndarray:
+    """i.i.d. uniform[lo, hi] rho and K per cell (numpy default_rng(seed))."""
+    n = 2 * int((descs["mx"].astype(np.int64) * descs["my"]).sum())
+    return np.random.default_rng(seed).uniform(lo, hi, n)
+
+
+def max_sound_speed(aux: np.ndarray, descs: np.ndarray) -> float:
+    """max sqrt(K / rho) over the cells of a flat media array (for dt0)."""
+    m = 0.0
+    off = 0
+    for p in range(len(descs)):
+        n = int(descs["mx"][p]) * int(descs["my"][p])
+        r, k = aux[off:off + n], aux[off + n:off + 2 * n]
+        m = max(m, float(np.sqrt(k / r).max()))
+        off += 2 * n
+    return m
+
+
+# ---------------------------------------------------------------------------
 # BASELINE.json configs
 # ---------------------------------------------------------------------------
 
@@ -157,6 +234,17 @@ def c5(patches_per_side: int = 256, mx: int = 64) -> Workload:
     return Workload(f"c5_{n*mx}sq_patches_{mx}x{mx}",
                     [Level(uniform_level(n, n, mx, mx))], steps=100,
                     note=f"{n*mx}^2 cells as {n}x{n} patches of {mx}x{mx}")
+
+
+def c5_layered(patches_per_side: int = 256, mx: int = 64) -> Workload:
+    """configs[4]'s layout (16,384^2 cells as 64x64 patches) in the layered
+    heterogeneous medium (NEXT-4, R20); ring pulse, MC, CFL 0.9 of
+    the fastest layer (c = 2)."""
+    n = patches_per_side
+    return Workload(f"c5vc_{n*mx}sq_patches_{mx}x{mx}_layered",
+                    [Level(uniform_level(n, n, mx, mx))], steps=100,
+                    note=f"{n*mx}^2 cells, layered medium (4 layers + inclusion), per-cell rho, K",
+                    extra={"media": layered_medium, "cmax": 2.0})
 
 
 def ragged_level(seed: int, nx: int = 40, ny: int = 36, max_w: int = 13) -> np.ndarray:
