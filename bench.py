@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Benchmark of the batched AMR-level advance (arXiv 1808.02638 hot path) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5|c4|c3|c2|c1]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5|c4|c3|c2|c1|paper|c5vc]
                     [--impl reference] [--no-cpu-baseline]
 
 One "step" = one level step of the whole hot path over the workload:
@@ -39,6 +39,7 @@ from paper_1808_02638_b200 import workloads as W  # noqa: E402
 
 LIMNAME = {0: "none", 1: "minmod", 2: "superbee", 3: "vanLeer", 4: "MC"}
 BYTES_PER_CELL = 48  # algorithmic: read q^n (3 x fp64) + write q^{n+1} (3 x fp64)
+BYTES_PER_CELL_VC = 64  # variable media: + read the cell's (Z, c) (2 x fp64)
 
 
 def env_int(k, d):
@@ -58,7 +59,8 @@ def measured_peaks():
 
 
 def workload(name: str) -> W.Workload:
-    return {"c1": W.c1, "c2": W.c2, "c3": W.c3, "c4": W.c4, "c5": W.c5, "paper": W.paper}[name]()
+    return {"c1": W.c1, "c2": W.c2, "c3": W.c3, "c4": W.c4, "c5": W.c5, "paper": W.paper,
+            "c5vc": W.c5_layered}[name]()
 
 
 def hierarchy_ratios(wl: W.Workload) -> list:
@@ -223,8 +225,11 @@ def oracle_sample(wl: W.Workload, budget_s: float = 12.0, steps_cap: int | None 
                       reflux=reflux and not uniform)
     if uniform:
         o.set_level(1, levels[0], q0)
+        if wl.extra.get("media"):
+            o.set_aux(1, W.media_field(levels[0], wl.extra["media"]))
+            desc += " (variable media)"
         cells = int((levels[0]["mx"].astype(np.int64) * levels[0]["my"]).sum())
-        dt = wl.cfl * float(d0["dx"][0])
+        dt = wl.dt0()
         n, t0 = 0, time.perf_counter()
         while True:
             o.fill_ghost(1, n * dt)
@@ -301,11 +306,15 @@ def oracle_workload_stepper(wl: W.Workload, cores: int, reflux: bool):
     d0 = wl.levels[0].descs
     if len(wl.levels) == 1:
         cells = int((d0["mx"].astype(np.int64) * d0["my"]).sum())
-        need = 24 * int(((d0["mx"].astype(np.int64) + 4) * (d0["my"] + 4)).sum()) + 2 * 24 * cells
+        media = wl.extra.get("media")
+        need = (24 + (16 if media else 0)) * int(((d0["mx"].astype(np.int64) + 4) * (d0["my"] + 4)).sum()) + \
+            (2 * 24 + (16 if media else 0)) * cells
         if need * 1.5 > mem_available_bytes():
             return None
         o = oracle.Oracle(wl.domain, wl.bc, wl.limiter, wl.order_trans, nthreads=cores)
         o.set_level(1, d0, W.ring_ic(d0))
+        if media:
+            o.set_aux(1, W.media_field(d0, media))
         dt = wl.dt0()
         n = [0]
 
@@ -422,7 +431,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5", "paper"])
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5", "paper", "c5vc"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -512,6 +521,13 @@ def main():
         W.ring_ic(mine, out=buf.numpy())
         g.set_level(L, lv.descs, buf)
         host_q.append(buf)
+        if wl.extra.get("media"):
+            # per-cell media of the whole level (problem description, set once)
+            if world > 1:
+                raise SystemExit("variable media (c5vc) are single-GPU in this version")
+            g.set_aux(L, W.media_field(lv.descs, wl.extra["media"]))
+    vc = bool(wl.extra.get("media"))
+    bpc = BYTES_PER_CELL_VC if vc else BYTES_PER_CELL
     dt = wl.dt0()
     dx1 = float(wl.levels[0].descs["dx"][0])
     regrid_ms = []
@@ -629,9 +645,9 @@ def main():
     # two -- interior and edge tiles -- when ranks overlap the halo exchange)
     advances = max(args.steps * sum(mult), 1)
     avg_ms = st["step_ms"] / advances
-    bytes_per_launch = BYTES_PER_CELL * cells_per_step_rank / max(1, sum(mult))  # per level-launch mean
+    bytes_per_launch = bpc * cells_per_step_rank / max(1, sum(mult))  # per level-launch mean
     if nlev == 1:
-        bytes_per_launch = BYTES_PER_CELL * cells_owned[0]
+        bytes_per_launch = bpc * cells_owned[0]
     achieved = bytes_per_launch / (avg_ms / 1000.0) / 1e9 if avg_ms > 0 else None
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_step_traffic.json")
@@ -646,9 +662,10 @@ def main():
             traffic = None
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-            "kernel": (f"step_grid_kernel<{LIMNAME[wl.limiter]},{wl.order_trans}>" if g.level_mode(1) == "grid" and nlev == 1
+            "kernel": (f"step_vc_kernel<{LIMNAME[wl.limiter]},{wl.order_trans}>" if vc else
+                       f"step_grid_kernel<{LIMNAME[wl.limiter]},{wl.order_trans}>" if g.level_mode(1) == "grid" and nlev == 1
                        else f"step_kernel<{LIMNAME[wl.limiter]},{wl.order_trans},uniform>"),
-            "bytes_per_cell": BYTES_PER_CELL,
+            "bytes_per_cell": bpc,
             "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,
             "kernel_share_of_step": (st["step_ms"] / ms) if ms > 0 else None,
             "peak_source": peak_src,
@@ -719,7 +736,8 @@ def main():
                "d2h_bytes_per_step": state_bytes / args.steps + 8 * sum(mult),
                "ms": ems, "wall_ms": wall,
                "what": "write_level (pinned host->device) + K x (fill_ghost + advance_level -> 8-byte cfl) "
-                       "+ read_level (device->pinned host), per rank, max over ranks"}
+                       "+ read_level (device->pinned host), per rank, max over ranks"
+                       + ("; the static medium is set once before (claw_set_aux, problem setup)" if vc else "")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -747,6 +765,8 @@ def main():
                            "patches": int(sum(len(lv.descs) for lv in wl.levels)),
                            "cells_per_step": total_cells_per_step, "limiter": wl.limiter, "order_trans": wl.order_trans,
                            "cfl": wl.cfl, "ic": "ring (Clawpack acoustics_2d_radial qinit)",
+                           "medium": "layered, per-cell rho and K (workloads.LAYERS + inclusion)" if vc
+                           else "homogeneous rho = K = 1",
                            "conservation_fix": bool(args.reflux and nlev > 1),
                            "regrid_every": args.regrid if nlev > 1 else 0,
                            "dynamic_hierarchy": dyn,

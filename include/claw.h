@@ -126,6 +126,27 @@ int claw_partition(int32_t npatch, const claw_patch_desc* descs, int32_t world,
 int claw_set_level(claw_ctx* ctx, int32_t level, int32_t npatch,
                    const claw_patch_desc* descs, const double* q0);
 
+/* Variable-coefficient acoustics (NEXT-4: heterogeneous media, P:66 and P:640;
+ * the per-system normal / transverse Riemann solvers of P:433-436 with the
+ * matrices A, B of P:457-466 varying from cell to cell; R20).
+ * aux = [patch][2][my][mx] fp64 (rho, K per interior cell, every value finite
+ * and > 0) for ALL npatch patches of the level, in global patch order, on
+ * every rank (the medium is part of the problem description, like the
+ * descriptors); copied during the call.  The library stores (Z = rho c,
+ * c = sqrt(K/rho)) per cell in device memory, 16 B per cell, next to q; ghost
+ * cells take their medium by the composite rule (BC map, same-level copy),
+ * exactly as q.  From then on claw_advance_level solves every face's Riemann
+ * problem with the two cells' own media (W1 at -c_l in the left medium, W2 at
+ * +c_r in the right one), splits transverse fluctuations with the media of
+ * the cells across each transverse edge, and returns the Courant number as the
+ * max over every swept face of max(c_l, c_r) dt/dx (dt/dy); the descriptors'
+ * rho, K are then ignored.  claw_patch_cfl gives each patch's max over its own
+ * faces.  Requirements (EINVAL otherwise): level 1 set as one uniform grid of
+ * equal patches covering the domain (claw_level_mode 1), world = 1, no finer
+ * level; a later claw_set_level(2..) or claw_regrid is refused while the
+ * medium is set, and claw_set_level(1) discards it. */
+int claw_set_aux(claw_ctx* ctx, int32_t level, const double* aux);
+
 /* Ghost fill at time t: same-level and physical-BC ghosts are read
  * by the step kernel straight from their donors' interiors; this call fills
  * the ghost cells that need work: space-time interpolation from level-1's two

@@ -35,7 +35,7 @@ EXPORTS = [
     "claw_level_mode", "claw_advance_hierarchy", "claw_halo_pack", "claw_halo_unpack",
     "claw_update_level", "claw_reflux_registers", "claw_level_extent", "claw_level_count",
     "claw_level_descs", "claw_flag", "claw_cluster", "claw_regrid", "claw_regrid_auto",
-    "claw_pool_stats", "claw_pool_trim", "claw_comm_info",
+    "claw_pool_stats", "claw_pool_trim", "claw_comm_info", "claw_set_aux",
 ]
 CLAW_HIER_UPDATE = 1
 
@@ -85,6 +85,7 @@ def load() -> ctypes.CDLL:
     L.claw_version.restype = ctypes.c_char_p
     L.claw_partition.argtypes = [i32, vp, i32, ctypes.POINTER(ctypes.c_int32)]
     L.claw_set_level.argtypes = [vp, i32, i32, vp, dp]
+    L.claw_set_aux.argtypes = [vp, i32, dp]
     L.claw_fill_ghost.argtypes = [vp, i32, d]
     L.claw_advance_level.argtypes = [vp, i32, d, dp]
     L.claw_advance_level_async.argtypes = [vp, i32, d]
@@ -283,6 +284,13 @@ class Claw:
         n = 3 * int((d["mx"].astype(np.int64) * d["my"].astype(np.int64)).sum())
         self._check(load().claw_set_level(self._h, level, len(d), d.ctypes.data,
                                           _host_f64(q0, n, "set_level q0")))
+
+    def set_aux(self, level: int, aux):
+        """Per-cell media of the level (claw_set_aux): aux = [patch][2][my][mx]
+        (rho, K) for ALL patches, flat float64 (2 * level cells doubles)."""
+        d = self._descs[level]
+        n = 2 * int((d["mx"].astype(np.int64) * d["my"].astype(np.int64)).sum())
+        self._check(load().claw_set_aux(self._h, level, _host_f64(_as_f64(aux), n, "set_aux aux")))
 
     def fill_ghost(self, level: int, t: float = 0.0):
         self._check(load().claw_fill_ghost(self._h, level, float(t)))

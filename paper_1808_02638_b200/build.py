@@ -9,7 +9,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libclaw.so")
 SOURCES = [os.path.join(PKG, "csrc", "claw_kernels.cu"), os.path.join(PKG, "csrc", "claw_host.cpp")]
-HEADERS = [os.path.join(PKG, "csrc", "claw_internal.h"), os.path.join(ROOT, "include", "claw.h")]
+HEADERS = [os.path.join(PKG, "csrc", "claw_internal.h"), os.path.join(PKG, "csrc", "claw_vc.cuh"),
+           os.path.join(ROOT, "include", "claw.h")]
 
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
               "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "-shared", "-Xptxas", "-warn-spills"]

@@ -379,6 +379,14 @@ struct Level {
   int gen = 0;           // level CFL slot generation (lcfl[gen] is the last step's)
   unsigned long long* hier = nullptr;  // coarse-step slot while claw_advance_hierarchy runs
 
+  // variable media (claw_set_aux; grid mode, single rank): (Z, c) per cell in
+  // q's patch layout, and per owned patch the max sound speed over its cells
+  // and 1-deep ghost frame (the cells its faces touch) for claw_patch_cfl
+  DevBuf<double> aux;
+  bool vc = false;
+  std::vector<double> vc_pcmax;
+  double last_r = 0.0, last_s = 0.0;  // dt/dx, dt/dy of the last step
+
   int npx = 0;
   int64_t ngrid_tiles = 0;
   int64_t ngrid_blocks = 0;   // row blocks of the band (grid mode)
@@ -1912,6 +1920,8 @@ int claw_set_level(claw_ctx* ctx, int32_t level, int32_t npatch, const claw_patc
   if (level > 1 && !ctx->lev[level - 1].set) return fail(ctx, CLAW_ESTATE, "level %d set before level %d", level, level - 1);
   if (level > 1 && ctx->cfg.world > 1)
     return fail(ctx, CLAW_EINVAL, "multi-level hierarchies are single-rank in this version (world=%d)", ctx->cfg.world);
+  if (level > 1 && ctx->lev[1].vc)
+    return fail(ctx, CLAW_EINVAL, "level %d: variable media (claw_set_aux) are single-level (DESIGN.md R20)", level);
   if (!ctx->host_only) CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   drop_graphs(ctx);
   for (int l = level; l <= kMaxLevel; ++l) {
@@ -1936,6 +1946,9 @@ int claw_set_level(claw_ctx* ctx, int32_t level, int32_t npatch, const claw_patc
     if (L.gapless) {
       CUDA_TRY(cudaMemcpy(L.q[0].p, q0, L.buf_elems * 8, cudaMemcpyHostToDevice));
     } else {
+      // alignment gaps between patches are never read; zero them so the
+      // whole-buffer copy below moves initialised bytes only
+      CUDA_TRY(cudaMemset(L.q[0].p, 0, L.buf_elems * 8));
       int64_t src = 0;
       for (size_t lp = 0; lp < L.owned.size(); ++lp) {
         const int64_t n = 3ll * L.hpatch[lp].mx * L.hpatch[lp].my;
@@ -1952,6 +1965,59 @@ int claw_set_level(claw_ctx* ctx, int32_t level, int32_t npatch, const claw_patc
   // non-blocking, so finish them before any kernel can read the level
   CUDA_TRY(cudaStreamSynchronize(nullptr));
   L.set = true;
+  return CLAW_OK;
+}
+
+int claw_set_aux(claw_ctx* ctx, int32_t level, const double* aux) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = check_level(ctx, level)) return rc;
+  Level& L = ctx->lev[level];
+  if (level != 1 || ctx->lev[2].set)
+    return fail(ctx, CLAW_EINVAL, "set_aux(level %d): variable media are single-level (level 1, no finer level)", level);
+  if (ctx->cfg.world != 1) return fail(ctx, CLAW_EINVAL, "set_aux: single rank only in this version (world=%d)", ctx->cfg.world);
+  if (!L.grid || L.sparse || L.band)
+    return fail(ctx, CLAW_EINVAL, "set_aux: the level must be one uniform grid of equal patches (claw_level_mode 1)");
+  if (!aux) return fail(ctx, CLAW_EINVAL, "aux is NULL");
+  const int mx = L.desc[0].mx, my = L.desc[0].my;
+  const int64_t plane = static_cast<int64_t>(mx) * my;
+  const int64_t n = static_cast<int64_t>(L.npatch) * 2 * plane;
+  for (int64_t k = 0; k < n; ++k)
+    if (!(aux[k] > 0.0) || !std::isfinite(aux[k]))
+      return fail(ctx, CLAW_EINVAL, "aux: patch %lld %s at cell %lld is %g (must be finite and > 0)",
+                  static_cast<long long>(k / (2 * plane)), (k / plane) % 2 ? "K" : "rho",
+                  static_cast<long long>(k % plane), aux[k]);
+  // (Z, c) per cell, the oracle's operation order: c = sqrt(K / rho), Z = rho c
+  std::vector<double> zc(static_cast<size_t>(n));
+  std::vector<double> cl(static_cast<size_t>(L.nx * L.ny));   // c on the level index grid
+  for (int p = 0; p < L.npatch; ++p) {
+    const double* a = aux + static_cast<int64_t>(p) * 2 * plane;
+    double* o = zc.data() + static_cast<int64_t>(p) * 2 * plane;
+    for (int64_t k = 0; k < plane; ++k) {
+      const double c = std::sqrt(a[plane + k] / a[k]);
+      o[k] = a[k] * c;
+      o[plane + k] = c;
+      cl[static_cast<size_t>((L.j0[p] + k / mx) * L.nx + L.i0[p] + k % mx)] = c;
+    }
+  }
+  // per patch: max c over its cells and 1-deep ghost frame (BC-mapped)
+  const bool px = ctx->cfg.bc[0] == CLAW_BC_PERIODIC, py = ctx->cfg.bc[2] == CLAW_BC_PERIODIC;
+  auto mapi = [](int64_t I, int64_t nn, bool per) { return I < 0 ? (per ? I + nn : 0) : (I >= nn ? (per ? I - nn : nn - 1) : I); };
+  L.vc_pcmax.assign(L.owned.size(), 0.0);
+  for (size_t lp = 0; lp < L.owned.size(); ++lp) {
+    const int p = L.owned[lp];
+    double m = 0.0;
+    for (int64_t J = L.j0[p] - 1; J <= L.j0[p] + my; ++J)
+      for (int64_t I = L.i0[p] - 1; I <= L.i0[p] + mx; ++I)
+        m = std::max(m, cl[static_cast<size_t>(mapi(J, L.ny, py) * L.nx + mapi(I, L.nx, px))]);
+    L.vc_pcmax[lp] = m;
+  }
+  if (!ctx->host_only) {
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    drop_graphs(ctx);
+    CUDA_TRY(L.aux.alloc(static_cast<size_t>(n)));
+    CUDA_TRY(cudaMemcpy(L.aux.p, zc.data(), static_cast<size_t>(n) * 8, cudaMemcpyHostToDevice));
+  }
+  L.vc = true;
   return CLAW_OK;
 }
 
@@ -2094,6 +2160,11 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
       P.hoff[k] = L.hoff[k];
       P.hcs[k] = L.hcs[k];
     }
+  }
+  if (L.vc) {
+    P.aux = L.aux.p;
+    L.last_r = P.k.r;
+    L.last_s = P.k.s;
   }
   record(ctx, ctx->ev_step, true);
   if (ctx->cfg.world > 1) {
@@ -2290,6 +2361,15 @@ int claw_patch_cfl(claw_ctx* ctx, int32_t level, int32_t patch, double* cfl) {
   int lp;
   if (int rc = owned_index(ctx, level, patch, &lp)) return rc;
   if (!cfl) return fail(ctx, CLAW_EINVAL, "cfl is NULL");
+  const Level& Lv = ctx->lev[level];
+  if (Lv.vc) {
+    // variable media: max over the patch's faces of max(c_l, c_r) dt/dx (dt/dy)
+    // = max(dt/dx, dt/dy) times the max c over the cells those faces touch
+    // (its cells and 1-deep ghost frame); the medium is static
+    const double m = Lv.vc_pcmax[static_cast<size_t>(lp)];
+    *cfl = std::max(Lv.last_r * m, Lv.last_s * m);
+    return CLAW_OK;
+  }
   unsigned long long bits = 0;
   // grid mode: every patch shares dt, dx, dy and c, so its max Courant number
   // is the level's (the grid kernel only maintains the level slot)
@@ -2931,6 +3011,7 @@ int claw_regrid(claw_ctx* ctx, int32_t level, int32_t nbox, const int32_t* boxes
   if (int rc = check_level(ctx, level)) return rc;
   if (level >= kMaxLevel) return fail(ctx, CLAW_EINVAL, "regrid: level %d has no finer level", level);
   if (ctx->cfg.world > 1) return fail(ctx, CLAW_EINVAL, "regridding is single-rank in this version");
+  if (ctx->lev[1].vc) return fail(ctx, CLAW_EINVAL, "regrid: variable media (claw_set_aux) are single-level (DESIGN.md R20)");
   if (nbox < 0 || (nbox > 0 && !boxes) || R < 1) return fail(ctx, CLAW_EINVAL, "regrid: nbox=%d R=%d", nbox, R);
   Level& C = ctx->lev[level];
   for (int b = 0; b < nbox; ++b) {
@@ -3035,6 +3116,7 @@ int claw_regrid(claw_ctx* ctx, int32_t level, int32_t nbox, const int32_t* boxes
   P.per_x = ctx->cfg.bc[0] == CLAW_BC_PERIODIC;
   P.per_y = ctx->cfg.bc[2] == CLAW_BC_PERIODIC;
   P.err = err.p;
+  if (!L.gapless) CUDA_TRY(cudaMemsetAsync(L.q[0].p, 0, L.buf_elems * 8, ctx->stream));  // alignment gaps
   CUDA_TRY(static_cast<cudaError_t>(claw::launch_regrid(P, static_cast<int32_t>(L.owned.size()), ctx->stream)));
   int32_t herr = 0;
   CUDA_TRY(cudaMemcpyAsync(&herr, err.p, 4, cudaMemcpyDeviceToHost, ctx->stream));

@@ -54,9 +54,10 @@ class Workload:
     extra: dict = field(default_factory=dict)
 
     def dt0(self) -> float:
-        """dt = nu * min(dx, dy) / c on the coarsest level (eq:cfl)."""
+        """dt = nu * min(dx, dy) / c on the coarsest level (eq:cfl, P:284-287);
+        c = the fastest sound speed of a heterogeneous medium (extra["cmax"])."""
         d = self.levels[0].descs
-        c = math.sqrt(float(d["K"][0]) / float(d["rho"][0]))
+        c = self.extra.get("cmax") or math.sqrt(float(d["K"][0]) / float(d["rho"][0]))
         return self.cfl * min(float(d["dx"][0]), float(d["dy"][0])) / c
 
 

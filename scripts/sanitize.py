@@ -18,7 +18,10 @@ what = sys.argv[1:] or ["grid", "generic", "hier", "regrid"]
 
 if "grid" in what:
     for d, bc in ((W.c1().levels[0].descs, W.EXTRAP), (W.uniform_level(8, 8, 32, 32), W.PERIODIC)):
-        g = binding.Claw(W.DOMAIN, bc, 4, 2, device=0, tile_rows=128 if len(d) > 1 else 0)
+        if len(d) > 1:
+            os.environ["CLAW_GRID_TH"] = "128"   # tiles spanning patch rows
+        g = binding.Claw(W.DOMAIN, bc, 4, 2, device=0)
+        os.environ.pop("CLAW_GRID_TH", None)
         g.set_level(1, d, W.random_ic(d, 1))
         for n in range(3):
             g.fill_ghost(1, 0.0)

@@ -192,3 +192,35 @@ def test_binding_rejects_bad_host_buffers_before_the_c_call():
         assert e.value.code == binding.CLAW_EINVAL
     for q in (np.zeros(n), torch.zeros(n, dtype=torch.float64)):
         assert binding._host_f64(q, n, "ok") is not None
+
+
+def test_set_aux_validation_host_only():
+    """claw_set_aux (variable media, R20): a uniform single-rank grid
+    level only, positive finite rho / K, single-level afterwards."""
+    d = W.uniform_level(2, 2, 8, 8)
+    g = host_ctx()
+    g.set_level(1, d)
+    assert g.level_mode(1) == "grid"
+    aux = W.random_media(d, 1)
+    bad = aux.copy()
+    bad[70] = -1.0
+    with pytest.raises(binding.ClawError) as e:
+        g.set_aux(1, bad)
+    assert e.value.code == binding.CLAW_EINVAL and "rho" in str(e.value) or "K" in str(e.value)
+    bad[70] = np.inf
+    with pytest.raises(binding.ClawError):
+        g.set_aux(1, bad)
+    with pytest.raises(binding.ClawError):
+        g.set_aux(1, aux[:-1])                 # wrong size (binding check)
+    g.set_aux(1, aux)
+    with pytest.raises(binding.ClawError) as e:  # no finer level under variable media
+        g.set_level(2, W.make_descs([4], [4], 8, 8, 2 / 32, 2 / 32))
+    assert e.value.code == binding.CLAW_EINVAL
+    g.close()
+    r = host_ctx()
+    rd = W.ragged_level(3, 20, 18, 7)
+    r.set_level(1, rd)
+    with pytest.raises(binding.ClawError) as e:  # not a uniform grid
+        r.set_aux(1, W.random_media(rd, 2))
+    assert e.value.code == binding.CLAW_EINVAL
+    r.close()
