@@ -40,6 +40,8 @@ extern "C" {
 #define CLAW_ECUDA (-4)      /* CUDA error (sticky) */
 #define CLAW_ENCCL (-5)      /* NCCL error or NCCL unavailable (sticky) */
 #define CLAW_ENEST (-6)      /* ghost cell with no same-level or coarse donor */
+#define CLAW_ENONFINITE (-7) /* claw_config.check_finite: a step produced NaN / Inf;
+                                not sticky (the state is left as computed) */
 #define CLAW_ENODEV (-8)     /* compute requested from a host-only (device = -1) context */
 
 #define CLAW_BC_EXTRAP 1     /* zero-order extrapolation, the paper's outflow BC */
@@ -87,6 +89,22 @@ typedef struct {
                                   P:151-225; R17).  Fine patches
                                   must be aligned to the coarser cells; single rank.
                                   See claw_update_level. */
+  int32_t check_finite;        /* 1: debug check -- after every level step a
+                                  reduction over the new state; claw_advance_level /
+                                  claw_wait_cfl / claw_advance_hierarchy then return
+                                  CLAW_ENONFINITE naming the level if any value is NaN or
+                                  Inf (costs one extra read of the level per step) */
+  void* arena;                 /* device memory of `device` the caller owns (e.g. a torch
+                                  tensor's storage), or NULL.  Given: EVERY device buffer of
+                                  this context (levels, tables, frames, scratch) is carved
+                                  from it by the library's pool rules (one big
+                                  allocation carved per patch/level instead of cudaMalloc
+                                  per patch); no cudaMalloc happens for the context and a
+                                  request that does not fit fails with CLAW_ENOMEM.  The
+                                  arena is borrowed: it must outlive claw_destroy and is
+                                  never freed by the library.  NULL: the library's own
+                                  process-wide cudaMalloc'ed pool (claw_pool_stats). */
+  uint64_t arena_bytes;        /* size of the arena in bytes */
   int32_t reserved[4];
 } claw_config;
 
@@ -102,10 +120,20 @@ typedef struct {
 
 typedef struct claw_ctx claw_ctx;
 
-/* Create a context: validates cfg (EINVAL), selects the device, creates or
- * adopts the stream, and for world > 1 joins the NCCL communicator (ENCCL). */
+/* Create a context for one AMR hierarchy on one device (the paper's GPU
+ * advance, P:316-352 / P:410-440, with its memory pool P:422-426): validates
+ * cfg (EINVAL, message via claw_last_error even on failure: *out is then a
+ * dead context to destroy), selects the device, creates or adopts the stream,
+ * adopts cfg->arena if given, and for world > 1 joins the NCCL communicator
+ * (ENCCL).  *out receives the context (owned by the caller until
+ * claw_destroy). */
 int claw_create(const claw_config* cfg, claw_ctx** out);
+/* Synchronise the context's stream and release everything it owns: device
+ * buffers go back to the pool (or the caller's arena), the stream (if the
+ * library created it), events and the NCCL communicator.  EINVAL for NULL. */
 int claw_destroy(claw_ctx* ctx);
+/* The message of the last failing call on ctx (a field / patch / level is
+ * named); valid until the next call on ctx.  Never NULL. */
 const char* claw_last_error(const claw_ctx* ctx);
 
 /* Deterministic owner map used by claw_set_level for `world` ranks: patches in
@@ -169,10 +197,16 @@ int claw_advance_level(claw_ctx* ctx, int32_t level, double dt, double* cfl_max)
 int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt);
 int claw_wait_cfl(claw_ctx* ctx, int32_t level, double* cfl_max);
 
-/* Interior of one owned patch, [3][my][mx] (EINVAL if not owned here). */
+/* The current time level q^n of one owned patch's interior (the
+ * patch's state; eq. (W)'s Q_ij), [3][my][mx] fp64 host array of
+ * 3*mx*my doubles the caller owns; synchronous (device->host copy, stream
+ * synchronised).  EINVAL: patch out of range or not owned here, NULL
+ * pointer; ESTATE: level not set.  claw_write is the inverse (host->device;
+ * the values become q^n of the next step; a test/helper entry). */
 int claw_read(claw_ctx* ctx, int32_t level, int32_t patch, double* q_out);
 int claw_write(claw_ctx* ctx, int32_t level, int32_t patch, const double* q_in);
-/* The owned patches' level array (see conventions above). */
+/* The owned patches' level array (see conventions above): the same for all
+ * owned patches of the level in one copy (the bench's e2e path). */
 int claw_read_level(claw_ctx* ctx, int32_t level, double* q_out);
 int claw_write_level(claw_ctx* ctx, int32_t level, const double* q_in);
 /* [3][my+4][mx+4]: the patch with its ghost frame exactly as the step kernel
@@ -181,6 +215,10 @@ int claw_read_padded(claw_ctx* ctx, int32_t level, int32_t patch, double* q_out)
 /* Per-patch max Courant number of the last step (owned patches). */
 int claw_patch_cfl(claw_ctx* ctx, int32_t level, int32_t patch, double* cfl);
 
+/* Which rank owns (advances, stores) patch `patch` of `level` under the
+ * claw_partition map (patches partitioned by cell-count balance, BASELINE
+ * north_star; the paper is single-GPU and cites multi-GPU AMR codes).
+ * Host-only lookup; EINVAL for a bad level / patch / NULL. */
 int claw_owner(const claw_ctx* ctx, int32_t level, int32_t patch, int32_t* rank);
 /* Kernel path chosen for a level: 0 generic ghost-table kernel, 1 grid kernel
  * (see claw_config.path), 2 grid kernel on a sparse lattice (a finer level of

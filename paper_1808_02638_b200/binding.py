@@ -23,7 +23,9 @@ LIB_PATH = os.environ.get("CLAW_LIB") or os.path.join(_PKG, "libclaw.so")
 
 CLAW_OK, CLAW_EINVAL, CLAW_ESTATE, CLAW_ENOMEM = 0, -1, -2, -3
 CLAW_ECUDA, CLAW_ENCCL, CLAW_ENEST, CLAW_ENODEV = -4, -5, -6, -8
-ERR_NAMES = {-1: "EINVAL", -2: "ESTATE", -3: "ENOMEM", -4: "ECUDA", -5: "ENCCL", -6: "ENEST", -8: "ENODEV"}
+ERR_NAMES = {-1: "EINVAL", -2: "ESTATE", -3: "ENOMEM", -4: "ECUDA", -5: "ENCCL", -6: "ENEST", -7: "ENONFINITE",
+             -8: "ENODEV"}
+CLAW_ENONFINITE = -7
 
 EXPORTS = [
     "claw_create", "claw_destroy", "claw_last_error", "claw_partition", "claw_set_level",
@@ -55,7 +57,8 @@ class ClawConfig(ctypes.Structure):
                 ("nccl_unique_id", ctypes.c_void_p), ("stream", ctypes.c_void_p),
                 ("tile_rows", ctypes.c_int32), ("path", ctypes.c_int32),
                 ("exchange", ctypes.c_int32), ("reflux", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 4)]
+                ("check_finite", ctypes.c_int32), ("arena", ctypes.c_void_p),
+                ("arena_bytes", ctypes.c_uint64), ("reserved", ctypes.c_int32 * 4)]
 
 
 class ClawStats(ctypes.Structure):
@@ -226,13 +229,26 @@ class Claw:
     def __init__(self, domain=(-1.0, 1.0, -1.0, 1.0), bc=(1, 1, 1, 1), limiter=4,
                  order_trans=2, device=0, rank=0, world=1, nccl_id: bytes | None = None,
                  stream: int | None = None, tile_rows: int = 0, path: int = 0, exchange: int = 0,
-                 reflux: bool = False):
+                 reflux: bool = False, check_finite: bool = False, arena=None):
+        """arena: None, or device memory the context carves every buffer from
+        (claw_config.arena): a CUDA torch tensor (kept referenced by this
+        object) or a (device pointer, bytes) pair."""
         L = load()
         self._idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None
+        self._arena = arena
+        if arena is None:
+            aptr, abytes = None, 0
+        elif hasattr(arena, "data_ptr"):
+            if arena.device.type != "cuda":
+                raise ClawError(CLAW_EINVAL, f"arena: tensor on {arena.device}, need a CUDA tensor")
+            aptr, abytes = arena.data_ptr(), arena.numel() * arena.element_size()
+        else:
+            aptr, abytes = int(arena[0]), int(arena[1])
         cfg = ClawConfig(*[float(v) for v in domain], (ctypes.c_int32 * 4)(*bc), int(limiter),
                          int(order_trans), int(device), int(rank), int(world),
                          ctypes.cast(self._idbuf, ctypes.c_void_p) if self._idbuf else None,
-                         stream, int(tile_rows), int(path), int(exchange), int(bool(reflux)))
+                         stream, int(tile_rows), int(path), int(exchange), int(bool(reflux)),
+                         int(bool(check_finite)), aptr, abytes)
         self._h = ctypes.c_void_p()
         rc = L.claw_create(ctypes.byref(cfg), ctypes.byref(self._h))
         if rc:
@@ -249,6 +265,7 @@ class Claw:
         if getattr(self, "_h", None):
             load().claw_destroy(self._h)
             self._h = None
+        self._arena = None   # the arena outlives claw_destroy (borrowed by the context)
 
     def __del__(self):
         try:

@@ -118,6 +118,13 @@ Nccl g_nccl;
 // beyond CLAW_POOL_LIMIT_MB (default 16384) of free memory go back to the
 // driver, and a failing cudaMalloc first returns every free chunk and retries.
 // ---------------------------------------------------------------------------
+// A context created with claw_config.arena (device memory the caller owns,
+// e.g. a torch tensor's storage) allocates from that arena only: the arena is
+// one borrowed chunk of its own key (device, arena id), carved by the same
+// best-fit / coalescing rules, never grown and never freed to the driver
+// (a request that does not fit fails with ENOMEM); the thread's current arena
+// is the one of the context whose API call is running (set by check_ctx).
+thread_local int64_t t_arena = 0;
 struct Pool {
   static constexpr size_t kGrain = 512;
   static constexpr size_t kChunk = size_t{1} << 30;  // first chunk (cudaMalloc of a chunk: 15-100 ms)
@@ -126,10 +133,13 @@ struct Pool {
     std::map<char*, size_t> free_at;       // free ranges by address
     std::multimap<size_t, char*> free_sz;  // the same by size (best fit)
     size_t free_bytes = 0;
+    bool borrowed = false;                 // a caller's arena: no growth, never cudaFree'd
   };
+  using Key = std::pair<int, int64_t>;     // (device, arena id; 0 = the library's own chunks)
   std::mutex mu;
-  std::map<int, Dev> devs;
-  std::unordered_map<void*, std::pair<int, size_t>> live;
+  std::map<Key, Dev> devs;
+  std::unordered_map<void*, std::pair<Key, size_t>> live;
+  int64_t next_arena = 1;
   size_t limit = 0;
   int64_t hits = 0, misses = 0;
   Pool() {
@@ -153,6 +163,7 @@ struct Pool {
     d.free_bytes += n;
   }
   void release_free_chunks(Dev& d, size_t keep) {
+    if (d.borrowed) return;
     for (auto it = d.chunks.begin(); it != d.chunks.end() && d.free_bytes > keep;) {
       auto f = d.free_at.find(it->first);
       if (f != d.free_at.end() && f->second == it->second) {  // chunk entirely free
@@ -170,8 +181,17 @@ struct Pool {
     if (e != cudaSuccess) return e;
     const size_t n = (std::max<size_t>(bytes, 1) + kGrain - 1) / kGrain * kGrain;
     std::lock_guard<std::mutex> g(mu);
-    Dev& d = devs[dev];
+    const Key key{dev, t_arena};
+    if (t_arena != 0 && devs.find(key) == devs.end()) {
+      *out = nullptr;
+      return cudaErrorInvalidValue;  // the arena lives on another device
+    }
+    Dev& d = devs[key];
     auto it = d.free_sz.lower_bound(n);
+    if (it == d.free_sz.end() && d.borrowed) {
+      *out = nullptr;
+      return cudaErrorMemoryAllocation;  // arena exhausted
+    }
     if (it == d.free_sz.end()) {
       // geometric growth (a new chunk at least as large as all chunks so far):
       // cudaMalloc of a few hundred MB costs 15-50 ms on B200, so a growing
@@ -207,9 +227,37 @@ struct Pool {
     const size_t fs = it->first;
     erase_free(d, p, fs);
     if (fs > n) insert_free(d, p + n, fs - n);
-    live[p] = {dev, n};
+    live[p] = {key, n};
     *out = p;
     return cudaSuccess;
+  }
+  // adopt [base, base + bytes) of device `dev` as a new arena; returns its id
+  int64_t add_arena(int dev, void* base, size_t bytes) {
+    std::lock_guard<std::mutex> g(mu);
+    char* b = static_cast<char*>(base);
+    const size_t skip = (kGrain - reinterpret_cast<uintptr_t>(b) % kGrain) % kGrain;
+    if (bytes <= skip + kGrain) return 0;
+    b += skip;
+    const size_t n = (bytes - skip) / kGrain * kGrain;
+    const int64_t id = next_arena++;
+    Dev& d = devs[Key{dev, id}];
+    d.borrowed = true;
+    d.chunks[b] = n;
+    insert_free(d, b, n);
+    return id;
+  }
+  // forget an arena (every buffer carved from it must have been released)
+  void remove_arena(int64_t id) {
+    std::lock_guard<std::mutex> g(mu);
+    for (auto it = devs.begin(); it != devs.end();)
+      it = (it->first.second == id) ? devs.erase(it) : std::next(it);
+  }
+  size_t arena_free(int64_t id) {
+    std::lock_guard<std::mutex> g(mu);
+    size_t f = 0;
+    for (auto& kv : devs)
+      if (kv.first.second == id) f += kv.second.free_bytes;
+    return f;
   }
   void release(void* vp) {
     std::lock_guard<std::mutex> g(mu);
@@ -246,7 +294,8 @@ struct Pool {
   }
   size_t cached() {
     size_t c = 0;
-    for (auto& kv : devs) c += kv.second.free_bytes;
+    for (auto& kv : devs)
+      if (!kv.second.borrowed) c += kv.second.free_bytes;
     return c;
   }
 };
@@ -462,6 +511,10 @@ struct claw_ctx {
   int alpha_n = 0;
   double* h_alpha = nullptr;   // pinned [kMaxAlpha], copied to d_alpha by the graph
   DevBuf<double> d_alpha;
+  int64_t arena_id = 0;        // claw_config.arena adopted by the pool (0: library chunks)
+  DevBuf<int32_t> nf_flag;     // claw_config.check_finite: non-finite flag of the last step
+  int32_t* h_nf = nullptr;     // pinned copy
+  int nf_level = 0;            // level whose step set it
 };
 
 namespace {
@@ -479,6 +532,10 @@ int fail(claw_ctx* c, int code, const char* fmt, ...) {
 }
 
 int cuda_fail(claw_ctx* c, cudaError_t e, const char* where) {
+  if (e == cudaErrorMemoryAllocation) {  // pool / arena exhausted: not sticky
+    cudaGetLastError();
+    return fail(c, CLAW_ENOMEM, "%s: out of device memory%s", where, c->arena_id ? " (arena full)" : "");
+  }
   c->dead = true;
   return fail(c, CLAW_ECUDA, "%s: %s", where, cudaGetErrorString(e));
 }
@@ -605,6 +662,10 @@ int validate_config(claw_ctx* c, const claw_config* cfg) {
     return fail(c, CLAW_EINVAL, "reflux: the conservation fix is single-rank in this version (world=%d)", cfg->world);
   if (cfg->tile_rows < 0 || cfg->tile_rows > claw::max_tile_rows())
     return fail(c, CLAW_EINVAL, "tile_rows=%d: must be 0..%d", cfg->tile_rows, claw::max_tile_rows());
+  if (cfg->check_finite != 0 && cfg->check_finite != 1)
+    return fail(c, CLAW_EINVAL, "check_finite=%d: must be 0 or 1", cfg->check_finite);
+  if (cfg->arena && (cfg->device < 0 || cfg->arena_bytes == 0))
+    return fail(c, CLAW_EINVAL, "arena needs a device context and arena_bytes > 0");
   return CLAW_OK;
 }
 
@@ -1730,8 +1791,19 @@ int alloc_level(claw_ctx* ctx, int level, Level& L) {
 
 int check_ctx(claw_ctx* c) {
   if (!c) return CLAW_EINVAL;
+  t_arena = c->arena_id;   // this call's allocations come from the context's arena, if any
   if (c->dead) return fail(c, CLAW_ECUDA, "context unusable after an earlier CUDA/NCCL error");
   return CLAW_OK;
+}
+
+// claw_config.check_finite: the flag the steps since the last read raised
+// (h_nf copied by the caller's synchronising read); ENONFINITE names the level
+int take_nonfinite(claw_ctx* ctx) {
+  if (!ctx->cfg.check_finite || *ctx->h_nf == 0) return CLAW_OK;
+  const int lv = *ctx->h_nf;
+  *ctx->h_nf = 0;
+  CUDA_TRY(cudaMemset(ctx->nf_flag.p, 0, 4));
+  return fail(ctx, CLAW_ENONFINITE, "non-finite value (NaN / Inf) in q after a step of level %d", lv);
 }
 
 int check_level(claw_ctx* c, int level) {
@@ -1837,6 +1909,22 @@ int claw_create(const claw_config* cfg, claw_ctx** out) {
   if (ctx->host_only) return CLAW_OK;
   CUDA_TRY(cudaSetDevice(cfg->device));
   CUDA_TRY(cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, cfg->device));
+  t_arena = 0;
+  if (cfg->arena) {
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, cfg->arena) != cudaSuccess || pa.type != cudaMemoryTypeDevice ||
+        pa.device != cfg->device) {
+      cudaGetLastError();
+      ctx->dead = true;
+      return fail(ctx, CLAW_EINVAL, "arena %p is not device memory of device %d", cfg->arena, cfg->device);
+    }
+    ctx->arena_id = pool().add_arena(cfg->device, cfg->arena, static_cast<size_t>(cfg->arena_bytes));
+    if (!ctx->arena_id) {
+      ctx->dead = true;
+      return fail(ctx, CLAW_EINVAL, "arena_bytes=%llu: too small", static_cast<unsigned long long>(cfg->arena_bytes));
+    }
+    t_arena = ctx->arena_id;
+  }
   if (cfg->stream) {
     ctx->stream = static_cast<cudaStream_t>(cfg->stream);
   } else {
@@ -1844,6 +1932,12 @@ int claw_create(const claw_config* cfg, claw_ctx** out) {
     ctx->own_stream = true;
   }
   CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_cfl), sizeof(double)));
+  if (cfg->check_finite) {
+    CUDA_TRY(ctx->nf_flag.alloc(1));
+    CUDA_TRY(cudaMemset(ctx->nf_flag.p, 0, 4));
+    CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_nf), sizeof(int32_t)));
+    *ctx->h_nf = 0;
+  }
   if (cfg->world > 1) {
     CUDA_TRY(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_ready, cudaEventDisableTiming));
@@ -1906,7 +2000,12 @@ int claw_destroy(claw_ctx* ctx) {
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
   if (ctx->ev_ready) cudaEventDestroy(ctx->ev_ready);
   if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
-  delete ctx;
+  ctx->nf_flag.reset();
+  if (ctx->h_nf) cudaFreeHost(ctx->h_nf);
+  const int64_t arena = ctx->arena_id;
+  delete ctx;                                  // (every buffer is back in the pool)
+  if (arena) pool().remove_arena(arena);
+  t_arena = 0;
   return CLAW_OK;
 }
 
@@ -2215,6 +2314,8 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
     if (P.side) ctx->stats.ghost_launches++;  // the side_kernel ahead of it
   }
   record(ctx, ctx->ev_step, false);
+  if (ctx->cfg.check_finite && !ctx->dry)  // debug check: every new value finite
+    CUDA_TRY(static_cast<cudaError_t>(claw::launch_nonfinite(P.qn, L.buf_elems, level, ctx->nf_flag.p, ctx->stream)));
   ctx->stats.cells_advanced += L.cells_owned;
   if (ctx->cfg.reflux) {
     // conservation fix: fine part of this level's registers (q^n of this level
@@ -2252,9 +2353,11 @@ int claw_wait_cfl(claw_ctx* ctx, int32_t level, double* cfl_max) {
   if (!cfl_max) return fail(ctx, CLAW_EINVAL, "cfl_max is NULL");
   Level& L = ctx->lev[level];
   CUDA_TRY(cudaMemcpyAsync(ctx->h_cfl, L.lcfl.p + L.gen, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (ctx->cfg.check_finite)
+    CUDA_TRY(cudaMemcpyAsync(ctx->h_nf, ctx->nf_flag.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   *cfl_max = *ctx->h_cfl;
-  return CLAW_OK;
+  return take_nonfinite(ctx);
 }
 
 int claw_advance_level(claw_ctx* ctx, int32_t level, double dt, double* cfl_max) {
@@ -2495,7 +2598,7 @@ int claw_advance_hierarchy(claw_ctx* ctx, double t, double dt, int32_t flags, do
   while (nlev < kMaxLevel && ctx->lev[nlev + 1].set) ++nlev;
   if (nlev == 0) return fail(ctx, CLAW_ESTATE, "no level set");
   if (!ctx->hier_buf.p) CUDA_TRY(ctx->hier_buf.alloc(1));
-  const bool graph = ctx->graphs_on && ctx->cfg.world == 1;
+  const bool graph = ctx->graphs_on && ctx->cfg.world == 1 && !ctx->cfg.check_finite;
   if (!graph) {
     CUDA_TRY(cudaMemsetAsync(ctx->hier_buf.p, 0, 8, ctx->stream));
     ctx->hier_slot = ctx->hier_buf.p;
@@ -2508,9 +2611,11 @@ int claw_advance_hierarchy(claw_ctx* ctx, double t, double dt, int32_t flags, do
       if (nr != ncclSuccess) return nccl_fail(ctx, nr, "ncclAllReduce(cfl, max)");
     }
     CUDA_TRY(cudaMemcpyAsync(ctx->h_cfl, ctx->hier_buf.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    if (ctx->cfg.check_finite)
+      CUDA_TRY(cudaMemcpyAsync(ctx->h_nf, ctx->nf_flag.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     *cfl_max = *ctx->h_cfl;
-    return CLAW_OK;
+    return take_nonfinite(ctx);
   }
   // CUDA-graph path: the whole coarse step -- every fill,
   // step, reflux and update launch -- is captured once per key and replayed;

@@ -114,6 +114,9 @@ struct InterpAlphas {
 };
 int launch_interp(const double* q_old, const double* q_new, const double* alphas, int nal, const double* alpha_dev,
                   const DevInterp* spec, int64_t n, double* frame, int64_t fcs, int64_t slice, void* stream);
+// debug check (claw_config.check_finite): atomicMax(flag, level) if any of
+// q[0..n) is NaN or +-Inf
+int launch_nonfinite(const double* q, int64_t n, int level, int32_t* flag, void* stream);
 int launch_pack(const double* q, const int64_t* off, const int64_t* cs, int64_t n,
                 double* out, void* stream);
 int launch_gather_padded(const double* q, const double* frame, const DevPatch* patches,

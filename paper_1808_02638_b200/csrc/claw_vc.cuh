@@ -88,20 +88,22 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
   vc_ptrs(P, Ca, j0, xq0, xa0);
   double (*ring)[5][34] = sq;
 
-  auto issue_ptr = [&](int sl, const double* g, const double* ga, const double* x, const double* xa) {
-    cp8(&ring[sl][XP][lane + 1], g);
-    cp8(&ring[sl][XU][lane + 1], g + cs);
-    cp8(&ring[sl][XV][lane + 1], g + 2 * cs);
-    cp8(&ring[sl][XZ][lane + 1], ga);
-    cp8(&ring[sl][XC][lane + 1], ga + cs);
-    cp8_pred(&ring[sl][XP][ax], x, edge);
-    cp8_pred(&ring[sl][XU][ax], x + cs, edge);
-    cp8_pred(&ring[sl][XZ][ax], xa, edge);
-    cp8_pred(&ring[sl][XC][ax], xa + cs, edge);
+  auto issue_ptr = [&](int sl, const double* g, const double* ga, const double* x, const double* xa, bool on) {
+    cp8_pred(&ring[sl][XP][lane + 1], g, on);
+    cp8_pred(&ring[sl][XU][lane + 1], g + cs, on);
+    cp8_pred(&ring[sl][XV][lane + 1], g + 2 * cs, on);
+    cp8_pred(&ring[sl][XZ][lane + 1], ga, on);
+    cp8_pred(&ring[sl][XC][lane + 1], ga + cs, on);
+    cp8_pred(&ring[sl][XP][ax], x, edge && on);
+    cp8_pred(&ring[sl][XU][ax], x + cs, edge && on);
+    cp8_pred(&ring[sl][XZ][ax], xa, edge && on);
+    cp8_pred(&ring[sl][XC][ax], xa + cs, edge && on);
     cp_commit();
   };
-  // general issue of row R (halo rows mapped by the BCs; clamped to rtop+1)
+  // general issue of row R (halo rows mapped by the BCs; rows past rtop + 1,
+  // never read for a stored cell, commit an empty group)
   auto issue = [&](int R) {
+    const bool on = R <= rtop + 1;
     R = min(R, rtop + 1);
     const int sl = (R - j0 + 2) & (kGRD - 1);
     const double *g, *ga, *x, *xa;
@@ -120,7 +122,7 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
       vc_ptrs(P, C, J, g, ga);
       vc_ptrs(P, Ca, J, x, xa);
     }
-    issue_ptr(sl, g, ga, x, xa);
+    issue_ptr(sl, g, ga, x, xa, on);
   };
   auto slot = [&](int R) { return (R - j0 + 2) & (kGRD - 1); };
 
@@ -146,14 +148,17 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
     cv[S] = ring[sl][XV][lane + 1];
   };
   // y-face F(k) between the cells in slots Sl (row k-1) and Su (row k)
-  auto yface = [&](int Sf, int Sl, int Su) {
+  // (live: the face / row belongs to the tile's stencil -- the unrolled march
+  // runs past the last row on ring slots that hold stale rows, whose speeds
+  // must not enter the Courant number)
+  auto yface = [&](int Sf, int Sl, int Su, bool live) {
     const double sg = vc_rcp(__dadd_rn(cZ[Sl], cZ[Su]));
     const double dp = __dsub_rn(cp_[Su], cp_[Sl]), dv = __dsub_rn(cv[Su], cv[Sl]);
     fa1[Sf] = __dmul_rn(sg, __fma_rn(cZ[Su], dv, -dp));
     fa2[Sf] = __dmul_rn(sg, __fma_rn(cZ[Sl], dv, dp));
     fm[Sf] = __fma_rn(cZ[Sl], cZ[Su], 1.0);
     fsg[Sf] = sg;
-    cmy = fmax(cmy, fmax(cc[Sl], cc[Su]));
+    if (live) cmy = fmax(cmy, fmax(cc[Sl], cc[Su]));
   };
   // limit y-face F(k): Sf its slot, Sl / Su its cells, Sd / Sup the faces
   // below / above (upwind of wave 2 / wave 1)
@@ -164,7 +169,7 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
     fqv[Sf] = __fma_rn(cey[Su], t2, __dmul_rn(cey[Sl], t1));
   };
   // x-sweep of the row in ring slot sl whose cell values sit in slot S
-  auto xsweep = [&](int S, int sl) {
+  auto xsweep = [&](int S, int sl, bool live) {
     const double p = ring[sl][XP][lane + 1], u = ring[sl][XU][lane + 1];
     const double pl = ring[sl][XP][lane], ul = ring[sl][XU][lane], Zl = ring[sl][XZ][lane];
     const double pr = ring[sl][XP][lane + 2], ur = ring[sl][XU][lane + 2], Zr = ring[sl][XZ][lane + 2];
@@ -172,7 +177,7 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
     const double Z = cZ[S], c = cc[S], K = cK[S];
     pk[S] = p;
     uk[S] = u;
-    cmx = fmax(cmx, fmax(cl, c));
+    if (live) cmx = fmax(cmx, fmax(cl, c));
     const double sL = vc_rcp(__dadd_rn(Zl, Z)), sR = vc_rcp(__dadd_rn(Z, Zr));
     const double dpl = __dsub_rn(p, pl), dul = __dsub_rn(u, ul);
     const double a1 = __dmul_rn(sL, __fma_rn(Z, dul, -dpl));
@@ -209,12 +214,12 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
   cell(3, slot(j0 - 1));
   cell(0, slot(j0));
   cell(1, slot(j0 + 1));
-  yface(3, 2, 3);   // F(j0-1)
-  yface(0, 3, 0);   // F(j0)
-  yface(1, 0, 1);   // F(j0+1)
+  yface(3, 2, 3, true);   // F(j0-1)
+  yface(0, 3, 0, true);   // F(j0)
+  yface(1, 0, 1, true);   // F(j0+1)
   ylimit(0, 3, 0, 3, 1);
-  xsweep(3, slot(j0 - 1));
-  xsweep(0, slot(j0));
+  xsweep(3, slot(j0 - 1), true);
+  xsweep(0, slot(j0), true);
   if (OT != 0) gedge(0, 3, 0);
   __syncwarp();
   issue(j0 + kGPD + 1);
@@ -240,7 +245,7 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
     }
     if (PH == 0 && span && jb != j0 && jb % myv == 0) o += jump_q;
     if (decltype(fastc)::value) {
-      issue_ptr((j + 2 + kGPD - j0 + 2) & (kGRD - 1), gq, ga, xq, xa);
+      issue_ptr((j + 2 + kGPD - j0 + 2) & (kGRD - 1), gq, ga, xq, xa, true);
     } else {
       issue(j + 2 + kGPD);
     }
@@ -251,10 +256,11 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
     cp_wait<kGPD>();
     __syncwarp();
     const int rs0 = slot(j), rs1 = slot(j + 1), rs2 = slot(j + 2);
+    const bool live = j < rtop;
     cell(S2, rs2);                    // row j+2
-    yface(S2, S1, S2);                // F(j+2)
+    yface(S2, S1, S2, live);          // F(j+2)
     ylimit(S1, S0, S1, S0, S2);       // F(j+1)
-    xsweep(S1, rs1);                  // row j+1
+    xsweep(S1, rs1, live);            // row j+1
     if (OT != 0) gedge(S1, S0, S1);   // G of F(j+1)
     // finalise row j
     const double K0 = cK[S0], c0v = cc[S0];

@@ -7,6 +7,8 @@ synccheck, initcheck); see scripts/gpu_sanitize.sh.
   hier     C3-shaped hierarchy (sparse-lattice grid kernel, interp_kernel,
            update kernels, reflux kernels) on a reduced C2 with reflux
   regrid   flag / dilate / sat / regrid kernels (claw_regrid_auto)
+  vc       step_vc_kernel (variable media): a small grid, spanning tiles, the
+           non-finite check
 """
 import os
 import sys
@@ -14,7 +16,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1808_02638_b200 import binding, workloads as W  # noqa: E402
 
-what = sys.argv[1:] or ["grid", "generic", "hier", "regrid"]
+what = sys.argv[1:] or ["grid", "generic", "hier", "regrid", "vc"]
 
 if "grid" in what:
     for d, bc in ((W.c1().levels[0].descs, W.EXTRAP), (W.uniform_level(8, 8, 32, 32), W.PERIODIC)):
@@ -77,3 +79,18 @@ if "regrid" in what:
     g.advance_hierarchy(0.0, wl.dt0(), update=True)
     g.close()
     print("regrid ok")
+
+if "vc" in what:
+    for d, th in ((W.uniform_level(3, 2, 16, 12), None), (W.uniform_level(4, 8, 24, 16), "64")):
+        if th:
+            os.environ["CLAW_GRID_TH"] = th
+        g = binding.Claw(W.DOMAIN, W.PERIODIC, 4, 2, device=0, check_finite=True)
+        os.environ.pop("CLAW_GRID_TH", None)
+        g.set_level(1, d, W.random_ic(d, 3))
+        g.set_aux(1, W.random_media(d, 3))
+        for n in range(3):
+            g.fill_ghost(1, 0.0)
+            g.advance_level(1, 0.3 * float(d["dy"][0]))
+        g.read_level(1)
+        g.close()
+    print("vc ok")
