@@ -220,8 +220,8 @@ struct Pool {
       insert_free(d, static_cast<char*>(c), cs);
       ++misses;
       it = d.free_sz.lower_bound(n);
-    } else {
-      ++hits;
+    } else if (!d.borrowed) {
+      ++hits;   // (hits / misses count the library's own chunks, not arenas)
     }
     char* p = it->second;
     const size_t fs = it->first;

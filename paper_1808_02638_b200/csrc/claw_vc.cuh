@@ -42,7 +42,19 @@ __device__ __forceinline__ void vc_ptrs(const StepParams& P, int C, int J, const
   a = P.aux + pid * 2 * plane + in;
 }
 
-__device__ __forceinline__ double vc_rcp(double x) { return __drcp_rn(x); }
+// 1/x for the positive, normal x of this kernel (impedance sums, Z^2 + 1):
+// the SFU's reciprocal estimate (~2^-22) and two Newton steps (error ~2^-88,
+// i.e. the last bit of the double), no special-case branch; the rounding may
+// differ from the correctly rounded __drcp_rn by one ulp (parity is by
+// tolerance, R20)
+__device__ __forceinline__ double vc_rcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = __fma_rn(-x, y, 1.0);
+  y = __fma_rn(y, e, y);
+  e = __fma_rn(-x, y, 1.0);
+  return __fma_rn(y, e, y);
+}
 
 template <int LIM, int OT>
 __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const StepParams P) {
@@ -158,7 +170,7 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
     fa2[Sf] = __dmul_rn(sg, __fma_rn(cZ[Sl], dv, dp));
     fm[Sf] = __fma_rn(cZ[Sl], cZ[Su], 1.0);
     fsg[Sf] = sg;
-    if (live) cmy = fmax(cmy, fmax(cc[Sl], cc[Su]));
+    if (live) cmy = dmax(cmy, dmax(cc[Sl], cc[Su]));
   };
   // limit y-face F(k): Sf its slot, Sl / Su its cells, Sd / Sup the faces
   // below / above (upwind of wave 2 / wave 1)
@@ -177,7 +189,7 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
     const double Z = cZ[S], c = cc[S], K = cK[S];
     pk[S] = p;
     uk[S] = u;
-    if (live) cmx = fmax(cmx, fmax(cl, c));
+    if (live) cmx = dmax(cmx, dmax(cl, c));
     const double sL = vc_rcp(__dadd_rn(Zl, Z)), sR = vc_rcp(__dadd_rn(Z, Zr));
     const double dpl = __dsub_rn(p, pl), dul = __dsub_rn(u, ul);
     const double a1 = __dmul_rn(sL, __fma_rn(Z, dul, -dpl));
@@ -189,7 +201,8 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
     const double t2 = Limiter<LIM>::apply(a2, __dmul_rn(a2u, __dmul_rn(mL, cnu[S])));
     const double ex = __dmul_rn(__dmul_rn(c, __fma_rn(-c, r, 1.0)), inv2ls);
     const double exZ = __dmul_rn(ex, Z);
-    const double exl = shfl_up(ex), exZl = shfl_up(exZ);
+    const double exl = __dmul_rn(__dmul_rn(cl, __fma_rn(-cl, r, 1.0)), inv2ls);  // the left cell's
+    const double exZl = __dmul_rn(exl, Zl);
     const double qp = __fma_rn(exZ, t2, -__dmul_rn(exZl, t1));   // 1/2 cq of the left face
     const double qu = __fma_rn(ex, t2, __dmul_rn(exl, t1));
     const double dqp = __dsub_rn(shfl_dn(qp), qp), dqu = __dsub_rn(shfl_dn(qu), qu);
@@ -275,7 +288,8 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
     double vn = __fma_rn(-sy, Vy, q0v);
     if (OT != 0) {
       const double Ty = (OT == 2) ? __fma_rn(2.0, dqy, __dmul_rn(K0, asy)) : __dmul_rn(K0, asy);
-      const double TyR = shfl_dn(Ty), KR = shfl_dn(K0), cR = shfl_dn(c0v);
+      const double TyR = shfl_dn(Ty);
+      const double cR = ring[rs0][XC][lane + 2], KR = __dmul_rn(cR, ring[rs0][XZ][lane + 2]);
       const double FpR = __dmul_rn(xsR[S0], __fma_rn(KR, Ty, -__dmul_rn(K0, TyR)));
       const double FuR = __dmul_rn(xsR[S0], __fma_rn(cR, Ty, __dmul_rn(c0v, TyR)));
       const double FpL = shfl_up(FpR), FuL = shfl_up(FuR);

@@ -125,7 +125,7 @@ def test_vc_degenerate_shapes():
 
 
 def test_vc_patch_cfl_matches_oracle():
-    d = W.uniform_level(4, 3, 10, 8)
+    d = W.uniform_level(4, 3, 16, 8)
     aux = W.random_media(d, 11, 0.2, 4.0)
     g, o = pair(d, W.random_ic(d, 11), aux)
     run(g, o, 2, dt_for(aux, d))
