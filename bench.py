@@ -443,6 +443,9 @@ def main():
                     help="multi-level configs: regrid every K coarse steps inside the timed region (NEXT-3; "
                          "claw_regrid_auto of levels 1..L-1, flag tol scaled by dx)")
     ap.add_argument("--regrid-tol", type=float, default=0.02)
+    ap.add_argument("--batch", type=int, default=10,
+                    help="fixed multi-level hierarchies: coarse steps per host synchronisation "
+                         "(claw_advance_hierarchy_n; 1 = one claw_advance_hierarchy call per coarse step)")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "host"],
                     help="host: TEST MODE -- halos through host memory over a gloo group "
                          "(claw exchange=1), ranks may share one GPU; never a bench number")
@@ -588,13 +591,29 @@ def main():
                 regrid(t + dt)
         t_sim[0] = t + dt
 
+    # fixed hierarchies (no regrid): K coarse steps per host synchronisation
+    # (claw_advance_hierarchy_n; the per-step CFLs come back together)
+    batch = nlev > 1 and not dyn and not args.regrid and args.batch > 1
+    cfl_seen = []
+
+    def steps(n):
+        if not batch:
+            for _ in range(n):
+                step()
+            return
+        done = 0
+        while done < n:
+            k = min(args.batch, n - done)
+            cfl_seen.extend(g.advance_hierarchy_n(t_sim[0], dt, k, update=True).tolist())
+            t_sim[0] += k * dt
+            done += k
+
     nwarm = max(args.warmup, 3) if args.warmup > 0 else 0
     if dyn and args.regrid and nwarm:
         # a dynamic hierarchy warms up through one regrid (its kernels, pool
         # chunks and host buffers), so the timed steps start in steady state
         nwarm = max(nwarm, args.regrid + 1)
-    for _ in range(nwarm):
-        step()
+    steps(nwarm)
     torch.cuda.synchronize()
 
     def barrier():
@@ -612,8 +631,7 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     regrid_ms.clear()
     ev0.record(stream)
-    for _ in range(args.steps):
-        step()
+    steps(args.steps)
     ev1.record(stream)
     barrier()
     clocks.stop()
@@ -718,8 +736,7 @@ def main():
         e0.record(stream)
         for L, b in enumerate(host_q, start=1):
             g.write_level(L, b)
-        for _ in range(args.steps):
-            step()
+        steps(args.steps)
         for L, b in enumerate(out_host, start=1):
             g.read_level(L, b)
         e1.record(stream)
@@ -773,6 +790,8 @@ def main():
                            "warmup_steps_run": nwarm,
                            "limiter_name": {0: "none", 1: "minmod", 2: "superbee", 3: "van Leer", 4: "MC"}[wl.limiter],
                            "regrids": len(regrid_ms),
+                           "coarse_steps_per_sync": args.batch if batch else 1,
+                           "cfl_max_seen": max(cfl_seen) if cfl_seen else None,
                            "regrid_ms_mean": statistics.mean(regrid_ms) if regrid_ms else None,
                            "patches_after": [len(g.descs(L)) for L in range(1, nlev + 1)] if nlev > 1 else None,
                            "parallelism": f"patch-partitioned over {world} rank(s), NCCL halo + max all-reduce"

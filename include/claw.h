@@ -260,6 +260,16 @@ int claw_reflux_registers(claw_ctx* ctx, int32_t level, int64_t* n, int32_t* edg
  * synchronisation at the end; *cfl_max receives the max Courant number over
  * all level steps.  Ratios are taken from the levels' dx. */
 int claw_advance_hierarchy(claw_ctx* ctx, double t, double dt, int32_t flags, double* cfl_max);
+/* nsteps consecutive coarse steps at the fixed dt (times t + k dt), each
+ * exactly as claw_advance_hierarchy would run it, with ONE host
+ * synchronisation at the end instead of one per coarse step: the launches of
+ * all steps are queued back to back, the per-step Courant numbers land in
+ * device slots (one memset for the batch) and cfl_out[k] (host array of
+ * nsteps doubles) receives the max Courant number of coarse step k.  The
+ * caller checks them afterwards (dt_next = dt nu / cfl; a step
+ * with cfl > 1 is to be retaken from saved data, as for the single-step
+ * call).  EINVAL: nsteps < 1 or cfl_out NULL. */
+int claw_advance_hierarchy_n(claw_ctx* ctx, double t, double dt, int32_t nsteps, int32_t flags, double* cfl_out);
 int claw_level_owned(const claw_ctx* ctx, int32_t level, int32_t* npatch_owned,
                      int64_t* cells_owned, int64_t* device_bytes);
 

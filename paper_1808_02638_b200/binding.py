@@ -37,7 +37,7 @@ EXPORTS = [
     "claw_level_mode", "claw_advance_hierarchy", "claw_halo_pack", "claw_halo_unpack",
     "claw_update_level", "claw_reflux_registers", "claw_level_extent", "claw_level_count",
     "claw_level_descs", "claw_flag", "claw_cluster", "claw_regrid", "claw_regrid_auto",
-    "claw_pool_stats", "claw_pool_trim", "claw_comm_info", "claw_set_aux",
+    "claw_pool_stats", "claw_pool_trim", "claw_comm_info", "claw_set_aux", "claw_advance_hierarchy_n",
 ]
 CLAW_HIER_UPDATE = 1
 
@@ -111,6 +111,7 @@ def load() -> ctypes.CDLL:
     L.claw_nccl_unique_id.argtypes = [vp]
     L.claw_level_mode.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_int32)]
     L.claw_advance_hierarchy.argtypes = [vp, d, d, i32, dp]
+    L.claw_advance_hierarchy_n.argtypes = [vp, d, d, i32, i32, dp]
     L.claw_update_level.argtypes = [vp, i32]
     L.claw_reflux_registers.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_int64), vp, vp]
     L.claw_level_extent.argtypes = [vp, i32, i64, i64]
@@ -385,6 +386,14 @@ class Claw:
         self._check(load().claw_advance_hierarchy(self._h, float(t), float(dt),
                                                   CLAW_HIER_UPDATE if update else 0, ctypes.byref(c)))
         return c.value
+
+    def advance_hierarchy_n(self, t: float, dt: float, nsteps: int, update: bool = False) -> np.ndarray:
+        """nsteps coarse steps at fixed dt with one host synchronisation;
+        returns the per-step max Courant numbers (claw_advance_hierarchy_n)."""
+        out = np.zeros(int(nsteps))
+        self._check(load().claw_advance_hierarchy_n(self._h, float(t), float(dt), int(nsteps),
+                                                    CLAW_HIER_UPDATE if update else 0, _dptr(out)))
+        return out
 
     def update_level(self, level: int):
         """Average `level` onto `level - 1` where fully covered (P:120-121);

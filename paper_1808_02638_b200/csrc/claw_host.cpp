@@ -511,6 +511,9 @@ struct claw_ctx {
   int alpha_n = 0;
   double* h_alpha = nullptr;   // pinned [kMaxAlpha], copied to d_alpha by the graph
   DevBuf<double> d_alpha;
+  DevBuf<unsigned long long> hier_many;  // claw_advance_hierarchy_n: one CFL slot per coarse step
+  double* h_many = nullptr;    // pinned copy
+  int h_many_n = 0;
   int64_t arena_id = 0;        // claw_config.arena adopted by the pool (0: library chunks)
   DevBuf<int32_t> nf_flag;     // claw_config.check_finite: non-finite flag of the last step
   int32_t* h_nf = nullptr;     // pinned copy
@@ -2001,7 +2004,9 @@ int claw_destroy(claw_ctx* ctx) {
   if (ctx->ev_ready) cudaEventDestroy(ctx->ev_ready);
   if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
   ctx->nf_flag.reset();
+  ctx->hier_many.reset();
   if (ctx->h_nf) cudaFreeHost(ctx->h_nf);
+  if (ctx->h_many) cudaFreeHost(ctx->h_many);
   const int64_t arena = ctx->arena_id;
   delete ctx;                                  // (every buffer is back in the pool)
   if (arena) pool().remove_arena(arena);
@@ -2695,6 +2700,44 @@ int claw_advance_hierarchy(claw_ctx* ctx, double t, double dt, int32_t flags, do
     }
   }
   return CLAW_OK;
+}
+
+int claw_advance_hierarchy_n(claw_ctx* ctx, double t, double dt, int32_t nsteps, int32_t flags, double* cfl_out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
+  if (nsteps < 1 || !cfl_out) return fail(ctx, CLAW_EINVAL, "nsteps=%d, cfl_out=%p", nsteps, static_cast<void*>(cfl_out));
+  int nlev = 0;
+  while (nlev < kMaxLevel && ctx->lev[nlev + 1].set) ++nlev;
+  if (nlev == 0) return fail(ctx, CLAW_ESTATE, "no level set");
+  // one CFL slot per coarse step, zeroed by one memset for the batch; the
+  // launches of all nsteps coarse steps are queued back to back on the
+  // stream (the host runs ahead of the GPU), one synchronisation at the end
+  if (ctx->hier_many.n < static_cast<size_t>(nsteps)) CUDA_TRY(ctx->hier_many.alloc(static_cast<size_t>(nsteps)));
+  if (ctx->h_many_n < nsteps) {
+    if (ctx->h_many) cudaFreeHost(ctx->h_many);
+    ctx->h_many = nullptr;
+    CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_many), static_cast<size_t>(nsteps) * sizeof(double)));
+    ctx->h_many_n = nsteps;
+  }
+  CUDA_TRY(cudaMemsetAsync(ctx->hier_many.p, 0, static_cast<size_t>(nsteps) * 8, ctx->stream));
+  for (int k = 0; k < nsteps; ++k) {
+    ctx->hier_slot = ctx->hier_many.p + k;
+    const int rc = advance_rec(ctx, 1, t + k * dt, dt, nlev, flags);
+    ctx->hier_slot = nullptr;
+    if (rc) return rc;
+  }
+  if (ctx->cfg.world > 1 && ctx->cfg.exchange == 0) {
+    ncclResult_t nr = g_nccl.AllReduce(ctx->hier_many.p, ctx->hier_many.p, static_cast<size_t>(nsteps), ncclFloat64,
+                                       ncclMax, ctx->comm, ctx->stream);
+    if (nr != ncclSuccess) return nccl_fail(ctx, nr, "ncclAllReduce(cfl, max)");
+  }
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_many, ctx->hier_many.p, static_cast<size_t>(nsteps) * 8, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  if (ctx->cfg.check_finite)
+    CUDA_TRY(cudaMemcpyAsync(ctx->h_nf, ctx->nf_flag.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(cfl_out, ctx->h_many, static_cast<size_t>(nsteps) * sizeof(double));
+  return take_nonfinite(ctx);
 }
 
 int claw_level_owned(const claw_ctx* ctx, int32_t level, int32_t* npatch_owned, int64_t* cells_owned,

@@ -124,3 +124,33 @@ def test_c5_full_size_sampled_every_step():
 
 def test_c4_full_size_sampled_every_step():
     assert sampled_steps(W.c4(), 32, 5, 78, 6) == 35
+
+
+@pytest.mark.parametrize("name,steps", [("c2", 30), ("c3", 12)])
+def test_batched_coarse_steps_equal_single_calls(name, steps):
+    """claw_advance_hierarchy_n (K coarse steps per host synchronisation) is
+    bitwise the same run as K claw_advance_hierarchy calls, CFLs included,
+    and matches the oracle's Berger-Oliger cycles."""
+    wl = getattr(W, name)()
+    q0s = W.hierarchy_ic(wl)
+    nlev = len(wl.levels)
+    ratios = [wl.levels[L].ratio for L in range(1, nlev)]
+    a = binding.Claw(wl.domain, wl.bc, wl.limiter, wl.order_trans, device=0)
+    b = binding.Claw(wl.domain, wl.bc, wl.limiter, wl.order_trans, device=0)
+    o = oracle.Oracle(wl.domain, wl.bc, wl.limiter, wl.order_trans, nthreads=0)
+    for L, (lv, q0) in enumerate(zip(wl.levels, q0s), start=1):
+        a.set_level(L, lv.descs, q0)
+        b.set_level(L, lv.descs, q0)
+        o.set_level(L, lv.descs, q0)
+    dt = wl.dt0()
+    ca = list(a.advance_hierarchy_n(0.0, dt, 5, update=True)) + \
+        list(a.advance_hierarchy_n(5 * dt, dt, steps - 5, update=True))
+    ts = [n * dt for n in range(5)] + [5 * dt + k * dt for k in range(steps - 5)]  # the batches' times
+    cb = [b.advance_hierarchy(t, dt, update=True) for t in ts]
+    co = [oracle_cycle(o, 1, t, dt, nlev, ratios, True) for t in ts]
+    assert ca == cb == co
+    for L in range(1, nlev + 1):
+        assert np.array_equal(a.read_level(L), b.read_level(L))
+        assert rel_err(a.read_level(L), o.read_level(L)) <= TOL
+    a.close()
+    b.close()
