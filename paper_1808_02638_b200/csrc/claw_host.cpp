@@ -9,6 +9,7 @@
 // a level max P:417-420.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX3: ranges cost nothing unless a tool is attached
 #include <unistd.h>
 #include <nccl.h>
 
@@ -548,6 +549,21 @@ int cuda_fail(claw_ctx* c, cudaError_t e, const char* where) {
     cudaError_t e_ = (expr);                           \
     if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #expr); \
   } while (0)
+
+// NVTX range over one API call / phase (tracing): named ranges for
+// ghost fill, level step, halo exchange, CFL all-reduce, updating, regrid and
+// the hierarchy drivers, visible in nsys / ncu timelines
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  Nvtx(const char* fmt, int a) {
+    char b[64];
+    std::snprintf(b, sizeof b, fmt, a);
+    nvtxRangePushA(b);
+  }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
 
 int nccl_fail(claw_ctx* c, ncclResult_t r, const char* where) {
   c->dead = true;
@@ -2018,6 +2034,7 @@ const char* claw_last_error(const claw_ctx* ctx) { return ctx ? ctx->err.c_str()
 
 int claw_set_level(claw_ctx* ctx, int32_t level, int32_t npatch, const claw_patch_desc* descs,
                    const double* q0) {
+  Nvtx nv_("claw_set_level L%d", level);
   if (int rc = check_ctx(ctx)) return rc;
   if (level < 1 || level > kMaxLevel) return fail(ctx, CLAW_EINVAL, "level=%d: must be 1..%d", level, kMaxLevel);
   if (npatch < 1 || !descs) return fail(ctx, CLAW_EINVAL, "npatch=%d: need >= 1 patch descriptors", npatch);
@@ -2073,6 +2090,7 @@ int claw_set_level(claw_ctx* ctx, int32_t level, int32_t npatch, const claw_patc
 }
 
 int claw_set_aux(claw_ctx* ctx, int32_t level, const double* aux) {
+  Nvtx nv_("claw_set_aux L%d", level);
   if (int rc = check_ctx(ctx)) return rc;
   if (int rc = check_level(ctx, level)) return rc;
   Level& L = ctx->lev[level];
@@ -2165,6 +2183,7 @@ int interp_frames(claw_ctx* ctx, int32_t level, const double* ts, int nts) {
 }  // namespace
 
 int claw_fill_ghost(claw_ctx* ctx, int32_t level, double t) {
+  Nvtx nv_("claw_fill_ghost L%d", level);
   if (int rc = check_ctx(ctx)) return rc;
   if (int rc = check_level(ctx, level)) return rc;
   if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
@@ -2186,6 +2205,7 @@ int claw_fill_ghost(claw_ctx* ctx, int32_t level, double t) {
                                                           L.dsend_buf[r]->p, cst)));
       ctx->stats.ghost_launches++;
     }
+    Nvtx nv_halo("claw_halo_exchange");
     ncclResult_t nr = g_nccl.GroupStart();
     if (nr != ncclSuccess) return nccl_fail(ctx, nr, "ncclGroupStart");
     for (int r = 0; r < world; ++r) {
@@ -2210,6 +2230,7 @@ int claw_fill_ghost(claw_ctx* ctx, int32_t level, double t) {
 }
 
 int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
+  Nvtx nv_("claw_step L%d", level);
   if (int rc = check_ctx(ctx)) return rc;
   if (int rc = check_level(ctx, level)) return rc;
   if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
@@ -2341,6 +2362,7 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
     }
   }
   if (ctx->cfg.world > 1 && ctx->cfg.exchange == 0) {
+    Nvtx nv_red("claw_cfl_allreduce");
     ncclResult_t nr = g_nccl.AllReduce(L.lcfl.p + g, L.lcfl.p + g, 1, ncclFloat64, ncclMax, ctx->comm, ctx->stream);
     if (nr != ncclSuccess) return nccl_fail(ctx, nr, "ncclAllReduce(cfl, max)");
   }
@@ -2505,6 +2527,7 @@ int claw_level_mode(const claw_ctx* ctx, int32_t level, int32_t* mode) {
 }
 
 int claw_update_level(claw_ctx* ctx, int32_t level) {
+  Nvtx nv_("claw_update L%d", level);
   if (int rc = check_ctx(ctx)) return rc;
   if (level < 2 || level > kMaxLevel || !ctx->lev[level].set || !ctx->lev[level - 1].set)
     return fail(ctx, CLAW_ESTATE, "update needs level %d and level %d set", level, level - 1);
@@ -2596,6 +2619,7 @@ static int advance_rec(claw_ctx* ctx, int level, double t, double dt, int nlev, 
 }
 
 int claw_advance_hierarchy(claw_ctx* ctx, double t, double dt, int32_t flags, double* cfl_max) {
+  Nvtx nv_("claw_advance_hierarchy");
   if (int rc = check_ctx(ctx)) return rc;
   if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
   if (!cfl_max) return fail(ctx, CLAW_EINVAL, "cfl_max is NULL");
@@ -2703,6 +2727,7 @@ int claw_advance_hierarchy(claw_ctx* ctx, double t, double dt, int32_t flags, do
 }
 
 int claw_advance_hierarchy_n(claw_ctx* ctx, double t, double dt, int32_t nsteps, int32_t flags, double* cfl_out) {
+  Nvtx nv_("claw_advance_hierarchy_n %d", nsteps);
   if (int rc = check_ctx(ctx)) return rc;
   if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
   if (nsteps < 1 || !cfl_out) return fail(ctx, CLAW_EINVAL, "nsteps=%d, cfl_out=%p", nsteps, static_cast<void*>(cfl_out));
@@ -3155,6 +3180,7 @@ int claw_flag(claw_ctx* ctx, int32_t level, double tol, int32_t buffer, int32_t 
 }
 
 int claw_regrid(claw_ctx* ctx, int32_t level, int32_t nbox, const int32_t* boxes, int32_t R) {
+  Nvtx nv_("claw_regrid L%d", level + 1);
   if (int rc = check_ctx(ctx)) return rc;
   if (int rc = check_level(ctx, level)) return rc;
   if (level >= kMaxLevel) return fail(ctx, CLAW_EINVAL, "regrid: level %d has no finer level", level);
