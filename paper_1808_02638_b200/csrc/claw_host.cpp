@@ -1456,14 +1456,25 @@ int plan_level(claw_ctx* c, int level, Level& L) {
       } else if (c->cfg.tile_rows > 0) {
         if (span_ok(c->cfg.tile_rows)) th = c->cfg.tile_rows;
       } else if (L.th == 64) {
-        // large level: the tallest tile (<= 256 rows) that still gives two
-        // waves of warps (SMs x 16 resident warps x 2); measured C5 +3.6%,
-        // C4 +7% over one-patch-row tiles (profiles/r01_grid_tile_rows.txt)
-        for (int w = 256; w > my; w /= 2)
-          if (span_ok(w) && nstrip0 * ((L.Y1 - L.Y0 + w - 1) / w) >= static_cast<int64_t>(c->nsm) * 16 * 2) {
+        // large level: tiles spanning whole patch rows, height chosen by the
+        // makespan of the launch -- ceil(tiles / resident warps) waves of
+        // (th + 4) row steps each (the 4 halo rows are the per-tile
+        // prologue); the tail of a partly filled last wave is what one-
+        // patch-row or fixed 256-row tiles lose on C4 (3.7 waves of 256-row
+        // tiles: the last wave 70% full).  Ties go to the taller tile.
+        const int64_t slots = static_cast<int64_t>(c->nsm) * claw::grid_resident_warps();
+        const int64_t rows = L.Y1 - L.Y0;
+        double best = -1.0;
+        for (int w = my; w <= 512; w += my) {
+          if (!(w == my || span_ok(w))) continue;
+          const int64_t tiles = nstrip0 * ((rows + w - 1) / w);
+          if (tiles < slots) continue;   // sub-wave: keep th <= my (latency-bound levels)
+          const double cost = static_cast<double>((tiles + slots - 1) / slots) * (w + 4);
+          if (best < 0 || cost <= best) {
+            best = cost;
             th = w;
-            break;
           }
+        }
       }
       L.grid_th = th;
       const int64_t nstrip = claw::grid_nstrip(L.nx);

@@ -211,6 +211,7 @@ int launch_regrid(const RegridParams& p, int32_t nnew, void* stream);
 extern int g_pdl;
 void set_pdl(int on);
 int max_tile_rows();
+int grid_resident_warps();   // resident warps per SM the grid kernel is compiled for
 int side_stride();
 int grid_strip();
 // grid-mode strips: count over nx level columns, output columns of strip s
