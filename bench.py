@@ -525,9 +525,8 @@ def main():
         g.set_level(L, lv.descs, buf)
         host_q.append(buf)
         if wl.extra.get("media"):
-            # per-cell media of the whole level (problem description, set once)
-            if world > 1:
-                raise SystemExit("variable media (c5vc) are single-GPU in this version")
+            # per-cell media of the whole level (problem description, set once;
+            # every rank passes all of it and keeps its band + halo rows)
             g.set_aux(L, W.media_field(lv.descs, wl.extra["media"]))
     vc = bool(wl.extra.get("media"))
     bpc = BYTES_PER_CELL_VC if vc else BYTES_PER_CELL

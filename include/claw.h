@@ -170,7 +170,9 @@ int claw_set_level(claw_ctx* ctx, int32_t level, int32_t npatch,
  * max over every swept face of max(c_l, c_r) dt/dx (dt/dy); the descriptors'
  * rho, K are then ignored.  claw_patch_cfl gives each patch's max over its own
  * faces.  Requirements (EINVAL otherwise): level 1 set as one uniform grid of
- * equal patches covering the domain (claw_level_mode 1), world = 1, no finer
+ * equal patches covering the domain (claw_level_mode 1; with world > 1 its
+ * band partition -- each rank then keeps its band's medium and the medium of
+ * its four halo rows, which is static, so nothing is exchanged), no finer
  * level; a later claw_set_level(2..) or claw_regrid is refused while the
  * medium is set, and claw_set_level(1) discards it. */
 int claw_set_aux(claw_ctx* ctx, int32_t level, const double* aux);

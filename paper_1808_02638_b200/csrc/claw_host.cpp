@@ -433,6 +433,7 @@ struct Level {
   // q's patch layout, and per owned patch the max sound speed over its cells
   // and 1-deep ghost frame (the cells its faces touch) for claw_patch_cfl
   DevBuf<double> aux;
+  DevBuf<double> aux_halo;            // band mode: (Z, c) of the four halo rows, [4][2][nx]
   bool vc = false;
   std::vector<double> vc_pcmax;
   double last_r = 0.0, last_s = 0.0;  // dt/dx, dt/dy of the last step
@@ -2107,9 +2108,9 @@ int claw_set_aux(claw_ctx* ctx, int32_t level, const double* aux) {
   Level& L = ctx->lev[level];
   if (level != 1 || ctx->lev[2].set)
     return fail(ctx, CLAW_EINVAL, "set_aux(level %d): variable media are single-level (level 1, no finer level)", level);
-  if (ctx->cfg.world != 1) return fail(ctx, CLAW_EINVAL, "set_aux: single rank only in this version (world=%d)", ctx->cfg.world);
-  if (!L.grid || L.sparse || L.band)
-    return fail(ctx, CLAW_EINVAL, "set_aux: the level must be one uniform grid of equal patches (claw_level_mode 1)");
+  if (!L.grid || L.sparse)
+    return fail(ctx, CLAW_EINVAL, "set_aux: the level must be one uniform grid of equal patches (claw_level_mode 1; "
+                "with world > 1 the band partition)");
   if (!aux) return fail(ctx, CLAW_EINVAL, "aux is NULL");
   const int mx = L.desc[0].mx, my = L.desc[0].my;
   const int64_t plane = static_cast<int64_t>(mx) * my;
@@ -2144,11 +2145,31 @@ int claw_set_aux(claw_ctx* ctx, int32_t level, const double* aux) {
         m = std::max(m, cl[static_cast<size_t>(mapi(J, L.ny, py) * L.nx + mapi(I, L.nx, px))]);
     L.vc_pcmax[lp] = m;
   }
+  // band mode (world > 1): the medium of the four halo rows Y0-2, Y0-1, Y1,
+  // Y1+1 (BC-mapped) as [4][2][nx]; the medium is static, so no exchange
+  std::vector<double> halo(static_cast<size_t>(8 * L.nx), 1.0);
+  for (int kk = 0; kk < 4 && L.band; ++kk) {
+    const int64_t J = kk < 2 ? L.Y0 - 2 + kk : L.Y1 + kk - 2;
+    const int64_t Jm = mapi(J, L.ny, py);
+    for (int64_t I = 0; I < L.nx; ++I) {
+      const int64_t pc = I / mx, pr = Jm / my, p = pr * (L.nx / mx) + pc;
+      const int64_t k = (Jm - pr * my) * mx + (I - pc * mx);
+      halo[static_cast<size_t>((2 * kk) * L.nx + I)] = zc[static_cast<size_t>(p * 2 * plane + k)];
+      halo[static_cast<size_t>((2 * kk + 1) * L.nx + I)] = zc[static_cast<size_t>(p * 2 * plane + plane + k)];
+    }
+  }
   if (!ctx->host_only) {
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     drop_graphs(ctx);
-    CUDA_TRY(L.aux.alloc(static_cast<size_t>(n)));
-    CUDA_TRY(cudaMemcpy(L.aux.p, zc.data(), static_cast<size_t>(n) * 8, cudaMemcpyHostToDevice));
+    // the owned patches: whole patch rows, consecutive (grid / band mode)
+    const int64_t p0 = L.owned.front(), nown = static_cast<int64_t>(L.owned.size());
+    CUDA_TRY(L.aux.alloc(static_cast<size_t>(nown * 2 * plane)));
+    CUDA_TRY(cudaMemcpy(L.aux.p, zc.data() + p0 * 2 * plane, static_cast<size_t>(nown * 2 * plane) * 8,
+                        cudaMemcpyHostToDevice));
+    if (L.band) {
+      CUDA_TRY(L.aux_halo.alloc(halo.size()));
+      CUDA_TRY(cudaMemcpy(L.aux_halo.p, halo.data(), halo.size() * 8, cudaMemcpyHostToDevice));
+    }
   }
   L.vc = true;
   return CLAW_OK;
@@ -2299,6 +2320,7 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
   }
   if (L.vc) {
     P.aux = L.aux.p;
+    P.aux_halo = L.aux_halo.p;
     L.last_r = P.k.r;
     L.last_s = P.k.s;
   }

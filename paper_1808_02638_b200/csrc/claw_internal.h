@@ -96,8 +96,9 @@ struct StepParams {
                                   // lattice slot (row-major, npx per row) the patch index
                                   // (>= 0) or -1-v for virtual slot v of the frame (coarse
                                   // ghost values); P.tiles then lists (strip, row block)
-  const double* aux;              // variable media (grid mode, single rank): [patch][2][my][mx]
-                                  // (Z, c) in q's patch order; null: constant media (R20)
+  const double* aux;              // variable media (grid mode): [owned patch][2][my][mx] (Z, c) in
+                                  // q's patch order; null: constant media (R20)
+  const double* aux_halo;         // band mode: (Z, c) of the 4 halo rows, [4][2][NX]
   double* side;                   // generic kernel: per-tile side records (side_stride()
                                   // doubles per tile), filled by a side_kernel launched
                                   // ahead of the step kernel; null: computed in the kernel

@@ -30,8 +30,8 @@
 #define CLAW_VC_RES_WARPS 12   // resident warps per SM (168 registers per thread)
 #endif
 
-// q and aux pointers of (level column C, level row J), both mapped into the
-// domain (single rank: the whole level is local)
+// q and aux pointers of (level column C, band row Jl = J - Y0) of this rank's
+// band (a whole level on one rank)
 __device__ __forceinline__ void vc_ptrs(const StepParams& P, int C, int J, const double*& q, const double*& a) {
   const int pc = C / P.mx, li = C - pc * P.mx;
   const int pr = J / P.my, lj = J - pr * P.my;
@@ -47,6 +47,25 @@ __device__ __forceinline__ void vc_ptrs(const StepParams& P, int C, int J, const
 // i.e. the last bit of the double), no special-case branch; the rounding may
 // differ from the correctly rounded __drcp_rn by one ulp (parity is by
 // tolerance, R20)
+// sources of (column C, level row J) for any row the march reads: the band
+// (after the BC map), or -- multi-rank band mode -- one of the four halo
+// rows: q from the frame the NCCL receives land in (grid_src's rule), the
+// medium from the rank's static copy of those rows (claw_set_aux)
+__device__ __forceinline__ void vc_src(const StepParams& P, int C, int J, const double*& q, const double*& a,
+                                       int64_t& cq, int64_t& ca) {
+  const int Jm = map_idx(J, P.NY, P.per_y);
+  if (Jm >= P.Y0 && Jm < P.Y1) {
+    vc_ptrs(P, C, Jm - P.Y0, q, a);
+    cq = ca = static_cast<int64_t>(P.mx) * P.my;
+    return;
+  }
+  const int kk = (J < P.Y0) ? (J - (P.Y0 - 2)) : (2 + J - P.Y1);
+  q = P.frame + P.hoff[kk] + C;
+  cq = P.hcs[kk];
+  a = P.aux_halo + static_cast<int64_t>(kk) * 2 * P.NX + C;
+  ca = P.NX;
+}
+
 __device__ __forceinline__ double vc_rcp(double x) {
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
@@ -74,13 +93,13 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
   const int b = P.blk_first + (t / nstrip) * P.blk_stride;
   int j0, th;
   if (span) {
-    j0 = b * P.th;
-    th = min(P.th, P.NY - j0);
+    j0 = P.Y0 + b * P.th;
+    th = min(P.th, P.Y1 - j0);
   } else {
     const int nbr = (myv + P.th - 1) / P.th;
     const int prow = b / nbr, r0 = (b - prow * nbr) * P.th;
     th = min(P.th, myv - r0);
-    j0 = prow * myv + r0;
+    j0 = P.Y0 + prow * myv + r0;
   }
   const int c0 = s * kStrip;
   const int tw = min(kStrip, P.NX - c0);
@@ -96,20 +115,23 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
   const int ax = lane == 0 ? 0 : 33;
   const int rtop = j0 + th;
   const double *gq0, *ga0, *xq0, *xa0;   // main / aux column at row j0
-  vc_ptrs(P, C, j0, gq0, ga0);
-  vc_ptrs(P, Ca, j0, xq0, xa0);
+  vc_ptrs(P, C, j0 - P.Y0, gq0, ga0);
+  vc_ptrs(P, Ca, j0 - P.Y0, xq0, xa0);
   double (*ring)[5][34] = sq;
 
-  auto issue_ptr = [&](int sl, const double* g, const double* ga, const double* x, const double* xa, bool on) {
+  // (component strides: cq / ca of the main column, xcq / xca of the aux
+  // column; the band's plane size except on halo rows)
+  auto issue_ptr = [&](int sl, const double* g, const double* ga, const double* x, const double* xa, bool on,
+                       int64_t cq, int64_t ca, int64_t xcq, int64_t xca) {
     cp8_pred(&ring[sl][XP][lane + 1], g, on);
-    cp8_pred(&ring[sl][XU][lane + 1], g + cs, on);
-    cp8_pred(&ring[sl][XV][lane + 1], g + 2 * cs, on);
+    cp8_pred(&ring[sl][XU][lane + 1], g + cq, on);
+    cp8_pred(&ring[sl][XV][lane + 1], g + 2 * cq, on);
     cp8_pred(&ring[sl][XZ][lane + 1], ga, on);
-    cp8_pred(&ring[sl][XC][lane + 1], ga + cs, on);
+    cp8_pred(&ring[sl][XC][lane + 1], ga + ca, on);
     cp8_pred(&ring[sl][XP][ax], x, edge && on);
-    cp8_pred(&ring[sl][XU][ax], x + cs, edge && on);
+    cp8_pred(&ring[sl][XU][ax], x + xcq, edge && on);
     cp8_pred(&ring[sl][XZ][ax], xa, edge && on);
-    cp8_pred(&ring[sl][XC][ax], xa + cs, edge && on);
+    cp8_pred(&ring[sl][XC][ax], xa + xca, edge && on);
     cp_commit();
   };
   // general issue of row R (halo rows mapped by the BCs; rows past rtop + 1,
@@ -119,22 +141,21 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
     R = min(R, rtop + 1);
     const int sl = (R - j0 + 2) & (kGRD - 1);
     const double *g, *ga, *x, *xa;
+    int64_t cq = cs, ca = cs, xcq = cs, xca = cs;
     if (R >= j0 && R < rtop) {
       g = gq0 + static_cast<int64_t>(R - j0) * mx;   // tile rows: inside one patch row unless span
       ga = ga0 + static_cast<int64_t>(R - j0) * mx;
       x = xq0 + static_cast<int64_t>(R - j0) * mx;
       xa = xa0 + static_cast<int64_t>(R - j0) * mx;
       if (span) {
-        const int J = R;
-        vc_ptrs(P, C, J, g, ga);
-        vc_ptrs(P, Ca, J, x, xa);
+        vc_ptrs(P, C, R - P.Y0, g, ga);
+        vc_ptrs(P, Ca, R - P.Y0, x, xa);
       }
     } else {
-      const int J = map_idx(R, P.NY, P.per_y);
-      vc_ptrs(P, C, J, g, ga);
-      vc_ptrs(P, Ca, J, x, xa);
+      vc_src(P, C, R, g, ga, cq, ca);
+      vc_src(P, Ca, R, x, xa, xcq, xca);
     }
-    issue_ptr(sl, g, ga, x, xa, on);
+    issue_ptr(sl, g, ga, x, xa, on, cq, ca, xcq, xca);
   };
   auto slot = [&](int R) { return (R - j0 + 2) & (kGRD - 1); };
 
@@ -250,15 +271,15 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
     constexpr int S0 = PH & 3, S1 = (PH + 1) & 3, S2 = (PH + 2) & 3, S3 = (PH + 3) & 3;
     const int j = jb + PH;
     static_assert((kGPD + 2 + 1) % 4 == 0, "the prefetched row crosses patch rows in phase 1");
-    if (PH == 1 && span && (jb + kGPD + 3) % myv == 0) {  // row j+2+kGPD starts a patch row
+    if (PH == 1 && span && (jb + kGPD + 3 - P.Y0) % myv == 0) {  // row j+2+kGPD starts a patch row
       gq += jump_q;
       xq += jump_q;
       ga += jump_a;
       xa += jump_a;
     }
-    if (PH == 0 && span && jb != j0 && jb % myv == 0) o += jump_q;
+    if (PH == 0 && span && jb != j0 && (jb - P.Y0) % myv == 0) o += jump_q;
     if (decltype(fastc)::value) {
-      issue_ptr((j + 2 + kGPD - j0 + 2) & (kGRD - 1), gq, ga, xq, xa, true);
+      issue_ptr((j + 2 + kGPD - j0 + 2) & (kGRD - 1), gq, ga, xq, xa, true, cs, cs, cs, cs);
     } else {
       issue(j + 2 + kGPD);
     }

@@ -75,3 +75,46 @@ def test_virtual_ranks_bitwise_equal_single_rank(world, name, bc, path):
                 got[offs[p]:offs[p + 1]] = mine[k:k + n]
                 k += n
     assert np.array_equal(got, full)
+
+
+@pytest.mark.parametrize("world,npx,mx,bc", [(2, 8, 32, W.EXTRAP), (3, 6, 16, W.PERIODIC), (4, 8, 32, (1, 1, 2, 2))])
+def test_virtual_ranks_variable_media_bitwise_equal_single_rank(world, npx, mx, bc):
+    """Variable media (claw_set_aux, R20) on a band-partitioned uniform grid:
+    every rank gets the whole medium, keeps its band and the (Z, c) of its
+    four halo rows; q halos move through the external exchange.  The N-rank
+    run is bitwise the 1-rank run, CFLs included (a per-face max, exact)."""
+    d = W.uniform_level(npx, npx, mx, mx)
+    q0 = W.random_ic(d, 7 * world)
+    aux = W.random_media(d, 5 * world, 0.4, 2.5)
+    offs = W.level_offsets(d)
+    owners = binding.partition(d, world)
+    ctxs = []
+    for r in range(world):
+        c = binding.Claw(W.DOMAIN, bc, 4, 2, device=0, rank=r, world=world, exchange=1)
+        mine = np.concatenate([q0[offs[p]:offs[p + 1]] for p in range(len(d)) if owners[p] == r])
+        c.set_level(1, d, mine)
+        assert c.level_mode(1) == "grid"
+        c.set_aux(1, aux)
+        ctxs.append(c)
+    ref = binding.Claw(W.DOMAIN, bc, 4, 2, device=0)
+    ref.set_level(1, d, q0)
+    ref.set_aux(1, aux)
+    dt = 0.8 * float(d["dx"][0]) / W.max_sound_speed(aux, d)
+    for n in range(6):
+        for c in ctxs:
+            c.fill_ghost(1, n * dt)
+        for r in range(world):
+            for s in range(world):
+                if r != s:
+                    ctxs[s].halo_unpack(1, r, ctxs[r].halo_pack(1, s))
+        cfl = max(c.advance_level(1, dt) for c in ctxs)
+        ref.fill_ghost(1, n * dt)
+        assert cfl == ref.advance_level(1, dt)
+    full = ref.read_level(1)
+    for r, c in enumerate(ctxs):
+        mine = c.read_level(1)
+        want = np.concatenate([full[offs[p]:offs[p + 1]] for p in range(len(d)) if owners[p] == r])
+        assert np.array_equal(mine, want)
+        for p in range(len(d)):
+            if owners[p] == r:
+                assert c.patch_cfl(1, p) == ref.patch_cfl(1, p)
