@@ -22,7 +22,9 @@
 //       G(j+1/2) = sigma (K_{j+1} T_j - K_j T_{j+1},  0,  c_{j+1} T_j + c_j T_{j+1}),
 //     sigma = 1 / (Z_j + Z_{j+1}), K = c Z (y-sweep edges likewise along x);
 //   * the Courant number is the max over every swept face of max(c_l, c_r)
-//     times dt/dx (dt/dy), kept per lane, warp-reduced, atomicMax'ed.
+//     times dt/dx (dt/dy): every cell is a left or right cell of a swept
+//     face, so each lane keeps the max c of its column's cells, then warp max
+//     and atomicMax.
 // Rounding differs from the oracle (FMA, reciprocals, division-free
 // limiters, combined transverse splits): parity is by tolerance.
 
@@ -166,11 +168,14 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
   double fa1[4], fa2[4], fm[4], fsg[4], fqp[4], fqv[4];               // y-faces
   double xP[4], xU[4], xT[4], xsR[4], pk[4], uk[4];                   // x-swept rows
   double Gp[4], Gv[4];                                                // x-transverse edge fluxes
-  double cmx = 0.0, cmy = 0.0;                                        // max face speeds (CFL)
+  double cm = 0.0;   // max sound speed over the cells of this lane's column the march reads (CFL)
 
-  // derived medium values of a freshly loaded row (own column)
-  auto cell = [&](int S, int sl) {
+  // derived medium values of a freshly loaded row (own column); live: the
+  // row belongs to the tile's stencil (the unrolled march runs past the last
+  // row on ring slots holding stale rows, whose speeds must not count)
+  auto cell = [&](int S, int sl, bool live) {
     const double Z = ring[sl][XZ][lane + 1], c = ring[sl][XC][lane + 1];
+    if (live) cm = dmax(cm, c);
     cZ[S] = Z;
     cc[S] = c;
     cnu[S] = vc_rcp(__fma_rn(Z, Z, 1.0));
@@ -181,17 +186,13 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
     cv[S] = ring[sl][XV][lane + 1];
   };
   // y-face F(k) between the cells in slots Sl (row k-1) and Su (row k)
-  // (live: the face / row belongs to the tile's stencil -- the unrolled march
-  // runs past the last row on ring slots that hold stale rows, whose speeds
-  // must not enter the Courant number)
-  auto yface = [&](int Sf, int Sl, int Su, bool live) {
+  auto yface = [&](int Sf, int Sl, int Su) {
     const double sg = vc_rcp(__dadd_rn(cZ[Sl], cZ[Su]));
     const double dp = __dsub_rn(cp_[Su], cp_[Sl]), dv = __dsub_rn(cv[Su], cv[Sl]);
     fa1[Sf] = __dmul_rn(sg, __fma_rn(cZ[Su], dv, -dp));
     fa2[Sf] = __dmul_rn(sg, __fma_rn(cZ[Sl], dv, dp));
     fm[Sf] = __fma_rn(cZ[Sl], cZ[Su], 1.0);
     fsg[Sf] = sg;
-    if (live) cmy = dmax(cmy, dmax(cc[Sl], cc[Su]));
   };
   // limit y-face F(k): Sf its slot, Sl / Su its cells, Sd / Sup the faces
   // below / above (upwind of wave 2 / wave 1)
@@ -202,15 +203,13 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
     fqv[Sf] = __fma_rn(cey[Su], t2, __dmul_rn(cey[Sl], t1));
   };
   // x-sweep of the row in ring slot sl whose cell values sit in slot S
-  auto xsweep = [&](int S, int sl, bool live) {
+  auto xsweep = [&](int S, int sl) {
     const double p = ring[sl][XP][lane + 1], u = ring[sl][XU][lane + 1];
     const double pl = ring[sl][XP][lane], ul = ring[sl][XU][lane], Zl = ring[sl][XZ][lane];
     const double pr = ring[sl][XP][lane + 2], ur = ring[sl][XU][lane + 2], Zr = ring[sl][XZ][lane + 2];
-    const double cl = ring[sl][XC][lane];
     const double Z = cZ[S], c = cc[S], K = cK[S];
     pk[S] = p;
     uk[S] = u;
-    if (live) cmx = dmax(cmx, dmax(cl, c));
     const double sL = vc_rcp(__dadd_rn(Zl, Z)), sR = vc_rcp(__dadd_rn(Z, Zr));
     const double dpl = __dsub_rn(p, pl), dul = __dsub_rn(u, ul);
     const double a1 = __dmul_rn(sL, __fma_rn(Z, dul, -dpl));
@@ -222,8 +221,7 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
     const double t2 = Limiter<LIM>::apply(a2, __dmul_rn(a2u, __dmul_rn(mL, cnu[S])));
     const double ex = __dmul_rn(__dmul_rn(c, __fma_rn(-c, r, 1.0)), inv2ls);
     const double exZ = __dmul_rn(ex, Z);
-    const double exl = __dmul_rn(__dmul_rn(cl, __fma_rn(-cl, r, 1.0)), inv2ls);  // the left cell's
-    const double exZl = __dmul_rn(exl, Zl);
+    const double exl = shfl_up(ex), exZl = shfl_up(exZ);   // the left cell's (lane 0: unused)
     const double qp = __fma_rn(exZ, t2, -__dmul_rn(exZl, t1));   // 1/2 cq of the left face
     const double qu = __fma_rn(ex, t2, __dmul_rn(exl, t1));
     const double dqp = __dsub_rn(shfl_dn(qp), qp), dqu = __dsub_rn(shfl_dn(qu), qu);
@@ -244,16 +242,16 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
   for (int R = j0 - 2; R <= j0 + kGRD - 3; ++R) issue(R);
   cp_wait<kGRD - 4>();
   __syncwarp();
-  cell(2, slot(j0 - 2));
-  cell(3, slot(j0 - 1));
-  cell(0, slot(j0));
-  cell(1, slot(j0 + 1));
-  yface(3, 2, 3, true);   // F(j0-1)
-  yface(0, 3, 0, true);   // F(j0)
-  yface(1, 0, 1, true);   // F(j0+1)
+  cell(2, slot(j0 - 2), true);
+  cell(3, slot(j0 - 1), true);
+  cell(0, slot(j0), true);
+  cell(1, slot(j0 + 1), true);
+  yface(3, 2, 3);   // F(j0-1)
+  yface(0, 3, 0);   // F(j0)
+  yface(1, 0, 1);   // F(j0+1)
   ylimit(0, 3, 0, 3, 1);
-  xsweep(3, slot(j0 - 1), true);
-  xsweep(0, slot(j0), true);
+  xsweep(3, slot(j0 - 1));
+  xsweep(0, slot(j0));
   if (OT != 0) gedge(0, 3, 0);
   __syncwarp();
   issue(j0 + kGPD + 1);
@@ -291,10 +289,10 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
     __syncwarp();
     const int rs0 = slot(j), rs1 = slot(j + 1), rs2 = slot(j + 2);
     const bool live = j < rtop;
-    cell(S2, rs2);                    // row j+2
-    yface(S2, S1, S2, live);          // F(j+2)
+    cell(S2, rs2, live);              // row j+2
+    yface(S2, S1, S2);                // F(j+2)
     ylimit(S1, S0, S1, S0, S2);       // F(j+1)
-    xsweep(S1, rs1, live);            // row j+1
+    xsweep(S1, rs1);                  // row j+1
     if (OT != 0) gedge(S1, S0, S1);   // G of F(j+1)
     // finalise row j
     const double K0 = cK[S0], c0v = cc[S0];
@@ -345,7 +343,11 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
   // Courant number: max over this warp's swept faces of max(c_l, c_r) dt/dx
   // (dt/dy) -- every face's cells are cells of the domain (BC images are
   // copies), so the level max is exact
-  double cf = fmax(__dmul_rn(r, cmx), __dmul_rn(sy, cmy));
+  // every swept x- (y-) face's speed is max(c_l, c_r) of two cells of the
+  // domain, and every cell is a left or right cell of such a face, so the max
+  // over the faces of max(c_l, c_r) dt/dx is dt/dx times the max over the
+  // cells; each cell is in some lane's column (BC images are copies)
+  double cf = fmax(__dmul_rn(r, cm), __dmul_rn(sy, cm));
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) cf = fmax(cf, __shfl_xor_sync(kFull, cf, off));
   if (lane == 0 && cf > 0.0) {
