@@ -1929,6 +1929,8 @@ int claw_create(const claw_config* cfg, claw_ctx** out) {
   {
     const char* pd = std::getenv("CLAW_PDL");  // programmatic dependent launches (default on)
     claw::set_pdl(pd ? std::atoi(pd) : 1);
+    const char* rc = std::getenv("CLAW_ROWCOPY");  // grid-kernel row copies
+    claw::set_rowcopy(rc ? std::atoi(rc) : 1);
   }
   {
     // opt-in (CLAW_GRAPH=1): measured slower than the asynchronous launch

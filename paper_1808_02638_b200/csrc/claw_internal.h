@@ -211,6 +211,10 @@ int launch_regrid(const RegridParams& p, int32_t nnew, void* stream);
 // programmatic dependent launches of the step-sequence kernels (default on)
 extern int g_pdl;
 void set_pdl(int on);
+// row copies of the grid kernel where the layout allows (step_grid_kernel RC:
+// 0 per-lane 8 B, 1 per-lane 16 B, 2 cp.async.bulk)
+extern int g_rowcopy;
+void set_rowcopy(int rc);
 int max_tile_rows();
 int grid_resident_warps();   // resident warps per SM the grid kernel is compiled for
 int side_stride();
