@@ -99,6 +99,7 @@ struct StepParams {
   const double* aux;              // variable media (grid mode): [owned patch][2][my][mx] (Z, c) in
                                   // q's patch order; null: constant media (R20)
   const double* aux_halo;         // band mode: (Z, c) of the 4 halo rows, [4][2][NX]
+  int32_t wide;                   // step_vc_kernel: 16-byte row copies allowed (set by its launcher)
   double* side;                   // generic kernel: per-tile side records (side_stride()
                                   // doubles per tile), filled by a side_kernel launched
                                   // ahead of the step kernel; null: computed in the kernel

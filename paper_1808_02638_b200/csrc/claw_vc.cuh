@@ -31,6 +31,11 @@
 #ifndef CLAW_VC_RES_WARPS
 #define CLAW_VC_RES_WARPS 12   // resident warps per SM (168 registers per thread)
 #endif
+#ifndef CLAW_VC_KW
+#define CLAW_VC_KW 1           // warps (consecutive strips of a row block) per CTA (2-4 measured slower:
+                               // this kernel is fp64-bound, profiles/r02_vc_rowcopy.txt)
+#endif
+static_assert(CLAW_VC_RES_WARPS % CLAW_VC_KW == 0, "CLAW_VC_KW must divide CLAW_VC_RES_WARPS");
 
 // q and aux pointers of (level column C, band row Jl = J - Y0) of this rank's
 // band (a whole level on one rank)
@@ -77,14 +82,21 @@ __device__ __forceinline__ double vc_rcp(double x) {
   return __fma_rn(y, e, y);
 }
 
+// Row copies as in the grid kernel's RC 1: the rows inside the tile of an
+// interior strip (all 34 ring columns in the level; wide = the level's rows
+// and planes are 16-byte aligned) arrive as 85 16-byte chunks (5 components
+// x 17 column pairs, 3 LDGSTS.128 per row instead of 9 8-byte copies),
+// allocated in L1 (a CTA may run CLAW_VC_KW consecutive strips so the
+// columns neighbouring strips share are re-read from L1; one is fastest).
 template <int LIM, int OT>
-__global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const StepParams P) {
+__global__ void __launch_bounds__(32 * CLAW_VC_KW, CLAW_VC_RES_WARPS / CLAW_VC_KW) step_vc_kernel(const StepParams P) {
   // ring row x = lane + 1 holds lane `lane`'s column; x = 0 / 33 the aux
   // columns (p, u, Z, c) left of lane 0 / right of the last halo lane
-  __shared__ __align__(16) double sq[kGRD][5][34];
+  constexpr int KW = CLAW_VC_KW;
+  __shared__ __align__(16) double sqr[KW][kGRD][5][34];
   constexpr int XP = 0, XU = 1, XV = 2, XZ = 3, XC = 4;
-  const int lane = threadIdx.x & 31;
-  const int t = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.x * KW + warp;
   const int nstrip = (P.NX + kStrip - 1) / kStrip;
   const int myv = P.my, mx = P.mx;
   const bool span = P.th > myv;
@@ -119,7 +131,44 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
   const double *gq0, *ga0, *xq0, *xa0;   // main / aux column at row j0
   vc_ptrs(P, C, j0 - P.Y0, gq0, ga0);
   vc_ptrs(P, Ca, j0 - P.Y0, xq0, xa0);
-  double (*ring)[5][34] = sq;
+  double (*ring)[5][34] = sqr[warp];
+  // wide strip (see above): chunk ch < 85 is component ch / 17 (p, u, v from
+  // q; Z, c from aux), columns cb + 2 (ch % 17) + {0, 1} (pairs start on even
+  // columns like the patches: no pair straddles two patches).  Lane l copies
+  // chunks l (q), l + 32 (q for l < 19, else aux) and l + 64 (aux, l < 21):
+  // running sources wq (chunk l) and wa (the lane's first aux chunk)
+  const bool wstrip = P.wide && c0 >= 2 && c0 + 32 <= P.NX;
+  const int cb = c0 - 2;
+  auto chunk_src = [&](int ch, int J) {
+    const int comp = ch / 17, pr2 = ch - 17 * comp;
+    const double *q, *a;
+    vc_ptrs(P, cb + 2 * pr2, J - P.Y0, q, a);
+    return comp < 3 ? q + comp * cs : a + (comp - 3) * cs;
+  };
+  auto chunk_dst = [&](int ch) {
+    const int comp = ch / 17, pr2 = ch - 17 * comp;
+    return smem_u32(&ring[0][comp][2 * pr2]);
+  };
+  const bool c2q = lane < 19, c3on = lane < 21;
+  const double *wq0 = nullptr, *wa0 = nullptr;
+  int32_t woff2 = 0;
+  unsigned wd1 = 0, wd2 = 0, wd3 = 0;
+  if (wstrip) {
+    wq0 = chunk_src(lane, j0);
+    wa0 = chunk_src(c3on ? lane + 64 : lane + 32, j0);
+    woff2 = static_cast<int32_t>(chunk_src(lane + 32, j0) - (c2q ? wq0 : wa0));
+    wd1 = chunk_dst(lane);
+    wd2 = chunk_dst(lane + 32);
+    wd3 = c3on ? chunk_dst(lane + 64) : 0u;
+  }
+  constexpr unsigned kSlotB = 5 * 34 * 8;   // bytes per ring slot
+  auto issue_wide = [&](int sl, const double* wq, const double* wa) {
+    const unsigned so = static_cast<unsigned>(sl) * kSlotB;
+    cp16s(wd1 + so, wq);
+    cp16s(wd2 + so, (c2q ? wq : wa) + woff2);
+    cp16s_pred(wd3 + so, wa, c3on);
+    cp_commit();
+  };
 
   // (component strides: cq / ca of the main column, xcq / xca of the aux
   // column; the band's plane size except on halo rows)
@@ -140,6 +189,17 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
   // never read for a stored cell, commit an empty group)
   auto issue = [&](int R) {
     const bool on = R <= rtop + 1;
+    if (wstrip && R >= j0 && R < rtop) {
+      const int sl = (R - j0 + 2) & (kGRD - 1);
+      if (span) {
+        const double* wq = chunk_src(lane, R);
+        const double* wa = chunk_src(c3on ? lane + 64 : lane + 32, R);
+        issue_wide(sl, wq, wa);
+      } else {
+        issue_wide(sl, wq0 + static_cast<int64_t>(R - j0) * mx, wa0 + static_cast<int64_t>(R - j0) * mx);
+      }
+      return;
+    }
     R = min(R, rtop + 1);
     const int sl = (R - j0 + 2) & (kGRD - 1);
     const double *g, *ga, *x, *xa;
@@ -259,8 +319,9 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
   double* o = P.qn + (gq0 - P.q);
   const int64_t jump_q = static_cast<int64_t>(P.npx) * 3 * mx * myv - static_cast<int64_t>(myv) * mx;
   const int64_t jump_a = static_cast<int64_t>(P.npx) * 2 * mx * myv - static_cast<int64_t>(myv) * mx;
-  const double* gq = gq0 + static_cast<int64_t>(kGPD + 2) * mx;
-  const double* ga = ga0 + static_cast<int64_t>(kGPD + 2) * mx;
+  // (wide strips: gq / ga run the lane's chunk sources wq / wa instead)
+  const double* gq = (wstrip ? wq0 : gq0) + static_cast<int64_t>(kGPD + 2) * mx;
+  const double* ga = (wstrip ? wa0 : ga0) + static_cast<int64_t>(kGPD + 2) * mx;
   const double* xq = xq0 + static_cast<int64_t>(kGPD + 2) * mx;
   const double* xa = xa0 + static_cast<int64_t>(kGPD + 2) * mx;
 
@@ -277,7 +338,12 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
     }
     if (PH == 0 && span && jb != j0 && (jb - P.Y0) % myv == 0) o += jump_q;
     if (decltype(fastc)::value) {
-      issue_ptr((j + 2 + kGPD - j0 + 2) & (kGRD - 1), gq, ga, xq, xa, true, cs, cs, cs, cs);
+      if (wstrip)
+        issue_wide((j + 2 + kGPD - j0 + 2) & (kGRD - 1), gq, ga);
+      else
+        issue_ptr((j + 2 + kGPD - j0 + 2) & (kGRD - 1), gq, ga, xq, xa, true, cs, cs, cs, cs);
+    } else if (wstrip && j + 2 + kGPD < rtop) {
+      issue_wide((j + 2 + kGPD - j0 + 2) & (kGRD - 1), gq, ga);
     } else {
       issue(j + 2 + kGPD);
     }
@@ -359,10 +425,12 @@ __global__ void __launch_bounds__(32, CLAW_VC_RES_WARPS) step_vc_kernel(const St
 
 template <int LIM>
 cudaError_t launch_vc(const StepParams& p, cudaStream_t st) {
-  const dim3 grid(p.ntiles), block(32);
+  const dim3 grid((p.ntiles + CLAW_VC_KW - 1) / CLAW_VC_KW), block(32 * CLAW_VC_KW);
+  StepParams w = p;   // 16-byte row copies: even patch width, 16-byte aligned q and aux
+  w.wide = g_rowcopy != 0 && p.mx % 2 == 0 && ((reinterpret_cast<uintptr_t>(p.q) | reinterpret_cast<uintptr_t>(p.aux)) & 15) == 0;
   switch (p.order_trans) {
-    case 0: return launch_k(step_vc_kernel<LIM, 0>, grid, block, st, p);
-    case 1: return launch_k(step_vc_kernel<LIM, 1>, grid, block, st, p);
-    default: return launch_k(step_vc_kernel<LIM, 2>, grid, block, st, p);
+    case 0: return launch_k(step_vc_kernel<LIM, 0>, grid, block, st, w);
+    case 1: return launch_k(step_vc_kernel<LIM, 1>, grid, block, st, w);
+    default: return launch_k(step_vc_kernel<LIM, 2>, grid, block, st, w);
   }
 }
