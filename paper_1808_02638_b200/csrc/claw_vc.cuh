@@ -94,6 +94,14 @@ __global__ void __launch_bounds__(32 * CLAW_VC_KW, CLAW_VC_RES_WARPS / CLAW_VC_K
   // columns (p, u, Z, c) left of lane 0 / right of the last halo lane
   constexpr int KW = CLAW_VC_KW;
   __shared__ __align__(16) double sqr[KW][kGRD][5][34];
+  // sources of the two halo rows above the tile (rtop, rtop + 1), resolved
+  // once in the prologue (the grid kernel's branch-free tail): q and aux of
+  // the lane's column and of its aux column, component strides
+  struct HaloSrcVC {
+    const double *g, *ga, *x, *xa;
+    int32_t cq, ca, xcq, xca;
+  };
+  __shared__ HaloSrcVC shalo[KW][2][32];
   constexpr int XP = 0, XU = 1, XV = 2, XZ = 3, XC = 4;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = blockIdx.x * KW + warp;
@@ -168,6 +176,13 @@ __global__ void __launch_bounds__(32 * CLAW_VC_KW, CLAW_VC_RES_WARPS / CLAW_VC_K
     cp16s(wd2 + so, (c2q ? wq : wa) + woff2);
     cp16s_pred(wd3 + so, wa, c3on);
     cp_commit();
+  };
+  // (no commit: the per-lane copies that follow it commit the row's group)
+  auto issue_wide_pred = [&](int sl, const double* wq, const double* wa, bool p) {
+    const unsigned so = static_cast<unsigned>(sl) * kSlotB;
+    cp16s_pred(wd1 + so, wq, p);
+    cp16s_pred(wd2 + so, (c2q ? wq : wa) + woff2, p);
+    cp16s_pred(wd3 + so, wa, c3on && p);
   };
 
   // (component strides: cq / ca of the main column, xcq / xca of the aux
@@ -298,6 +313,18 @@ __global__ void __launch_bounds__(32 * CLAW_VC_KW, CLAW_VC_RES_WARPS / CLAW_VC_K
   };
 
   // ---- prologue: rows j0-2 .. j0+1 (slots 2, 3, 0, 1)
+#pragma unroll
+  for (int k2 = 0; k2 < 2; ++k2) {
+    HaloSrcVC h;
+    int64_t cq, ca, xcq, xca;
+    vc_src(P, C, rtop + k2, h.g, h.ga, cq, ca);
+    vc_src(P, Ca, rtop + k2, h.x, h.xa, xcq, xca);
+    h.cq = static_cast<int32_t>(cq);
+    h.ca = static_cast<int32_t>(ca);
+    h.xcq = static_cast<int32_t>(xcq);
+    h.xca = static_cast<int32_t>(xca);
+    shalo[warp][k2][lane] = h;
+  }
 #pragma unroll 1
   for (int R = j0 - 2; R <= j0 + kGRD - 3; ++R) issue(R);
   cp_wait<kGRD - 4>();
@@ -342,10 +369,17 @@ __global__ void __launch_bounds__(32 * CLAW_VC_KW, CLAW_VC_RES_WARPS / CLAW_VC_K
         issue_wide((j + 2 + kGPD - j0 + 2) & (kGRD - 1), gq, ga);
       else
         issue_ptr((j + 2 + kGPD - j0 + 2) & (kGRD - 1), gq, ga, xq, xa, true, cs, cs, cs, cs);
-    } else if (wstrip && j + 2 + kGPD < rtop) {
-      issue_wide((j + 2 + kGPD - j0 + 2) & (kGRD - 1), gq, ga);
     } else {
-      issue(j + 2 + kGPD);
+      // general issue, branch-free (see HaloSrcVC): rows inside the tile from
+      // the running pointers (wide strips: 16-byte chunks), rows rtop, rtop + 1
+      // from the table, rows past rtop + 1 nothing (empty group)
+      const int R = j + 2 + kGPD;
+      const bool in = R < rtop, on = R <= rtop + 1, wide = wstrip && in;
+      const int sl = (min(R, rtop + 1) - j0 + 2) & (kGRD - 1);
+      const HaloSrcVC& h = shalo[warp][min(max(R - rtop, 0), 1)][lane];
+      issue_wide_pred(sl, gq, ga, wide);
+      issue_ptr(sl, in ? gq : h.g, in ? ga : h.ga, in ? xq : h.x, in ? xa : h.xa, on && !wide,
+                in ? cs : h.cq, in ? cs : h.ca, in ? cs : h.xcq, in ? cs : h.xca);
     }
     gq += mx;
     ga += mx;
