@@ -364,6 +364,11 @@ __global__ void __launch_bounds__(32 * CLAW_VC_KW, CLAW_VC_RES_WARPS / CLAW_VC_K
       xa += jump_a;
     }
     if (PH == 0 && span && jb != j0 && (jb - P.Y0) % myv == 0) o += jump_q;
+    // row j+2 landed (rows up to j+1+kGPD are in flight); the warp barrier
+    // also orders every read of the slot the next issue overwrites (row j-1:
+    // its finalisation read neighbours' media, one step ago) before the copy
+    cp_wait<kGPD - 1>();
+    __syncwarp();
     if (decltype(fastc)::value) {
       if (wstrip)
         issue_wide((j + 2 + kGPD - j0 + 2) & (kGRD - 1), gq, ga);
@@ -385,8 +390,6 @@ __global__ void __launch_bounds__(32 * CLAW_VC_KW, CLAW_VC_RES_WARPS / CLAW_VC_K
     ga += mx;
     xq += mx;
     xa += mx;
-    cp_wait<kGPD>();
-    __syncwarp();
     const int rs0 = slot(j), rs1 = slot(j + 1), rs2 = slot(j + 2);
     const bool live = j < rtop;
     cell(S2, rs2, live);              // row j+2
