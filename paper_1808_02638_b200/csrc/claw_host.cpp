@@ -1929,8 +1929,8 @@ int claw_create(const claw_config* cfg, claw_ctx** out) {
   {
     const char* pd = std::getenv("CLAW_PDL");  // programmatic dependent launches (default on)
     claw::set_pdl(pd ? std::atoi(pd) : 1);
-    const char* rc = std::getenv("CLAW_ROWCOPY");  // grid-kernel row copies
-    claw::set_rowcopy(rc ? std::atoi(rc) : 1);
+    const char* rc = std::getenv("CLAW_ROWCOPY");  // grid-kernel row copies: 3 auto
+    claw::set_rowcopy(rc ? std::atoi(rc) : 3);
   }
   {
     // opt-in (CLAW_GRAPH=1): measured slower than the asynchronous launch
@@ -1942,6 +1942,7 @@ int claw_create(const claw_config* cfg, claw_ctx** out) {
   if (ctx->host_only) return CLAW_OK;
   CUDA_TRY(cudaSetDevice(cfg->device));
   CUDA_TRY(cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, cfg->device));
+  claw::set_grid_wave(ctx->nsm * claw::grid_resident_warps());
   t_arena = 0;
   if (cfg->arena) {
     cudaPointerAttributes pa{};

@@ -213,9 +213,14 @@ int launch_regrid(const RegridParams& p, int32_t nnew, void* stream);
 extern int g_pdl;
 void set_pdl(int on);
 // row copies of the grid kernel where the layout allows (step_grid_kernel RC:
-// 0 per-lane 8 B, 1 per-lane 16 B, 2 cp.async.bulk)
+// 0 per-lane 8 B; 1 per-lane 16 B, 4-warp CTAs; 2 per-lane 16 B, one-warp
+// CTAs; 3 = auto: 1 for dense launches of a wave or more, else 2)
 extern int g_rowcopy;
 void set_rowcopy(int rc);
+// warps of one full wave of the grid kernel (SMs x resident warps): smaller
+// launches take one-warp CTAs
+extern int g_grid_wave;
+void set_grid_wave(int warps);
 int max_tile_rows();
 int grid_resident_warps();   // resident warps per SM the grid kernel is compiled for
 int side_stride();

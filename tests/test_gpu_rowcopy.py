@@ -1,8 +1,9 @@
 """Row copies of the grid and vc kernels ("Row copies"):
-the 16-byte per-lane copies of interior strips (RC 1, the default where the
-layout allows it) and the per-lane 8-byte copies (RC 0, CLAW_ROWCOPY=0) feed
-the same arithmetic, so the results are bitwise equal; and both match the
-oracle.  Shapes cover patch widths where a 34-column ring row spans 1, 2 or 3
+the 16-byte per-lane copies of interior strips (RC 1 with 4-warp CTAs, RC 2
+with one-warp CTAs -- chosen by launch size where the layout allows them) and
+the per-lane 8-byte copies (RC 0, CLAW_ROWCOPY=0) feed the same arithmetic,
+so the results are bitwise equal; and all match the oracle.  The sparse
+lattice (RC 2 vs RC 0) is covered at the end.  Shapes cover patch widths where a 34-column ring row spans 1, 2 or 3
 patches (even widths 2 .. 130), levels just wider than one or two strips
 (edge strips fall back to 8-byte copies), tiles spanning patch rows, and both
 BCs.  CLAW_ROWCOPY is read when a context is created (one setting per
@@ -74,8 +75,9 @@ def test_grid_row_copies_bitwise(monkeypatch, npx, npy, mx, my, bc, limiter, ot)
     q0 = W.random_ic(d, 13 * mx + my)
     dt = (0.9 if ot else 0.45) * 2 / max(npx * mx, npy * my)
     q0c, c0 = run_grid(monkeypatch, 0, d, q0, bc, limiter, ot, dt, 6)
-    q1c, c1 = run_grid(monkeypatch, 1, d, q0, bc, limiter, ot, dt, 6)
-    assert np.array_equal(q0c, q1c) and c0 == c1
+    for rc in (1, 2):   # 16-byte copies with 4-warp / one-warp CTAs
+        q1c, c1 = run_grid(monkeypatch, rc, d, q0, bc, limiter, ot, dt, 6)
+        assert np.array_equal(q0c, q1c) and c0 == c1, rc
     assert rel_err(q1c, oracle_run(d, q0, bc, limiter, ot, dt, 6)) <= TOL
 
 
@@ -85,8 +87,9 @@ def test_grid_row_copies_spanning_tiles_bitwise(monkeypatch, th):
     q0 = W.random_ic(d, th)
     dt = 0.9 * 2 / 192
     a = run_grid(monkeypatch, 0, d, q0, W.EXTRAP, 4, 2, dt, 5, th=th)
-    b = run_grid(monkeypatch, 1, d, q0, W.EXTRAP, 4, 2, dt, 5, th=th)
-    assert np.array_equal(a[0], b[0]) and a[1] == b[1]
+    for rc in (1, 2):
+        b = run_grid(monkeypatch, rc, d, q0, W.EXTRAP, 4, 2, dt, 5, th=th)
+        assert np.array_equal(a[0], b[0]) and a[1] == b[1], rc
 
 
 @pytest.mark.parametrize("npx,npy,mx,my,bc", [(4, 3, 18, 16, W.PERIODIC), (2, 2, 34, 16, W.EXTRAP),
@@ -102,3 +105,24 @@ def test_vc_row_copies_bitwise(monkeypatch, npx, npy, mx, my, bc):
     b = run_grid(monkeypatch, 1, d, q0, bc, 4, 2, dt, 6, aux=aux)
     assert np.array_equal(a[0], b[0]) and a[1] == b[1]
     assert rel_err(b[0], oracle_run(d, q0, bc, 4, 2, dt, 6, aux=aux)) <= TOL
+
+
+def test_sparse_lattice_row_copies_bitwise(monkeypatch):
+    """The sparse-lattice grid kernel (C3's level 3) with 16-byte copies
+    (chunks from patch or virtual frame slots, one-warp CTAs) vs per-lane
+    8-byte copies: whole-hierarchy runs bitwise equal.  (The ratio-2 / 4
+    lattices of test_gpu_parity's sparse test run the default copies against
+    the generic kernel.)"""
+    wl = W.c3()
+    res = []
+    for rc in (0, 3):
+        monkeypatch.setenv("CLAW_ROWCOPY", str(rc))
+        g = binding.Claw(wl.domain, wl.bc, wl.limiter, wl.order_trans, device=0)
+        for L, (lv, q) in enumerate(zip(wl.levels, W.hierarchy_ic(wl)), start=1):
+            g.set_level(L, lv.descs, q)
+        assert g.level_mode(3) == "sparse"
+        dt = wl.dt0()
+        cfl = [g.advance_hierarchy(n * dt, dt, update=True) for n in range(3)]
+        res.append(([g.read_level(L) for L in range(1, 4)], cfl))
+        g.close()
+    assert all(np.array_equal(a, b) for a, b in zip(res[0][0], res[1][0])) and res[0][1] == res[1][1]
