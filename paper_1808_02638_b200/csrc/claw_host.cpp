@@ -1408,7 +1408,11 @@ int plan_level(claw_ctx* c, int level, Level& L) {
     L.grid = true;
     L.Y0 = 0;
     L.Y1 = L.ny;
-    const int th = std::min(L.th, my);
+    int th = std::min(L.th, my);
+    if (const char* e = std::getenv("CLAW_SPARSE_TH")) {  // tuning: rows per sparse-lattice tile
+      const int v = std::atoi(e);
+      if (v >= 4 && v <= my && my % v == 0) th = v;
+    }
     L.grid_th = th;
     const int nbr = (my + th - 1) / th;
     const int64_t npy = L.ny / my, nstrip = claw::grid_nstrip(L.nx);
