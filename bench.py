@@ -590,9 +590,11 @@ def main():
                 regrid(t + dt)
         t_sim[0] = t + dt
 
-    # fixed hierarchies (no regrid): K coarse steps per host synchronisation
-    # (claw_advance_hierarchy_n; the per-step CFLs come back together)
-    batch = nlev > 1 and not dyn and not args.regrid and args.batch > 1
+    # fixed hierarchies and single levels (no regrid): K coarse steps per host
+    # synchronisation (claw_advance_hierarchy_n; the per-step CFLs come back
+    # together and are checked afterwards, DESIGN.md section 8 "K coarse steps
+    # per host synchronisation")
+    batch = not dyn and not args.regrid and args.batch > 1 and not host_x
     cfl_seen = []
 
     def steps(n):
@@ -621,11 +623,12 @@ def main():
         torch.cuda.synchronize()
 
     # ---- device-resident timed region
-    # (one level: CUDA events around every step launch, for the roofline's
-    # per-launch time; a hierarchy's latency-bound coarse step would pay for
-    # them -- ~30 event records per coarse step -- so its per-launch times
-    # come from a profiled pass of the same length right after)
-    prof_live = nlev == 1
+    # (a bandwidth-bound level: CUDA events around every step launch, for the
+    # roofline's per-launch time; a latency-bound step -- a hierarchy's
+    # coarse step, ~30 event records, or C1's 40 us step -- would pay for
+    # them, so its per-launch times come from a profiled pass of the same
+    # length right after)
+    prof_live = nlev == 1 and total_cells_per_step >= (1 << 24)
     g.reset_stats()
     g.set_profiling(prof_live)
     clocks = ClockSampler(device)
@@ -764,7 +767,8 @@ def main():
                "h2d_bytes_per_step": state_bytes / args.steps + 8 * sum(mult),
                "d2h_bytes_per_step": state_bytes / args.steps + 8 * sum(mult),
                "ms": ems, "wall_ms": wall,
-               "what": "write_level (pinned host->device) + K x (fill_ghost + advance_level -> 8-byte cfl) "
+               "what": "write_level (pinned host->device) + K x (fill_ghost + advance_level -> 8-byte cfl"
+                       + (f", read back {args.batch} at a time" if batch else "") + ") "
                        "+ read_level (device->pinned host), per rank, max over ranks"
                        + ("; the static medium is set once before (claw_set_aux, problem setup)" if vc else "")}
 

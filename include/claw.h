@@ -260,7 +260,10 @@ int claw_reflux_registers(claw_ctx* ctx, int32_t level, int64_t* n, int32_t* edg
  * time; with CLAW_HIER_UPDATE in flags, level L+1 is averaged onto level L
  * after its R_L steps.  Runs entirely on the library's stream with one host
  * synchronisation at the end; *cfl_max receives the max Courant number over
- * all level steps.  Ratios are taken from the levels' dx. */
+ * all level steps.  Ratios are taken from the levels' dx.  With world > 1
+ * that value is reduced across ranks once per call (one 8-byte NCCL max
+ * all-reduce per call, not per level step); the levels' own CFL slots
+ * (claw_wait_cfl) then hold rank-local maxima. */
 int claw_advance_hierarchy(claw_ctx* ctx, double t, double dt, int32_t flags, double* cfl_max);
 /* nsteps consecutive coarse steps at the fixed dt (times t + k dt), each
  * exactly as claw_advance_hierarchy would run it, with ONE host
@@ -270,7 +273,10 @@ int claw_advance_hierarchy(claw_ctx* ctx, double t, double dt, int32_t flags, do
  * nsteps doubles) receives the max Courant number of coarse step k.  The
  * caller checks them afterwards (dt_next = dt nu / cfl; a step
  * with cfl > 1 is to be retaken from saved data, as for the single-step
- * call).  EINVAL: nsteps < 1 or cfl_out NULL. */
+ * call).  With world > 1 the nsteps values are reduced across ranks by one
+ * all-reduce at the end.  A single level (level 1 only) is a valid
+ * hierarchy: K level steps per host synchronisation.  EINVAL: nsteps < 1 or
+ * cfl_out NULL. */
 int claw_advance_hierarchy_n(claw_ctx* ctx, double t, double dt, int32_t nsteps, int32_t flags, double* cfl_out);
 int claw_level_owned(const claw_ctx* ctx, int32_t level, int32_t* npatch_owned,
                      int64_t* cells_owned, int64_t* device_bytes);

@@ -2401,7 +2401,11 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
       ctx->stats.ghost_launches++;
     }
   }
-  if (ctx->cfg.world > 1 && ctx->cfg.exchange == 0) {
+  // the level's CFL all-reduce; inside a hierarchy call the step's Courant
+  // number also lands in the hierarchy slot, reduced once for the whole call
+  // (one all-reduce per claw_advance_hierarchy[_n] instead of one per level
+  // step, which nothing overlaps), so the level slot stays rank-local there
+  if (ctx->cfg.world > 1 && ctx->cfg.exchange == 0 && !ctx->hier_slot) {
     Nvtx nv_red("claw_cfl_allreduce");
     ncclResult_t nr = g_nccl.AllReduce(L.lcfl.p + g, L.lcfl.p + g, 1, ncclFloat64, ncclMax, ctx->comm, ctx->stream);
     if (nr != ncclSuccess) return nccl_fail(ctx, nr, "ncclAllReduce(cfl, max)");

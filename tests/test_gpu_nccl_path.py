@@ -30,18 +30,26 @@ import sys, numpy as np
 sys.path.insert(0, sys.argv[1])
 from paper_1808_02638_b200 import binding, workloads as W
 rank, world, idhex, name, bcs, out = int(sys.argv[2]), int(sys.argv[3]), sys.argv[4], sys.argv[5], sys.argv[6], sys.argv[7]
+driver = sys.argv[8]
 bc = tuple(int(x) for x in bcs.split(","))
-d = W.c5(patches_per_side=6, mx=32).levels[0].descs if name == "uniform" else W.ragged_level(6, 90, 70, 30)
+d = W.c5(patches_per_side=6, mx=32).levels[0].descs if name in ("uniform", "vc") else W.ragged_level(6, 90, 70, 30)
 q0 = W.random_ic(d, 77)
 offs = W.level_offsets(d)
 owners = binding.partition(d, world)
 g = binding.Claw(W.DOMAIN, bc, 4, 2, device=0, rank=rank, world=world, nccl_id=bytes.fromhex(idhex))
 g.set_level(1, d, np.concatenate([q0[offs[p]:offs[p + 1]] for p in range(len(d)) if owners[p] == rank]))
 dt = 0.9 * float(d["dx"][0])
+if name == "vc":
+    aux = W.media_field(d)
+    g.set_aux(1, aux)
+    dt /= W.max_sound_speed(aux, d)
 cfl = []
-for n in range(5):
-    g.fill_ghost(1, n * dt)
-    cfl.append(g.advance_level(1, dt))
+if driver == "batch":
+    cfl = g.advance_hierarchy_n(0.0, dt, 5).tolist()
+else:
+    for n in range(5):
+        g.fill_ghost(1, n * dt)
+        cfl.append(g.advance_level(1, dt))
 np.save(out, g.read_level(1))
 np.save(out + ".cfl.npy", np.array(cfl))
 print("mode", g.level_mode(1))
@@ -59,9 +67,19 @@ def shim(tmp_path_factory):
     return out
 
 
-@pytest.mark.parametrize("world,name,bc", [(2, "uniform", W.EXTRAP), (3, "uniform", W.PERIODIC),
-                                           (2, "ragged", W.PERIODIC), (4, "ragged", (1, 1, 2, 2))])
-def test_nccl_path_processes_bitwise_equal_single_rank(shim, tmp_path, world, name, bc):
+@pytest.mark.parametrize("world,name,bc,driver", [(2, "uniform", W.EXTRAP, "level"), (3, "uniform", W.PERIODIC, "level"),
+                                                  (2, "ragged", W.PERIODIC, "level"),
+                                                  (4, "ragged", (1, 1, 2, 2), "level"),
+                                                  (3, "uniform", W.EXTRAP, "batch"),
+                                                  (2, "ragged", W.PERIODIC, "batch"),
+                                                  (4, "vc", W.EXTRAP, "level"), (4, "vc", W.EXTRAP, "batch")])
+def test_nccl_path_processes_bitwise_equal_single_rank(shim, tmp_path, world, name, bc, driver):
+    """driver "level": claw_advance_level per step (the CFL all-reduce of
+    every level step); "batch": claw_advance_hierarchy_n of the single level
+    (K steps per host synchronisation, one all-reduce of the K per-step CFLs
+    at the end).  "vc": a layered medium whose max sound speed differs
+    between the ranks' bands, so only the reduction gives every rank the
+    global CFL."""
     env = dict(os.environ, CLAW_NCCL_LIB=shim)
     # the unique id comes from the same library call rank 0 would make
     gen = subprocess.run([sys.executable, "-c",
@@ -73,21 +91,25 @@ def test_nccl_path_processes_bitwise_equal_single_rank(shim, tmp_path, world, na
     script.write_text(WORKER)
     bcs = ",".join(str(x) for x in bc)
     procs = [subprocess.Popen([sys.executable, str(script), ROOT, str(r), str(world), idhex, name, bcs,
-                               str(tmp_path / f"rank{r}.npy")], env=env, stdout=subprocess.PIPE,
+                               str(tmp_path / f"rank{r}.npy"), driver], env=env, stdout=subprocess.PIPE,
                               stderr=subprocess.PIPE, text=True) for r in range(world)]
     outs = [p.communicate(timeout=600) for p in procs]
     for p, (so, se) in zip(procs, outs):
         assert p.returncode == 0, se[-3000:]
     modes = {so.strip().splitlines()[-1] for so, _ in outs}
-    assert modes == {"mode grid" if name == "uniform" else "mode generic"}, modes
+    assert modes == {"mode generic" if name == "ragged" else "mode grid"}, modes
     # the one-rank reference
-    d = W.c5(patches_per_side=6, mx=32).levels[0].descs if name == "uniform" else W.ragged_level(6, 90, 70, 30)
+    d = W.c5(patches_per_side=6, mx=32).levels[0].descs if name in ("uniform", "vc") else W.ragged_level(6, 90, 70, 30)
     q0 = W.random_ic(d, 77)
     offs = W.level_offsets(d)
     owners = binding.partition(d, world)
     ref = binding.Claw(W.DOMAIN, bc, 4, 2, device=0)
     ref.set_level(1, d, q0)
     dt = 0.9 * float(d["dx"][0])
+    if name == "vc":
+        aux = W.media_field(d)
+        ref.set_aux(1, aux)
+        dt /= W.max_sound_speed(aux, d)
     cfl = []
     for n in range(5):
         ref.fill_ghost(1, n * dt)
@@ -98,3 +120,11 @@ def test_nccl_path_processes_bitwise_equal_single_rank(shim, tmp_path, world, na
         mine = np.concatenate([full[offs[p]:offs[p + 1]] for p in range(len(d)) if owners[p] == r])
         assert np.array_equal(np.load(tmp_path / f"rank{r}.npy"), mine), r
         assert np.load(tmp_path / f"rank{r}.npy.cfl.npy").tolist() == cfl
+    if name == "vc":  # the bands' own maxima differ: the CFL really was reduced
+        local = []
+        for r in range(world):
+            sub = d[owners == r]
+            ao = offs // 3 * 2   # (rho, K) per cell; offs counts (p, u, v)
+            a_r = np.concatenate([aux[ao[p]:ao[p + 1]] for p in range(len(d)) if owners[p] == r])
+            local.append(W.max_sound_speed(a_r, sub))
+        assert len(set(local)) > 1, local
