@@ -43,6 +43,7 @@ namespace {
 
 constexpr int kMaxLevel = 8;
 constexpr int kBucket = 16;
+constexpr int kBandEdge = 4;   // band split: rows of each edge tile (a multiple of 4)
 
 // ---------------------------------------------------------------------------
 // NCCL through dlopen: the library loads without NCCL; world > 1 needs it.
@@ -442,6 +443,9 @@ struct Level {
   int64_t ngrid_tiles = 0;
   int64_t ngrid_blocks = 0;   // row blocks of the band (grid mode)
   int grid_th = 0;            // rows per grid tile (> my: tiles span patch rows)
+  int band_te = 0;            // band split (world > 1): rows of each edge tile (0: row blocks)
+  int grid_th_int = 0;        // band split: rows per interior tile
+  int64_t ngrid_blocks_int = 0;
   bool use_side = false;      // generic kernel: side records by a side_kernel ahead of the step
   bool sparse = false;        // grid kernel on a sparse lattice of equal patches
   std::vector<int32_t> hslots;  // lattice slot -> patch (>= 0) or -1-v (virtual slot v)
@@ -1485,6 +1489,40 @@ int plan_level(claw_ctx* c, int level, Level& L) {
       const int64_t nstrip = claw::grid_nstrip(L.nx);
       L.ngrid_blocks = th > my ? ((L.Y1 - L.Y0) + th - 1) / th : ((L.Y1 - L.Y0) / my) * ((my + th - 1) / th);
       L.ngrid_tiles = nstrip * L.ngrid_blocks;
+      // band split (world > 1): every step is an interior launch, which runs
+      // while the halo is in flight, and an edge launch after it lands.  The
+      // edge launch takes only the kBandEdge rows at each end of the band
+      // (the rows whose stencil reaches a halo row), so nearly all the work
+      // is in the interior launch, whose tile height is chosen by the same
+      // makespan rule over the band minus its edges (split into row blocks
+      // instead, the edge launch would hold a third of the band as a second,
+      // sub-wave launch: DESIGN.md section 9).  Tiles of the interior start
+      // kBandEdge rows into a patch row, so my >= 16 keeps a tile's first
+      // ring rows inside one patch row (the kernels' prologue).
+      L.band_te = 0;
+      if (L.band && my >= 16 && my % 4 == 0 && L.Y1 - L.Y0 >= 4 * kBandEdge) {
+        L.band_te = kBandEdge;
+        const int64_t slots = static_cast<int64_t>(c->nsm) * claw::grid_resident_warps();
+        const int64_t rows = L.Y1 - L.Y0 - 2 * kBandEdge;
+        int thi = my;
+        double best = -1.0;
+        for (int w = my; w <= 512; w += my) {
+          const int64_t tiles = nstrip * ((rows + w - 1) / w);
+          if (tiles < slots && w > my) continue;
+          const double cost = static_cast<double>((tiles + slots - 1) / slots) * (w + 4);
+          if (best < 0 || cost <= best) {
+            best = cost;
+            thi = w;
+          }
+        }
+        if (const char* e = std::getenv("CLAW_GRID_TH")) {
+          if (span_ok(std::atoi(e)) || std::atoi(e) == my) thi = std::atoi(e);
+        } else if (c->cfg.tile_rows > 0 && (span_ok(c->cfg.tile_rows) || c->cfg.tile_rows == my)) {
+          thi = c->cfg.tile_rows;
+        }
+        L.grid_th_int = thi;
+        L.ngrid_blocks_int = (rows + thi - 1) / thi;
+      }
     }
   }
   // generic tiles: strips of 30 columns for the halo-lane kernel (default;
@@ -2320,6 +2358,9 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
     }
     P.Y0 = static_cast<int32_t>(L.Y0);
     P.Y1 = static_cast<int32_t>(L.Y1);
+    P.span = L.grid_th > L.desc[0].my ? 1 : 0;
+    P.R0 = P.Y0;
+    P.R1 = P.Y1;
     for (int k = 0; k < 4; ++k) {
       P.hoff[k] = L.hoff[k];
       P.hcs[k] = L.hcs[k];
@@ -2337,7 +2378,23 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
     // landed -- the edge tiles
     claw::StepParams Pi = P, Pe = P;
     int64_t n_int = 0, n_all = 0;
-    if (L.grid) {
+    if (L.grid && L.band_te > 0) {
+      // interior: rows [Y0 + te, Y1 - te); edge: the te rows at each end
+      const int64_t nstrip = claw::grid_nstrip(L.nx);
+      const int te = L.band_te;
+      Pi.span = 1;
+      Pi.th = L.grid_th_int;
+      Pi.R0 = P.Y0 + te;
+      Pi.R1 = P.Y1 - te;
+      Pi.ntiles = static_cast<int32_t>(nstrip * L.ngrid_blocks_int);
+      Pe.span = 1;
+      Pe.th = te;
+      Pe.blk_first = 0;
+      Pe.blk_stride = (P.Y1 - P.Y0) / te - 1;
+      Pe.ntiles = static_cast<int32_t>(nstrip * 2);
+      n_int = 1;
+      n_all = 1;
+    } else if (L.grid) {
       const int64_t nstrip = claw::grid_nstrip(L.nx);
       const int64_t nb = L.ngrid_blocks;
       if (nb >= 3) {

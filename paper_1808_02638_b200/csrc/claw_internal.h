@@ -84,7 +84,11 @@ struct StepParams {
   // row-major order, gapless buffer): level-index strips, no tables
   int32_t grid;
   int32_t NX, NY, mx, my, npx;    // level extent, patch size, patches per row
-  int32_t th;                     // rows per tile (tiles stay in one patch row)
+  int32_t th;                     // rows per tile (tiles stay in one patch row unless span)
+  int32_t span;                   // 1: row block b is rows [R0 + b th, min(R0 + (b+1) th, R1))
+                                  // and tiles may span patch rows (th > my, or a band-split
+                                  // launch); 0: blocks of th rows inside each patch row
+  int32_t R0, R1;                 // span: the launch's row range (whole band: Y0, Y1)
   int32_t per_x, per_y;           // periodic in x / y
   int32_t Y0, Y1;                 // this rank's band of level rows (whole level: 0, NY)
   int32_t blk_first, blk_stride;  // grid tiles: row block = blk_first + k*blk_stride,

@@ -50,7 +50,7 @@ __device__ __forceinline__ void vc_ptrs(const StepParams& P, int C, int J, const
 }
 
 // 1/x for the positive, normal x of this kernel (impedance sums, Z^2 + 1):
-// the SFU's reciprocal estimate (~2^-22) and two Newton steps (error ~2^-88,
+// the SFU's reciprocal estimate (~2^-20 measured) and one cubic step (error ~2^-60,
 // i.e. the last bit of the double), no special-case branch; the rounding may
 // differ from the correctly rounded __drcp_rn by one ulp (parity is by
 // tolerance, R20)
@@ -73,13 +73,24 @@ __device__ __forceinline__ void vc_src(const StepParams& P, int C, int J, const 
   ca = P.NX;
 }
 
+#ifndef CLAW_VC_RCP3
+#define CLAW_VC_RCP3 1
+#endif
 __device__ __forceinline__ double vc_rcp(double x) {
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   double e = __fma_rn(-x, y, 1.0);
+#if CLAW_VC_RCP3
+  // one cubic step instead of two Newton steps: with e = 1 - x y0 (exact up
+  // to one rounding of a ~2^-22 quantity), 1/x = y0 (1 + e + e^2 + ...), so
+  // y0 + y0 (e + e^2) leaves ~e^3 ~ 2^-66 relative before its final rounding
+  // -- the accuracy of two Newton steps in three dependent FMAs, not four
+  return __fma_rn(y, __fma_rn(e, e, e), y);
+#else
   y = __fma_rn(y, e, y);
   e = __fma_rn(-x, y, 1.0);
   return __fma_rn(y, e, y);
+#endif
 }
 
 // Row copies as in the grid kernel's RC 1: the rows inside the tile of an
@@ -107,7 +118,7 @@ __global__ void __launch_bounds__(32 * CLAW_VC_KW, CLAW_VC_RES_WARPS / CLAW_VC_K
   const int t = blockIdx.x * KW + warp;
   const int nstrip = (P.NX + kStrip - 1) / kStrip;
   const int myv = P.my, mx = P.mx;
-  const bool span = P.th > myv;
+  const bool span = P.span != 0;
   griddep_wait();
   if (blockIdx.x == 0 && threadIdx.x == 0 && P.level_cfl_reset) *P.level_cfl_reset = 0ull;
   if (t >= P.ntiles) return;
@@ -115,8 +126,8 @@ __global__ void __launch_bounds__(32 * CLAW_VC_KW, CLAW_VC_RES_WARPS / CLAW_VC_K
   const int b = P.blk_first + (t / nstrip) * P.blk_stride;
   int j0, th;
   if (span) {
-    j0 = P.Y0 + b * P.th;
-    th = min(P.th, P.Y1 - j0);
+    j0 = P.R0 + b * P.th;
+    th = min(P.th, P.R1 - j0);
   } else {
     const int nbr = (myv + P.th - 1) / P.th;
     const int prow = b / nbr, r0 = (b - prow * nbr) * P.th;

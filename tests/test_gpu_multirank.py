@@ -118,3 +118,57 @@ def test_virtual_ranks_variable_media_bitwise_equal_single_rank(world, npx, mx, 
         for p in range(len(d)):
             if owners[p] == r:
                 assert c.patch_cfl(1, p) == ref.patch_cfl(1, p)
+
+
+@pytest.mark.parametrize("world,npx,mx,tile_rows,bc,media", [
+    (2, 16, 32, 0, W.EXTRAP, False), (4, 16, 32, 64, W.PERIODIC, False), (4, 16, 32, 96, (1, 1, 2, 2), False),
+    (3, 12, 16, 48, W.EXTRAP, False), (2, 8, 64, 128, W.PERIODIC, False), (8, 16, 32, 32, W.EXTRAP, False),
+    (4, 16, 32, 64, W.EXTRAP, True), (2, 8, 64, 128, (1, 1, 2, 2), True)])
+def test_band_split_tiles_bitwise_equal_single_rank(world, npx, mx, tile_rows, bc, media, monkeypatch):
+    """Band split: each rank's step is an interior
+    launch over rows [Y0 + 4, Y1 - 4) -- tiles of tile_rows rows that start 4
+    rows into a patch row and span patch rows -- and an edge launch of the 4
+    rows at each end of the band, after the halo.  With the grid kernel and
+    the variable-media kernel, N ranks are bitwise the one-rank run.
+    tile_rows: the interior tile height (CLAW_GRID_TH; 0 = the makespan rule)."""
+    if tile_rows:
+        monkeypatch.setenv("CLAW_GRID_TH", str(tile_rows))
+    d = W.uniform_level(npx, npx, mx, mx)
+    q0 = W.random_ic(d, 11 * world + mx)
+    aux = W.random_media(d, 3 * world, 0.4, 2.5) if media else None
+    offs = W.level_offsets(d)
+    owners = binding.partition(d, world)
+    ctxs = []
+    for r in range(world):
+        c = binding.Claw(W.DOMAIN, bc, 4, 2, device=0, rank=r, world=world, exchange=1)
+        c.set_level(1, d, np.concatenate([q0[offs[p]:offs[p + 1]] for p in range(len(d)) if owners[p] == r]))
+        assert c.level_mode(1) == "grid"
+        if media:
+            c.set_aux(1, aux)
+        ctxs.append(c)
+    ref = binding.Claw(W.DOMAIN, bc, 4, 2, device=0)
+    ref.set_level(1, d, q0)
+    dt = 0.9 * float(d["dx"][0])
+    if media:
+        ref.set_aux(1, aux)
+        dt = 0.8 * float(d["dx"][0]) / W.max_sound_speed(aux, d)
+    for n in range(5):
+        for c in ctxs:
+            c.fill_ghost(1, n * dt)
+        for r in range(world):
+            for s in range(world):
+                if r != s:
+                    ctxs[s].halo_unpack(1, r, ctxs[r].halo_pack(1, s))
+        st0 = [c.stats()["step_launches"] for c in ctxs]
+        cfl = max(c.advance_level(1, dt) for c in ctxs)
+        # two launches per rank and step: interior tiles, then edge tiles
+        assert [c.stats()["step_launches"] - s0 for c, s0 in zip(ctxs, st0)] == [2] * world
+        ref.fill_ghost(1, n * dt)
+        assert cfl == ref.advance_level(1, dt)
+    full = ref.read_level(1)
+    for r, c in enumerate(ctxs):
+        want = np.concatenate([full[offs[p]:offs[p + 1]] for p in range(len(d)) if owners[p] == r])
+        assert np.array_equal(c.read_level(1), want), r
+    ref.close()
+    for c in ctxs:
+        c.close()
