@@ -1,0 +1,14 @@
+#!/bin/bash
+# lane kernel prologue (both initial segments inline), update_rect_kernel<R> (all child loads before the adds), interp_kernel (30 donor loads first; static tables before the PDL wait) vs previous build
+OUT=gpurun_out/r02_bi; mkdir -p $OUT
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_lane.py tests/test_gpu_paper.py tests/test_gpu_long.py tests/test_gpu_regrid.py tests/test_gpu_reflux.py tests/test_gpu_graph.py -q -x > $OUT/tests.log 2>&1; echo "rc=$?" >> $OUT/tests.log
+for i in 1 2; do
+  for v in base gridpro; do
+    lib=build/variants/libclaw_$v.so; [ $v = base ] && lib=paper_1808_02638_b200/libclaw.so
+    for c in c3 c2; do CLAW_LIB=$lib timeout 600 python bench.py --config $c --steps 100 --warmup 10 --no-cpu-baseline --no-e2e > $OUT/${c}_${v}_$i.json 2> $OUT/${c}_${v}_$i.err; done
+    CLAW_LIB=$lib timeout 600 python bench.py --config c4 --steps 50 --warmup 5 --no-cpu-baseline --no-e2e > $OUT/c4_${v}_$i.json 2> $OUT/c4_${v}_$i.err
+    CLAW_LIB=$lib timeout 600 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --no-e2e > $OUT/c5_${v}_$i.json 2> $OUT/c5_${v}_$i.err
+  done
+done
+tail -n 2 $OUT/tests.log
+for f in $OUT/c*_*.json; do echo "$(basename $f .json) $(python -c "import json; j=json.load(open('$f')); print(round(j['value']/1e9,3), 'ms_per_step', round(j['ms_per_step'],4))" 2>&1 | tail -1)"; done
