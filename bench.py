@@ -697,6 +697,8 @@ def main():
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
             "kernel": (f"step_vc_kernel<{LIMNAME[wl.limiter]},{wl.order_trans}>" if vc else
                        f"step_grid_kernel<{LIMNAME[wl.limiter]},{wl.order_trans}>" if g.level_mode(1) == "grid" and nlev == 1
+                       else "level step kernels, mean per level launch (" +
+                       ", ".join(f"L{L} {g.level_mode(L)}" for L in range(1, nlev + 1)) + ")" if nlev > 1
                        else f"step_kernel<{LIMNAME[wl.limiter]},{wl.order_trans},uniform>"),
             "bytes_per_cell": bpc,
             "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,

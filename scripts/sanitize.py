@@ -9,6 +9,9 @@ synccheck, initcheck); see scripts/gpu_sanitize.sh.
   regrid   flag / dilate / sat / regrid kernels (claw_regrid_auto)
   vc       step_vc_kernel (variable media): a small grid, spanning tiles, the
            non-finite check
+  band     band-split launches (interior rows [Y0+4, Y1-4), then the 4-row
+           edge tiles) of the grid and vc kernels: 2 virtual ranks, external
+           exchange
 """
 import os
 import sys
@@ -16,7 +19,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1808_02638_b200 import binding, workloads as W  # noqa: E402
 
-what = sys.argv[1:] or ["grid", "generic", "hier", "regrid", "vc"]
+what = sys.argv[1:] or ["grid", "generic", "hier", "regrid", "vc", "band"]
 
 if "grid" in what:
     for d, bc in ((W.c1().levels[0].descs, W.EXTRAP), (W.uniform_level(8, 8, 32, 32), W.PERIODIC)):
@@ -94,3 +97,32 @@ if "vc" in what:
         g.read_level(1)
         g.close()
     print("vc ok")
+
+if "band" in what:
+    import numpy as np
+    d = W.uniform_level(8, 8, 32, 32)
+    offs = W.level_offsets(d)
+    for media in (False, True):
+        world = 2
+        owners = binding.partition(d, world)
+        q0 = W.random_ic(d, 4)
+        ctxs = []
+        for r in range(world):
+            c = binding.Claw(W.DOMAIN, W.EXTRAP, 4, 2, device=0, rank=r, world=world, exchange=1)
+            c.set_level(1, d, np.concatenate([q0[offs[p]:offs[p + 1]] for p in range(len(d)) if owners[p] == r]))
+            if media:
+                c.set_aux(1, W.random_media(d, 5))
+            ctxs.append(c)
+        for n in range(2):
+            for c in ctxs:
+                c.fill_ghost(1, 0.0)
+            for r in range(world):
+                for s_ in range(world):
+                    if r != s_:
+                        ctxs[s_].halo_unpack(1, r, ctxs[r].halo_pack(1, s_))
+            for c in ctxs:
+                c.advance_level(1, 0.3 * float(d["dx"][0]))
+        for c in ctxs:
+            c.read_level(1)
+            c.close()
+    print("band ok")
