@@ -1391,16 +1391,21 @@ int plan_level(claw_ctx* c, int level, Level& L) {
     if (L.hpatch[lp].c != L.hpatch[0].c || L.hpatch[lp].Z != L.hpatch[0].Z) L.uniform = false;
   // rows per tile: the configured value, or (auto) the largest power of two
   // <= 64 that still gives ~half a tile per resident warp of the GPU (SMs
-  // x 16 warps); small, latency-bound levels get short tiles (>= 8) so the
+  // x 16 warps); small, latency-bound levels get short tiles (>= 4) so the
   // serial row march of each warp stays short (measured: C3's level 3 runs
   // 2.5% faster with 32-row tiles at 0.7 tiles per warp than with 16-row
-  // ones, C1/C2 fastest at 8; profiles/r01_tile_rows_c123.txt)
+  // ones, profiles/r01_tile_rows_c123.txt; a floor of 4 rows instead of 8:
+  // C2 0.061 -> 0.056 ms, C1 0.0089 -> 0.0084 ms per step, C3 and the paper
+  // workload unchanged, profiles/r02_min_tile_rows.txt)
   if (c->cfg.tile_rows > 0) {
     L.th = c->tile_rows;
   } else {
     const int64_t want = static_cast<int64_t>(c->nsm) * 8;
+    int min_th = 4;
+    if (const char* e = std::getenv("CLAW_MIN_TH"))   // tuning: smallest auto tile height (4 or 8)
+      if (std::atoi(e) == 4 || std::atoi(e) == 8) min_th = std::atoi(e);
     int th = 64;
-    while (th > 8 && L.cells_owned / (32ll * th) < want) th /= 2;
+    while (th > min_th && L.cells_owned / (32ll * th) < want) th /= 2;
     L.th = th;
   }
   // grid mode: whole domain tiled by equal patches in row-major order, gapless
