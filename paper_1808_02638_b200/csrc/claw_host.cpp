@@ -375,6 +375,7 @@ struct Level {
   // host tables
   std::vector<DevPatch> hpatch;
   std::vector<DevRect> hrect;
+  int64_t ncellrect = 0;           // entries of the ghost-cell rectangle map (DevPatch::crect)
   std::vector<int4> htile;
   int lane_tiles = 0;         // generic tiles: 30-column strips for step_lane_kernel
   std::vector<DevInterp> hinterp;
@@ -394,6 +395,7 @@ struct Level {
   DevBuf<double> frame;
   DevBuf<DevPatch> dpatch;
   DevBuf<DevRect> drect;
+  DevBuf<int32_t> dcellrect;
   DevBuf<int4> dtile;
   DevBuf<DevInterp> dinterp;
   DevBuf<unsigned long long> pcfl;  // per owned patch
@@ -1363,6 +1365,7 @@ int plan_level(claw_ctx* c, int level, Level& L) {
     d.rect_begin = static_cast<int32_t>(L.hrect.size());
     L.hrect.insert(L.hrect.end(), rects_p[lp].begin(), rects_p[lp].end());
     d.rect_end = static_cast<int32_t>(L.hrect.size());
+    d.crect = -1;   // (set below for levels the halo-lane kernel steps)
     // regions: strips W (i in [-2,0), j in [0,my)), E, S, N and 2x2 corners
     // SW, SE, NW, NE, each covered by one rectangle (or -1)
     const int X0 = -2, X1 = 0, X2 = d.mx, X3 = d.mx + 2, Y0 = -2, Y1 = 0, Y2 = d.my, Y3 = d.my + 2;
@@ -1555,6 +1558,20 @@ int plan_level(claw_ctx* c, int level, Level& L) {
       L.lane_tiles = (5 * n30 <= 6 * n32 || t30 <= static_cast<int64_t>(c->nsm) * 16) ? 1 : 0;
     }
   }
+  // each ghost cell's rectangle (the rectangles partition the frame ring),
+  // for the levels the halo-lane kernel steps: it resolves a column segment
+  // with one table load instead of searching the patch's rectangle list
+  // (ragged levels whose ghost strips have several donors have no single
+  // region rectangle; the search was the paper workload's top stall)
+  // (offsets here; the map itself is written on the device from the
+  // rectangle list, launch_cellrect in alloc_level: building it on the host
+  // cost the paper workload ~1.5 ms per regrid)
+  L.ncellrect = 0;
+  if (L.lane_tiles && !L.grid)
+    for (size_t lp = 0; lp < L.owned.size(); ++lp) {
+      L.hpatch[lp].crect = L.ncellrect;
+      L.ncellrect += frame_size(L.hpatch[lp].mx, L.hpatch[lp].my);
+    }
   const int tstrip = L.lane_tiles ? 30 : 32;
   // halo-lane tiles take at most 32 rows: measured 1.3% faster per coarse
   // step on the paper workload's fine levels than 64 (more, shorter marches
@@ -1821,6 +1838,15 @@ int alloc_level(claw_ctx* ctx, int level, Level& L) {
   CUDA_TRY(L.frame.alloc(std::max<int64_t>(L.frame_elems, 1) * L.nslice));
   if (int r2 = upload(ctx, L.dpatch, L.hpatch)) return r2;
   if (int r2 = upload(ctx, L.drect, L.hrect)) return r2;
+  if (L.ncellrect > 0) {
+    // (on the legacy stream, after the pageable uploads of the patch and
+    // rectangle tables it reads, and waited for: the step kernels on the
+    // library's stream read the map)
+    CUDA_TRY(L.dcellrect.alloc(static_cast<size_t>(L.ncellrect)));
+    CUDA_TRY(static_cast<cudaError_t>(claw::launch_cellrect(L.dpatch.p, static_cast<int32_t>(L.hpatch.size()),
+                                                            L.drect.p, L.dcellrect.p, nullptr)));
+    CUDA_TRY(cudaStreamSynchronize(nullptr));
+  }
   if (int r2 = upload(ctx, L.dtile, L.htile)) return r2;
   if (int r2 = upload(ctx, L.dinterp, L.hinterp)) return r2;
   if (int r2 = upload(ctx, L.du, L.hu)) return r2;
@@ -2332,6 +2358,7 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
   P.patches = L.dpatch.p;
   P.rects = L.drect.p;
   P.tiles = L.dtile.p;
+  P.cellrect = L.ncellrect > 0 ? L.dcellrect.p : nullptr;
   P.ntiles = static_cast<int32_t>(L.htile.size());
   P.lane_tiles = L.lane_tiles;
   P.limiter = ctx->cfg.limiter;
@@ -3236,6 +3263,7 @@ int flag_device(claw_ctx* ctx, int level, double tol, int buffer, int clip, DevB
   P.frame = L.frame.p + static_cast<int64_t>(L.fsel) * L.frame_elems;
   P.patches = L.dpatch.p;
   P.rects = L.drect.p;
+  P.cellrect = L.ncellrect > 0 ? L.dcellrect.p : nullptr;
   CUDA_TRY(static_cast<cudaError_t>(claw::launch_flag(P, orig.p, static_cast<int32_t>(L.owned.size()), L.nx, tol,
                                                       raw.p, on.p, ctx->stream)));
   const uint8_t* mask = nullptr;

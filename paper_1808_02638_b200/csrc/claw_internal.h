@@ -19,8 +19,11 @@ struct DevPatch {
                       // SW, SE, NW, NE 2x2 corner block, or -1 (search the list)
   double dx, dy;
   double c, Z;        // sound speed sqrt(K/rho), impedance rho*c
+  int64_t crect;      // offset of this patch's ghost-frame rectangle map in the level's
+                      // cell-rect table (one int32 rectangle index per ghost cell, frame
+                      // ring order), or -1
 };
-static_assert(sizeof(DevPatch) == 96, "DevPatch layout");
+static_assert(sizeof(DevPatch) == 104, "DevPatch layout");
 
 // Ghost-source rectangle: patch-local cells (i, j) with i0 <= i < i0+w,
 // j0 <= j < j0+h (0-based, ghosts are -2..-1 and mx..mx+1) take their value
@@ -69,6 +72,7 @@ struct StepParams {
   const double* frame;    // frame buffer
   const DevPatch* patches;
   const DevRect* rects;
+  const int32_t* cellrect;        // generic levels: per ghost cell its rectangle (DevPatch::crect)
   const int4* tiles;
   int32_t ntiles;
   int32_t limiter, order_trans;
@@ -123,6 +127,9 @@ int launch_interp(const double* q_old, const double* q_new, const double* alphas
 // debug check (claw_config.check_finite): atomicMax(flag, level) if any of
 // q[0..n) is NaN or +-Inf
 int launch_nonfinite(const double* q, int64_t n, int level, int32_t* flag, void* stream);
+// the ghost-cell rectangle map of a generic level (DevPatch::crect; one CTA
+// per patch, every cell of every rectangle of the patch)
+int launch_cellrect(const DevPatch* patches, int32_t npatch, const DevRect* rects, int32_t* map, void* stream);
 int launch_pack(const double* q, const int64_t* off, const int64_t* cs, int64_t n,
                 double* out, void* stream);
 int launch_gather_padded(const double* q, const double* frame, const DevPatch* patches,
