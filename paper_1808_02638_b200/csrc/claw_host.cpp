@@ -1113,7 +1113,9 @@ int plan_level(claw_ctx* c, int level, Level& L) {
       need[p] = touch;
     }
 
-  L.hinterp.clear();
+  // (L.hinterp keeps its previous contents here: the one-rank path below
+  // overwrites every entry it keeps, so a regrid does not zero-fill tens of
+  // MB of interpolation specs first)
   L.dbg_src.assign(L.owned.size(), {});
   L.dbg_remote.assign(L.owned.size(), {});
 
@@ -1252,14 +1254,21 @@ int plan_level(claw_ctx* c, int level, Level& L) {
   lap("ghosts");
   // coarse donors of a frame slot: centre, x-, x+, y-, y+ (coarse composite
   // via clamp/wrap)
-  auto make_spec = [&](const Pending& pd, int64_t slot, DevInterp& sp, std::string& emsg) -> int {
+  // (hint: the coarse patch of the previous donor -- a ghost cell's five
+  // donors and the next ghost cell's are nearly always in one coarse patch,
+  // so most lookups skip the bucket search; same result as C->find)
+  auto make_spec = [&](const Pending& pd, int64_t slot, DevInterp& sp, std::string& emsg, int& hint) -> int {
     sp = DevInterp{};
     const int64_t cI[5] = {pd.Ic, map_axis(pd.Ic - 1, C->nx, cfg.bc[0], cfg.bc[1]),
                            map_axis(pd.Ic + 1, C->nx, cfg.bc[0], cfg.bc[1]), pd.Ic, pd.Ic};
     const int64_t cJ[5] = {pd.Jc, pd.Jc, pd.Jc, map_axis(pd.Jc - 1, C->ny, cfg.bc[2], cfg.bc[3]),
                            map_axis(pd.Jc + 1, C->ny, cfg.bc[2], cfg.bc[3])};
     for (int d = 0; d < 5; ++d) {
-      const int q = C->find(cI[d], cJ[d]);
+      const int h = hint;
+      const bool in_h = h >= 0 && cI[d] >= C->i0[h] && cI[d] < C->i0[h] + C->desc[h].mx && cJ[d] >= C->j0[h] &&
+                        cJ[d] < C->j0[h] + C->desc[h].my;
+      const int q = in_h ? h : C->find(cI[d], cJ[d]);
+      if (q >= 0) hint = q;
       if (q < 0 || C->local[q] < 0) {
         char b[200];
         std::snprintf(b, sizeof b, "level %d: coarse cell (%lld,%lld) needed for interpolation is not on level %d",
@@ -1291,13 +1300,14 @@ int plan_level(claw_ctx* c, int level, Level& L) {
       L.frame_elems = static_cast<int64_t>(L.nvirt) * 3 * smx * smy;
       L.frame_cs = static_cast<int64_t>(smx) * smy;
     }
-    L.hinterp.assign(static_cast<size_t>(L.ncoarse), DevInterp{});
+    L.hinterp.resize(static_cast<size_t>(L.ncoarse));   // every entry is written below
     parallel_for(host_threads(np), np, [&](int p) {
+      int hint = -1;
       for (size_t k = 0; k < pend_p[p].size() && !rc_p[p]; ++k) {
         const Pending& pd = pend_p[p][k];
         const int64_t slot = cstart[p] + static_cast<int64_t>(k);
         DevInterp& sp = L.hinterp[static_cast<size_t>(slot)];
-        rc_p[p] = make_spec(pd, slot, sp, msg_p[p]);
+        rc_p[p] = make_spec(pd, slot, sp, msg_p[p], hint);
         if (L.sparse) {
           const int32_t sl = L.hslots[(pd.J / smy) * L.npx + pd.I / smx];
           if (sl >= 0) {
@@ -1331,6 +1341,8 @@ int plan_level(claw_ctx* c, int level, Level& L) {
   L.frame_cs = L.ncoarse;
   std::vector<int64_t> rk(world, 0);
   int64_t ck = 0;
+  int hint = -1;
+  L.hinterp.clear();
   for (const Pending& pd : pend) {
     if (pd.kind == 1) {
       const int64_t k = rk[pd.src_rank]++;
@@ -1340,7 +1352,7 @@ int plan_level(claw_ctx* c, int level, Level& L) {
       cells[pd.lp][pd.cellidx] = Src{1, L.coarse_frame_off + k, L.ncoarse};
       DevInterp sp;
       std::string emsg;
-      if (int rc = make_spec(pd, k, sp, emsg)) return fail(c, rc, "%s", emsg.c_str());
+      if (int rc = make_spec(pd, k, sp, emsg, hint)) return fail(c, rc, "%s", emsg.c_str());
       L.hinterp.push_back(sp);
     }
   }
@@ -3264,8 +3276,10 @@ int flag_device(claw_ctx* ctx, int level, double tol, int buffer, int clip, DevB
   P.patches = L.dpatch.p;
   P.rects = L.drect.p;
   P.cellrect = L.ncellrect > 0 ? L.dcellrect.p : nullptr;
+  int64_t max_cells = 1;
+  for (const DevPatch& d : L.hpatch) max_cells = std::max<int64_t>(max_cells, static_cast<int64_t>(d.mx) * d.my);
   CUDA_TRY(static_cast<cudaError_t>(claw::launch_flag(P, orig.p, static_cast<int32_t>(L.owned.size()), L.nx, tol,
-                                                      raw.p, on.p, ctx->stream)));
+                                                      raw.p, on.p, max_cells, ctx->stream)));
   const uint8_t* mask = nullptr;
   if (clip == 1) mask = on.p;
   if (clip == 2) {

@@ -185,7 +185,7 @@ int launch_reflux_apply(double* qc, const DevPatch* cpatches, const DevReflux* t
 // |p_n - p| > tol) and on[J*nx+I] = 1; neighbours resolved like the step
 // kernel's (p.q, p.frame, p.patches, p.rects).
 int launch_flag(const StepParams& p, const int2* orig, int32_t nown, int64_t nx, double tol, uint8_t* raw,
-                uint8_t* on, void* stream);
+                uint8_t* on, int64_t max_cells, void* stream);
 // Chebyshev dilation by b, clipped to [0,nx) x [0,ny) and (mask != null) to
 // mask != 0; *count (device, zeroed by the caller) receives the set cells.
 int launch_dilate(const uint8_t* in, uint8_t* tmp, uint8_t* out, const uint8_t* mask, int64_t nx, int64_t ny, int b,
