@@ -87,7 +87,8 @@ typedef struct {
                                   (tests and custom transports; no NCCL needed) */
   int32_t reflux;              /* 1: conservation fix at coarse-fine interfaces (P:122-123,
                                   P:151-225; R17).  Fine patches
-                                  must be aligned to the coarser cells; single rank.
+                                  must be aligned to the coarser cells; single rank
+                                  (EINVAL with world > 1).
                                   See claw_update_level. */
   int32_t check_finite;        /* 1: debug check -- after every level step a
                                   reduction over the new state; claw_advance_level /
@@ -105,7 +106,21 @@ typedef struct {
                                   never freed by the library.  NULL: the library's own
                                   process-wide cudaMalloc'ed pool (claw_pool_stats). */
   uint64_t arena_bytes;        /* size of the arena in bytes */
-  int32_t reserved[4];
+  int32_t dist_level;          /* world > 1: the level partitioned across the ranks.
+                                  0: level 1 (single-level runs: band or Morton partition,
+                                  levels > 1 refused).  K >= 2: levels 1 .. K-1 are
+                                  replicated -- every rank holds and steps all their
+                                  patches, identically -- and level K (the finest; setting
+                                  a level above K fails) is Morton-partitioned: its coarse
+                                  interpolation donors are local, its same-level halo is
+                                  exchanged as for level 1, and claw_update_level(K)
+                                  averages each rank's patches locally, then exchanges the
+                                  averaged level-(K-1) cells so the replicas stay equal
+                                  (NCCL, or claw_update_pack / claw_update_unpack with
+                                  exchange = 1).  The finest level must be aligned to the
+                                  coarse cells (every coarse cell's children in one fine
+                                  patch).  Conservation fix and regridding stay single-rank. */
+  int32_t reserved[3];
 } claw_config;
 
 /* Kernel-level statistics, accumulated while profiling is on. */
@@ -136,9 +151,12 @@ int claw_destroy(claw_ctx* ctx);
  * named); valid until the next call on ctx.  Never NULL. */
 const char* claw_last_error(const claw_ctx* ctx);
 
-/* Deterministic owner map used by claw_set_level for `world` ranks: patches in
- * Morton order of their lower-left index, split contiguously into chunks of
- * ~equal cell count.  owner[npatch] receives ranks.  Host-only. */
+/* Deterministic owner map used by claw_set_level for the partitioned level
+ * (claw_config.dist_level) on `world` ranks: a uniform grid of equal patches
+ * covering the domain in bands of whole patch rows, otherwise patches in
+ * Morton order of their lower-left index (relative to the level's minimum
+ * corner), split contiguously into chunks of ~equal cell count.
+ * owner[npatch] receives ranks.  Host-only. */
 int claw_partition(int32_t npatch, const claw_patch_desc* descs, int32_t world,
                    int32_t* owner);
 
@@ -149,8 +167,10 @@ int claw_partition(int32_t npatch, const claw_patch_desc* descs, int32_t world,
  * builds the ghost-source, tile and exchange tables, allocates the level's
  * device pool (two ping-pong buffers) and uploads q0 (NULL = zeros): the
  * owned patches' level array.  Replaces any previous definition of the level;
- * finer levels must be set again afterwards.  world > 1 requires a single
- * level. */
+ * finer levels must be set again afterwards.  world > 1: the level named by
+ * claw_config.dist_level (default level 1) is partitioned (q0: the owned
+ * patches, in global patch order); every other level is replicated (q0: all
+ * patches) and levels above dist_level fail (EINVAL). */
 int claw_set_level(claw_ctx* ctx, int32_t level, int32_t npatch,
                    const claw_patch_desc* descs, const double* q0);
 
@@ -364,6 +384,24 @@ int claw_debug_halo_counts(const claw_ctx* ctx, int32_t level, int32_t peer,
 /* The k-th cell sent to `peer`: global donor patch and local (i, j). */
 int claw_debug_halo_send(const claw_ctx* ctx, int32_t level, int32_t peer,
                          int64_t k, int32_t* patch, int32_t* i, int32_t* j);
+
+/* Update exchange of the partitioned level `level` (claw_config.dist_level
+ * >= 2) with exchange = 1 (the coarse level takes the average of
+ * its children; it is replicated on every rank, so each rank's averages must
+ * reach every replica).  After claw_update_level(level) on every rank:
+ * claw_update_pack writes the level-(level-1) cells this rank's patches
+ * averaged into host_out ([3][n], component-major, in patch / rectangle /
+ * row-major order); claw_update_unpack writes rank `peer`'s pack into this
+ * rank's replica.  Synchronous.  EINVAL: `level` not the partitioned level,
+ * peer out of range or this rank, NULL buffer.  With exchange = 0
+ * claw_update_level does the same through NCCL itself. */
+int claw_update_pack(claw_ctx* ctx, int32_t level, double* host_out);
+int claw_update_unpack(claw_ctx* ctx, int32_t level, int32_t peer, const double* host_in);
+/* Update exchange plan: the number of cells this rank sends (to every peer)
+ * and the number it receives from `peer` (0 for peer = this rank, and 0 and 0
+ * for a level that is not partitioned). */
+int claw_debug_update_counts(const claw_ctx* ctx, int32_t level, int32_t peer,
+                             int64_t* nsend, int64_t* nrecv);
 
 /* The process-wide device memory pool every context allocates from (the
  * paper's GPU memory pool): per device, chunks from cudaMalloc (the

@@ -38,6 +38,7 @@ EXPORTS = [
     "claw_update_level", "claw_reflux_registers", "claw_level_extent", "claw_level_count",
     "claw_level_descs", "claw_flag", "claw_cluster", "claw_regrid", "claw_regrid_auto",
     "claw_pool_stats", "claw_pool_trim", "claw_comm_info", "claw_set_aux", "claw_advance_hierarchy_n",
+    "claw_update_pack", "claw_update_unpack", "claw_debug_update_counts",
 ]
 CLAW_HIER_UPDATE = 1
 
@@ -58,7 +59,8 @@ class ClawConfig(ctypes.Structure):
                 ("tile_rows", ctypes.c_int32), ("path", ctypes.c_int32),
                 ("exchange", ctypes.c_int32), ("reflux", ctypes.c_int32),
                 ("check_finite", ctypes.c_int32), ("arena", ctypes.c_void_p),
-                ("arena_bytes", ctypes.c_uint64), ("reserved", ctypes.c_int32 * 4)]
+                ("arena_bytes", ctypes.c_uint64), ("dist_level", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 3)]
 
 
 class ClawStats(ctypes.Structure):
@@ -127,6 +129,9 @@ def load() -> ctypes.CDLL:
                                  ctypes.POINTER(ctypes.c_int32)]
     L.claw_halo_pack.argtypes = [vp, i32, i32, dp]
     L.claw_halo_unpack.argtypes = [vp, i32, i32, dp]
+    L.claw_update_pack.argtypes = [vp, i32, dp]
+    L.claw_update_unpack.argtypes = [vp, i32, i32, dp]
+    L.claw_debug_update_counts.argtypes = [vp, i32, i32, i64, i64]
     _lib = L
     return L
 
@@ -230,10 +235,12 @@ class Claw:
     def __init__(self, domain=(-1.0, 1.0, -1.0, 1.0), bc=(1, 1, 1, 1), limiter=4,
                  order_trans=2, device=0, rank=0, world=1, nccl_id: bytes | None = None,
                  stream: int | None = None, tile_rows: int = 0, path: int = 0, exchange: int = 0,
-                 reflux: bool = False, check_finite: bool = False, arena=None):
+                 reflux: bool = False, check_finite: bool = False, arena=None, dist_level: int = 0):
         """arena: None, or device memory the context carves every buffer from
         (claw_config.arena): a CUDA torch tensor (kept referenced by this
-        object) or a (device pointer, bytes) pair."""
+        object) or a (device pointer, bytes) pair.  dist_level (world > 1):
+        the level partitioned across ranks (claw_config.dist_level; 0 = level
+        1, K >= 2 = levels below K replicated, level K partitioned)."""
         L = load()
         self._idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None
         self._arena = arena
@@ -249,7 +256,7 @@ class Claw:
                          int(order_trans), int(device), int(rank), int(world),
                          ctypes.cast(self._idbuf, ctypes.c_void_p) if self._idbuf else None,
                          stream, int(tile_rows), int(path), int(exchange), int(bool(reflux)),
-                         int(bool(check_finite)), aptr, abytes)
+                         int(bool(check_finite)), aptr, abytes, int(dist_level))
         self._h = ctypes.c_void_p()
         rc = L.claw_create(ctypes.byref(cfg), ctypes.byref(self._h))
         if rc:
@@ -490,6 +497,31 @@ class Claw:
     def debug_halo_counts(self, level: int, peer: int):
         s, r = ctypes.c_int64(), ctypes.c_int64()
         self._check(load().claw_debug_halo_counts(self._h, level, peer, ctypes.byref(s), ctypes.byref(r)))
+        return s.value, r.value
+
+    def update_pack(self, level: int) -> np.ndarray:
+        """The level-(level-1) cells this rank's patches of the partitioned
+        level `level` averaged in the last claw_update_level ([3][n];
+        claw_update_pack, exchange = 1)."""
+        ns, _ = self.debug_update_counts(level, self.rank)
+        out = np.empty(3 * ns)
+        if ns:
+            self._check(load().claw_update_pack(self._h, level, _host_f64(out, 3 * ns, "update_pack", True)))
+        return out
+
+    def update_unpack(self, level: int, peer: int, buf: np.ndarray):
+        """Write rank `peer`'s averaged cells (its update_pack) into this
+        rank's replica of level `level` - 1 (claw_update_unpack)."""
+        buf = np.ascontiguousarray(buf, dtype=np.float64)
+        _, nr = self.debug_update_counts(level, peer)
+        if buf.size or nr:
+            self._check(load().claw_update_unpack(self._h, level, peer, _host_f64(buf, 3 * nr, "update_unpack")))
+
+    def debug_update_counts(self, level: int, peer: int):
+        """(cells this rank sends, cells rank `peer` sends) of the update
+        exchange of the partitioned level `level`."""
+        s, r = ctypes.c_int64(), ctypes.c_int64()
+        self._check(load().claw_debug_update_counts(self._h, level, peer, ctypes.byref(s), ctypes.byref(r)))
         return s.value, r.value
 
     def debug_halo_send(self, level: int, peer: int, k: int):

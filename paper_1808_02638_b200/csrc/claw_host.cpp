@@ -401,6 +401,18 @@ struct Level {
   DevBuf<unsigned long long> pcfl;  // per owned patch
   DevBuf<unsigned long long> lcfl;  // level slot
   std::vector<std::unique_ptr<DevBuf<int64_t>>> dsend_off, dsend_cs;
+  // world > 1: this level is the partitioned one (claw_config.dist_level);
+  // otherwise every rank holds all of it (replicated, or world = 1)
+  bool dist = false;
+  // update exchange of the partitioned level (dist, level > 1): the
+  // level-(L-1) cells this rank averages (send) and those each peer
+  // averages (recv), as (offset in the coarse level buffer, component stride)
+  std::vector<int64_t> upd_send_off, upd_send_cs;
+  std::vector<std::vector<int64_t>> upd_recv_off, upd_recv_cs;
+  DevBuf<int64_t> dupd_send_off, dupd_send_cs;
+  DevBuf<double> dupd_send_buf;
+  std::vector<std::unique_ptr<DevBuf<int64_t>>> dupd_recv_off, dupd_recv_cs;
+  std::vector<std::unique_ptr<DevBuf<double>>> dupd_recv_buf;
   std::vector<std::unique_ptr<DevBuf<double>>> dsend_buf;
   double t_old = 0, t_new = 0;
   bool stepped_once = false;
@@ -684,6 +696,8 @@ int validate_config(claw_ctx* c, const claw_config* cfg) {
   if (cfg->world > 1 && cfg->exchange == 0 && !cfg->nccl_unique_id && cfg->device >= 0)
     return fail(c, CLAW_EINVAL, "world>1 needs nccl_unique_id");
   if (cfg->reflux != 0 && cfg->reflux != 1) return fail(c, CLAW_EINVAL, "reflux=%d: must be 0 or 1", cfg->reflux);
+  if (cfg->dist_level < 0 || cfg->dist_level == 1 || cfg->dist_level > kMaxLevel)
+    return fail(c, CLAW_EINVAL, "dist_level=%d: 0 (level 1) or 2..%d", cfg->dist_level, kMaxLevel);
   if (cfg->reflux && cfg->world > 1)
     return fail(c, CLAW_EINVAL, "reflux: the conservation fix is single-rank in this version (world=%d)", cfg->world);
   if (cfg->tile_rows < 0 || cfg->tile_rows > claw::max_tile_rows())
@@ -993,10 +1007,26 @@ int plan_level(claw_ctx* c, int level, Level& L) {
     t_last = t;
   };
   const claw_config& cfg = c->cfg;
-  const int me = cfg.rank, world = cfg.world;
+  // the partitioned level (world > 1): level 1, or claw_config.dist_level;
+  // any other level is replicated -- every rank owns every patch and plans
+  // it as a one-rank level
+  L.dist = cfg.world > 1 && level == (cfg.dist_level >= 2 ? cfg.dist_level : 1);
+  const int me = cfg.rank, world = L.dist ? cfg.world : 1;
   const int np = L.npatch;
-  L.owner.assign(np, 0);
-  partition_impl(np, L.desc.data(), L.i0, L.j0, world, L.owner.data());
+  if (L.dist) {
+    // (indices relative to the level's minimum corner, as claw_partition
+    // computes them from the descriptors alone: the Morton order is not
+    // shift-invariant, and callers slice their data with claw_partition)
+    L.owner.assign(np, 0);
+    const int64_t mi = np ? *std::min_element(L.i0.begin(), L.i0.end()) : 0;
+    const int64_t mj = np ? *std::min_element(L.j0.begin(), L.j0.end()) : 0;
+    std::vector<int64_t> ri(L.i0), rj(L.j0);
+    for (auto& v : ri) v -= mi;
+    for (auto& v : rj) v -= mj;
+    partition_impl(np, L.desc.data(), ri, rj, world, L.owner.data());
+  } else {
+    L.owner.assign(np, me);
+  }
   L.local.assign(np, -1);
   L.owned.clear();
   L.off.clear();
@@ -1623,7 +1653,15 @@ int plan_level(claw_ctx* c, int level, Level& L) {
   L.hur_chunk.clear();
   L.hu_src.clear();
   L.hu_scs.clear();
-  if (C && world == 1) {
+  L.upd_send_off.clear();
+  L.upd_send_cs.clear();
+  L.upd_recv_off.assign(world, {});
+  L.upd_recv_cs.assign(world, {});
+  if (C && (world == 1 || L.dist)) {
+    // (partitioned level: the coarse level is replicated, so every fine
+    // patch's rectangles are computed -- the device tables take the owned
+    // ones, the exchange lists every rank's -- and the level must be aligned
+    // to the coarse cells: no per-cell entries)
     const int R = L.ratio;
     // per fine patch in parallel (host workers), concatenated in patch order:
     // the tables are the sequential ones
@@ -1656,7 +1694,7 @@ int plan_level(claw_ctx* c, int level, Level& L) {
           const int lc = C->local[cq];
           claw::DevUpdateRect r{};
           r.dst = C->off[lc] + (y0 - C->j0[cq]) * C->desc[cq].mx + (x0 - C->i0[cq]);
-          r.src = L.off[L.local[fp]] + (y0 * R - fj0) * L.desc[fp].mx + (x0 * R - fi0);
+          r.src = L.local[fp] >= 0 ? L.off[L.local[fp]] + (y0 * R - fj0) * L.desc[fp].mx + (x0 * R - fi0) : 0;
           r.dcs = static_cast<int64_t>(C->desc[cq].mx) * C->desc[cq].my;
           r.fcs = static_cast<int64_t>(L.desc[fp].mx) * L.desc[fp].my;
           r.cmx = C->desc[cq].mx;
@@ -1697,6 +1735,10 @@ int plan_level(claw_ctx* c, int level, Level& L) {
               sc.push_back(static_cast<int64_t>(L.desc[q].mx) * L.desc[q].my);
             }
           if (!all) continue;
+          if (L.dist) {   // (unaligned fine patches: rejected below)
+            P.cells.push_back(claw::DevUpdate{});
+            continue;
+          }
           claw::DevUpdate u{};
           u.dst = C->off[lc] + (Jc - C->j0[cq]) * C->desc[cq].mx + (Ic - C->i0[cq]);
           u.dcs = C->desc[cq].mx * C->desc[cq].my;
@@ -1714,7 +1756,29 @@ int plan_level(claw_ctx* c, int level, Level& L) {
           P.cells.push_back(u);
         }
     });
+    for (int fp = 0; fp < np && L.dist; ++fp) {
+      if (!parts[fp].cells.empty())
+        return fail(c, CLAW_EINVAL,
+                    "level %d is partitioned across ranks (dist_level): patch %d is not aligned to the level-%d "
+                    "cells (R=%d)", level, fp, level - 1, R);
+      // every rank's averaged coarse cells, in patch, rectangle, row-major
+      // order (the same lists on every rank)
+      const int ow = L.owner[fp];
+      for (const claw::DevUpdateRect& r : parts[fp].rects)
+        for (int y = 0; y < r.h; ++y)
+          for (int x = 0; x < r.w; ++x) {
+            const int64_t o = r.dst + static_cast<int64_t>(y) * r.cmx + x;
+            if (ow == me) {
+              L.upd_send_off.push_back(o);
+              L.upd_send_cs.push_back(r.dcs);
+            } else {
+              L.upd_recv_off[ow].push_back(o);
+              L.upd_recv_cs[ow].push_back(r.dcs);
+            }
+          }
+    }
     for (int fp = 0; fp < np; ++fp) {
+      if (L.local[fp] < 0) continue;   // (partitioned level: owned patches only)
       UpdPart& P = parts[fp];
       for (claw::DevUpdateRect r : P.rects) {
         r.chunk0 = static_cast<int32_t>(L.hur_chunk.size());
@@ -1845,7 +1909,7 @@ int alloc_level(claw_ctx* ctx, int level, Level& L) {
   }
   // a fine level's coarse ghost values for all R substeps of a coarse step
   // are interpolated by one launch into R slices (claw_advance_hierarchy)
-  L.nslice = (level > 1 && L.ncoarse > 0 && ctx->cfg.world == 1 && L.ratio >= 2 &&
+  L.nslice = (level > 1 && L.ncoarse > 0 && !L.dist && L.ratio >= 2 &&
               L.ratio <= claw::kMaxInterpAlphas) ? L.ratio : 1;
   CUDA_TRY(L.frame.alloc(std::max<int64_t>(L.frame_elems, 1) * L.nslice));
   if (int r2 = upload(ctx, L.dpatch, L.hpatch)) return r2;
@@ -1877,10 +1941,24 @@ int alloc_level(claw_ctx* ctx, int level, Level& L) {
   CUDA_TRY(cudaMemset(L.pcfl.p, 0, L.pcfl.n * 8));
   CUDA_TRY(cudaMemset(L.lcfl.p, 0, 16));
   L.gen = 0;
-  const int world = ctx->cfg.world;
+  const int world = static_cast<int>(L.send_off.size());   // (1 unless the level is partitioned)
   L.dsend_off.clear();
   L.dsend_cs.clear();
   L.dsend_buf.clear();
+  if (int r2 = upload(ctx, L.dupd_send_off, L.upd_send_off)) return r2;
+  if (int r2 = upload(ctx, L.dupd_send_cs, L.upd_send_cs)) return r2;
+  CUDA_TRY(L.dupd_send_buf.alloc(std::max<size_t>(3 * L.upd_send_off.size(), 1)));
+  L.dupd_recv_off.clear();
+  L.dupd_recv_cs.clear();
+  L.dupd_recv_buf.clear();
+  for (size_t r = 0; r < L.upd_recv_off.size(); ++r) {
+    L.dupd_recv_off.emplace_back(new DevBuf<int64_t>());
+    L.dupd_recv_cs.emplace_back(new DevBuf<int64_t>());
+    L.dupd_recv_buf.emplace_back(new DevBuf<double>());
+    if (int r2 = upload(ctx, *L.dupd_recv_off[r], L.upd_recv_off[r])) return r2;
+    if (int r2 = upload(ctx, *L.dupd_recv_cs[r], L.upd_recv_cs[r])) return r2;
+    CUDA_TRY(L.dupd_recv_buf[r]->alloc(std::max<size_t>(3 * L.upd_recv_off[r].size(), 1)));
+  }
   for (int r = 0; r < world; ++r) {
     L.dsend_off.emplace_back(new DevBuf<int64_t>());
     L.dsend_cs.emplace_back(new DevBuf<int64_t>());
@@ -1896,7 +1974,7 @@ int alloc_level(claw_ctx* ctx, int level, Level& L) {
   {
     const char* e = std::getenv("CLAW_SIDE");
     const bool want = e ? e[0] == '1' : (L.htile.size() >= 1024 && L.th >= 64);
-    L.use_side = want && !L.grid && !L.lane_tiles && ctx->cfg.world == 1 && !L.htile.empty();
+    L.use_side = want && !L.grid && !L.lane_tiles && !L.dist && !L.htile.empty();
     if (L.use_side) CUDA_TRY(L.side.alloc(L.htile.size() * static_cast<size_t>(claw::side_stride())));
   }
   L.device_bytes = 2 * L.buf_elems * 8 + L.frame_elems * 8 +
@@ -2139,8 +2217,10 @@ int claw_set_level(claw_ctx* ctx, int32_t level, int32_t npatch, const claw_patc
   if (level < 1 || level > kMaxLevel) return fail(ctx, CLAW_EINVAL, "level=%d: must be 1..%d", level, kMaxLevel);
   if (npatch < 1 || !descs) return fail(ctx, CLAW_EINVAL, "npatch=%d: need >= 1 patch descriptors", npatch);
   if (level > 1 && !ctx->lev[level - 1].set) return fail(ctx, CLAW_ESTATE, "level %d set before level %d", level, level - 1);
-  if (level > 1 && ctx->cfg.world > 1)
-    return fail(ctx, CLAW_EINVAL, "multi-level hierarchies are single-rank in this version (world=%d)", ctx->cfg.world);
+  if (level > 1 && ctx->cfg.world > 1 && level > ctx->cfg.dist_level)
+    return fail(ctx, CLAW_EINVAL,
+                "level %d with world=%d: a multi-rank hierarchy needs claw_config.dist_level >= %d (the partitioned, "
+                "finest level; the levels below it are replicated)", level, ctx->cfg.world, level);
   if (level > 1 && ctx->lev[1].vc)
     return fail(ctx, CLAW_EINVAL, "level %d: variable media (claw_set_aux) are single-level (DESIGN.md R20)", level);
   if (!ctx->host_only) CUDA_TRY(cudaStreamSynchronize(ctx->stream));
@@ -2310,7 +2390,7 @@ int claw_fill_ghost(claw_ctx* ctx, int32_t level, double t) {
   Level& L = ctx->lev[level];
   record(ctx, ctx->ev_ghost, true);
   if (int rc = interp_frames(ctx, level, &t, 1)) return rc;
-  if (ctx->cfg.world > 1 && ctx->cfg.exchange == 0) {
+  if (L.dist && ctx->cfg.exchange == 0) {
     // halo on the comm stream: starts when q^n is complete on the main
     // stream; claw_advance_level runs the interior tiles meanwhile and waits
     // for it only before the edge tiles
@@ -2417,7 +2497,7 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
     L.last_s = P.k.s;
   }
   record(ctx, ctx->ev_step, true);
-  if (ctx->cfg.world > 1) {
+  if (L.dist) {
     // interior tiles (no remote ghost) first, then -- once the halo has
     // landed -- the edge tiles
     claw::StepParams Pi = P, Pe = P;
@@ -2506,7 +2586,7 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
   // number also lands in the hierarchy slot, reduced once for the whole call
   // (one all-reduce per claw_advance_hierarchy[_n] instead of one per level
   // step, which nothing overlaps), so the level slot stays rank-local there
-  if (ctx->cfg.world > 1 && ctx->cfg.exchange == 0 && !ctx->hier_slot) {
+  if (L.dist && ctx->cfg.exchange == 0 && !ctx->hier_slot) {
     Nvtx nv_red("claw_cfl_allreduce");
     ncclResult_t nr = g_nccl.AllReduce(L.lcfl.p + g, L.lcfl.p + g, 1, ncclFloat64, ncclMax, ctx->comm, ctx->stream);
     if (nr != ncclSuccess) return nccl_fail(ctx, nr, "ncclAllReduce(cfl, max)");
@@ -2677,9 +2757,9 @@ int claw_update_level(claw_ctx* ctx, int32_t level) {
   if (level < 2 || level > kMaxLevel || !ctx->lev[level].set || !ctx->lev[level - 1].set)
     return fail(ctx, CLAW_ESTATE, "update needs level %d and level %d set", level, level - 1);
   if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
-  if (ctx->cfg.world > 1) return fail(ctx, CLAW_EINVAL, "updating is single-rank in this version");
   Level& F = ctx->lev[level];
   Level& C = ctx->lev[level - 1];
+  if (C.dist) return fail(ctx, CLAW_EINVAL, "update: level %d is partitioned across ranks", level - 1);
   if (std::fabs(F.t_new - C.t_new) > 1e-12 * std::max(1.0, std::fabs(C.t_new)))
     return fail(ctx, CLAW_ESTATE, "update: level %d (t=%.17g) has not caught up with level %d (t=%.17g)", level,
                 F.t_new, level - 1, C.t_new);
@@ -2691,6 +2771,41 @@ int claw_update_level(claw_ctx* ctx, int32_t level) {
   if (!ctx->dry) CUDA_TRY(static_cast<cudaError_t>(claw::launch_update(C.q[C.cur].p, F.q[F.cur].p, F.du.p, n, F.ratio,
                                                         F.du_src.p, F.du_scs.p, ctx->stream)));
   ctx->stats.ghost_launches += (F.hur.empty() ? 0 : 1) + (n > 0 ? 1 : 0);
+  if (F.dist && ctx->cfg.exchange == 0 && !ctx->dry) {
+    // the replicated coarse level takes every rank's averages: each rank
+    // sends the cells its patches averaged to every peer, receives theirs,
+    // and writes them into its replica (grouped NCCL send/recv)
+    Nvtx nv_x("claw_update_exchange");
+    const int world = ctx->cfg.world, me = ctx->cfg.rank;
+    const int64_t ns = static_cast<int64_t>(F.upd_send_off.size());
+    if (ns)
+      CUDA_TRY(static_cast<cudaError_t>(claw::launch_pack(C.q[C.cur].p, F.dupd_send_off.p, F.dupd_send_cs.p, ns,
+                                                          F.dupd_send_buf.p, ctx->stream)));
+    ncclResult_t nr = g_nccl.GroupStart();
+    if (nr != ncclSuccess) return nccl_fail(ctx, nr, "ncclGroupStart");
+    for (int r = 0; r < world; ++r) {
+      if (r == me) continue;
+      if (ns) {
+        nr = g_nccl.Send(F.dupd_send_buf.p, 3 * ns, ncclFloat64, r, ctx->comm, ctx->stream);
+        if (nr != ncclSuccess) return nccl_fail(ctx, nr, "ncclSend");
+      }
+      const size_t nrv = F.upd_recv_off[r].size();
+      if (nrv) {
+        nr = g_nccl.Recv(F.dupd_recv_buf[r]->p, 3 * nrv, ncclFloat64, r, ctx->comm, ctx->stream);
+        if (nr != ncclSuccess) return nccl_fail(ctx, nr, "ncclRecv");
+      }
+    }
+    nr = g_nccl.GroupEnd();
+    if (nr != ncclSuccess) return nccl_fail(ctx, nr, "ncclGroupEnd");
+    for (int r = 0; r < world; ++r) {
+      const int64_t nrv = static_cast<int64_t>(F.upd_recv_off[r].size());
+      if (r != me && nrv)
+        CUDA_TRY(static_cast<cudaError_t>(claw::launch_scatter(F.dupd_recv_buf[r]->p, F.dupd_recv_off[r]->p,
+                                                               F.dupd_recv_cs[r]->p, nrv, C.q[C.cur].p,
+                                                               ctx->stream)));
+    }
+    ctx->stats.ghost_launches += 1 + (world - 1);
+  }
   if (ctx->cfg.reflux && !F.hreg.empty()) {
     if (!ctx->dry) CUDA_TRY(static_cast<cudaError_t>(claw::launch_reflux_apply(C.q[C.cur].p, C.dpatch.p, F.dreg.p, F.dheads.p,
                                                                 static_cast<int64_t>(F.hheads.size()) - 1, F.racc.p,
@@ -2944,6 +3059,7 @@ int claw_halo_pack(claw_ctx* ctx, int32_t level, int32_t peer, double* host_out)
   if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
   if (peer < 0 || peer >= ctx->cfg.world || !host_out) return fail(ctx, CLAW_EINVAL, "bad peer or buffer");
   Level& L = ctx->lev[level];
+  if (!L.dist) return CLAW_OK;   // (a replicated level has no halo)
   const int64_t n = static_cast<int64_t>(L.send_off[peer].size());
   if (n == 0) return CLAW_OK;
   CUDA_TRY(static_cast<cudaError_t>(claw::launch_pack(L.q[L.cur].p, L.dsend_off[peer]->p, L.dsend_cs[peer]->p, n,
@@ -2959,6 +3075,7 @@ int claw_halo_unpack(claw_ctx* ctx, int32_t level, int32_t peer, const double* h
   if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
   if (peer < 0 || peer >= ctx->cfg.world || !host_in) return fail(ctx, CLAW_EINVAL, "bad peer or buffer");
   Level& L = ctx->lev[level];
+  if (!L.dist) return CLAW_OK;
   const int64_t n = L.nrecv[peer];
   if (n == 0) return CLAW_OK;
   CUDA_TRY(cudaMemcpyAsync(L.frame.p + L.recv_frame_off[peer], host_in, 3 * n * 8, cudaMemcpyHostToDevice,
@@ -2971,8 +3088,52 @@ int claw_debug_halo_counts(const claw_ctx* ctx, int32_t level, int32_t peer, int
   if (!ctx || level < 1 || level > kMaxLevel || !ctx->lev[level].set) return CLAW_EINVAL;
   const Level& L = ctx->lev[level];
   if (peer < 0 || peer >= ctx->cfg.world) return CLAW_EINVAL;
-  if (nsend) *nsend = static_cast<int64_t>(L.send_off[peer].size());
-  if (nrecv) *nrecv = L.nrecv[peer];
+  if (nsend) *nsend = L.dist ? static_cast<int64_t>(L.send_off[peer].size()) : 0;
+  if (nrecv) *nrecv = L.dist ? L.nrecv[peer] : 0;
+  return CLAW_OK;
+}
+
+int claw_update_pack(claw_ctx* ctx, int32_t level, double* host_out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = check_level(ctx, level)) return rc;
+  if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
+  if (level < 2 || !ctx->lev[level].dist || !host_out)
+    return fail(ctx, CLAW_EINVAL, "update_pack: level %d is not the partitioned level, or no buffer", level);
+  Level& F = ctx->lev[level];
+  Level& C = ctx->lev[level - 1];
+  const int64_t n = static_cast<int64_t>(F.upd_send_off.size());
+  if (n == 0) return CLAW_OK;
+  CUDA_TRY(static_cast<cudaError_t>(claw::launch_pack(C.q[C.cur].p, F.dupd_send_off.p, F.dupd_send_cs.p, n,
+                                                      F.dupd_send_buf.p, ctx->stream)));
+  CUDA_TRY(cudaMemcpyAsync(host_out, F.dupd_send_buf.p, 3 * n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return CLAW_OK;
+}
+
+int claw_update_unpack(claw_ctx* ctx, int32_t level, int32_t peer, const double* host_in) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = check_level(ctx, level)) return rc;
+  if (ctx->host_only) return fail(ctx, CLAW_ENODEV, "host-only context");
+  if (level < 2 || !ctx->lev[level].dist || peer < 0 || peer >= ctx->cfg.world || peer == ctx->cfg.rank ||
+      !host_in)
+    return fail(ctx, CLAW_EINVAL, "update_unpack: level %d / peer %d / buffer", level, peer);
+  Level& F = ctx->lev[level];
+  Level& C = ctx->lev[level - 1];
+  const int64_t n = static_cast<int64_t>(F.upd_recv_off[peer].size());
+  if (n == 0) return CLAW_OK;
+  CUDA_TRY(cudaMemcpyAsync(F.dupd_recv_buf[peer]->p, host_in, 3 * n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(static_cast<cudaError_t>(claw::launch_scatter(F.dupd_recv_buf[peer]->p, F.dupd_recv_off[peer]->p,
+                                                         F.dupd_recv_cs[peer]->p, n, C.q[C.cur].p, ctx->stream)));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return CLAW_OK;
+}
+
+int claw_debug_update_counts(const claw_ctx* ctx, int32_t level, int32_t peer, int64_t* nsend, int64_t* nrecv) {
+  if (!ctx || level < 2 || level > kMaxLevel || !ctx->lev[level].set) return CLAW_EINVAL;
+  const Level& F = ctx->lev[level];
+  if (peer < 0 || peer >= ctx->cfg.world) return CLAW_EINVAL;
+  if (nsend) *nsend = F.dist ? static_cast<int64_t>(F.upd_send_off.size()) : 0;
+  if (nrecv) *nrecv = (F.dist && peer != ctx->cfg.rank) ? static_cast<int64_t>(F.upd_recv_off[peer].size()) : 0;
   return CLAW_OK;
 }
 

@@ -127,6 +127,8 @@ int launch_interp(const double* q_old, const double* q_new, const double* alphas
 // debug check (claw_config.check_finite): atomicMax(flag, level) if any of
 // q[0..n) is NaN or +-Inf
 int launch_nonfinite(const double* q, int64_t n, int level, int32_t* flag, void* stream);
+// scatter [3][n] values into q at offset off[s] (+ m cs[s]) (update exchange)
+int launch_scatter(const double* buf, const int64_t* off, const int64_t* cs, int64_t n, double* q, void* stream);
 // the ghost-cell rectangle map of a generic level (DevPatch::crect; one CTA
 // per patch, every cell of every rectangle of the patch)
 int launch_cellrect(const DevPatch* patches, int32_t npatch, const DevRect* rects, int32_t* map, void* stream);

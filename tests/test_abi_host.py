@@ -224,3 +224,44 @@ def test_set_aux_validation_host_only():
         r.set_aux(1, W.random_media(rd, 2))
     assert e.value.code == binding.CLAW_EINVAL
     r.close()
+
+
+@pytest.mark.parametrize("name,world", [("c2", 2), ("c2", 3), ("c3", 2), ("c3", 4)])
+def test_dist_level_update_exchange_plans_agree(name, world):
+    """claw_config.dist_level (host-only contexts, one per rank): the coarse
+    levels are replicated (every rank owns every patch), the finest is
+    partitioned as claw_partition says; the update exchange lists agree
+    pairwise (what rank r sends is what every other rank expects from r), and
+    together they cover every coarse cell the finest level averages, once
+    (the rectangles of the one-rank plan)."""
+    wl = getattr(W, name)()
+    nlev = len(wl.levels)
+    ctxs = []
+    for r in range(world):
+        c = binding.Claw(wl.domain, wl.bc, 4, 2, device=-1, rank=r, world=world, exchange=1, dist_level=nlev)
+        for L, lv in enumerate(wl.levels, start=1):
+            c.set_level(L, lv.descs)
+        ctxs.append(c)
+    owners = binding.partition(wl.levels[-1].descs, world)
+    for r, c in enumerate(ctxs):
+        for L in range(1, nlev):
+            assert [c.owner(L, p) for p in range(len(wl.levels[L - 1].descs))] == [r] * len(wl.levels[L - 1].descs)
+        assert [c.owner(nlev, p) for p in range(len(owners))] == list(owners)
+    sends = [c.debug_update_counts(nlev, r)[0] for r, c in enumerate(ctxs)]
+    for s, cs in enumerate(ctxs):
+        for r in range(world):
+            if r != s:
+                assert cs.debug_update_counts(nlev, r)[1] == sends[r]
+    # the averaged coarse cells: every coarse cell whose R x R children are on the finest level
+    R = wl.levels[-1].ratio
+    fine = wl.levels[-1].descs
+    cover = set()
+    for d in fine:
+        i0 = int(round((d["xlower"] - wl.domain[0]) / d["dx"]))
+        j0 = int(round((d["ylower"] - wl.domain[2]) / d["dy"]))
+        for J in range(j0 // R, (j0 + int(d["my"])) // R):
+            for I in range(i0 // R, (i0 + int(d["mx"])) // R):
+                cover.add((I, J))
+    assert sum(sends) == len(cover)
+    for c in ctxs:
+        c.close()

@@ -128,3 +128,73 @@ def test_nccl_path_processes_bitwise_equal_single_rank(shim, tmp_path, world, na
             a_r = np.concatenate([aux[ao[p]:ao[p + 1]] for p in range(len(d)) if owners[p] == r])
             local.append(W.max_sound_speed(a_r, sub))
         assert len(set(local)) > 1, local
+
+
+HIER_WORKER = r'''
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_1808_02638_b200 import binding, workloads as W
+rank, world, idhex, name, out = int(sys.argv[2]), int(sys.argv[3]), sys.argv[4], sys.argv[5], sys.argv[6]
+wl = getattr(W, name)()
+nlev = len(wl.levels)
+q0s = W.hierarchy_ic(wl)
+d = wl.levels[-1].descs
+owners = binding.partition(d, world)
+offs = W.level_offsets(d)
+g = binding.Claw(wl.domain, wl.bc, wl.limiter, wl.order_trans, device=0, rank=rank, world=world,
+                 nccl_id=bytes.fromhex(idhex), dist_level=nlev)
+for L, (lv, q) in enumerate(zip(wl.levels, q0s), start=1):
+    if L < nlev:
+        g.set_level(L, lv.descs, q)
+    else:
+        g.set_level(L, lv.descs, np.concatenate([q[offs[p]:offs[p + 1]] for p in range(len(d)) if owners[p] == rank]))
+dt = wl.dt0()
+cfl = g.advance_hierarchy_n(0.0, dt, 3, update=True).tolist()
+cfl.append(g.advance_hierarchy(3 * dt, dt, update=True))
+for L in range(1, nlev + 1):
+    np.save(out + f".L{L}.npy", g.read_level(L))
+np.save(out + ".cfl.npy", np.array(cfl))
+g.close()
+'''
+
+
+@pytest.mark.parametrize("world,name", [(2, "c2"), (3, "c2"), (2, "c3")])
+def test_nccl_path_hierarchy_replicated_coarse_partitioned_finest(shim, tmp_path, world, name):
+    """claw_config.dist_level through the library's NCCL path (stand-in NCCL,
+    processes on one GPU): the native hierarchy driver exchanges the finest
+    level's halo and, after its updating, the averaged coarse cells (grouped
+    send/recv), and reduces the per-step CFLs once per call.  Every rank's
+    coarse replicas and its own fine patches are bitwise the one-rank run."""
+    env = dict(os.environ, CLAW_NCCL_LIB=shim)
+    gen = subprocess.run([sys.executable, "-c",
+                          "import sys; sys.path.insert(0, sys.argv[1]); "
+                          "from paper_1808_02638_b200 import binding; print(binding.nccl_unique_id().hex())", ROOT],
+                         env=env, capture_output=True, text=True, check=True)
+    idhex = gen.stdout.strip().splitlines()[-1]
+    script = tmp_path / "hworker.py"
+    script.write_text(HIER_WORKER)
+    procs = [subprocess.Popen([sys.executable, str(script), ROOT, str(r), str(world), idhex, name,
+                               str(tmp_path / f"rank{r}")], env=env, stdout=subprocess.PIPE,
+                              stderr=subprocess.PIPE, text=True) for r in range(world)]
+    outs = [p.communicate(timeout=600) for p in procs]
+    for p, (so, se) in zip(procs, outs):
+        assert p.returncode == 0, se[-3000:]
+    wl = getattr(W, name)()
+    nlev = len(wl.levels)
+    ref = binding.Claw(wl.domain, wl.bc, wl.limiter, wl.order_trans, device=0)
+    for L, (lv, q) in enumerate(zip(wl.levels, W.hierarchy_ic(wl)), start=1):
+        ref.set_level(L, lv.descs, q)
+    dt = wl.dt0()
+    cfl = ref.advance_hierarchy_n(0.0, dt, 3, update=True).tolist()
+    cfl.append(ref.advance_hierarchy(3 * dt, dt, update=True))
+    d = wl.levels[-1].descs
+    owners = binding.partition(d, world)
+    offs = W.level_offsets(d)
+    for r in range(world):
+        for L in range(1, nlev):
+            assert np.array_equal(np.load(tmp_path / f"rank{r}.L{L}.npy"), ref.read_level(L)), (r, L)
+        full = ref.read_level(nlev)
+        mine = np.concatenate([full[offs[p]:offs[p + 1]] for p in range(len(d)) if owners[p] == r])
+        assert np.array_equal(np.load(tmp_path / f"rank{r}.L{nlev}.npy"), mine), r
+        assert np.load(tmp_path / f"rank{r}.cfl.npy").tolist() == cfl
+    ref.close()
