@@ -11,7 +11,10 @@ all-reduce are not in it.  Lines: N, rank, ms per step (CUDA events around K
 batched steps), the two launches' mean times (profiled pass right after), and
 the projected speed-up t(1) / t(N) for a strong-scaled level.
 
-usage: python scripts/rank_time.py [c5|c5vc] [K] [N ...]
+usage: python scripts/rank_time.py [c5|c5vc|c2|c3] [K] [N ...]
+
+c2 / c3: multi-rank hierarchies (claw_config.dist_level = the finest level:
+coarse levels replicated, the finest partitioned); ms per coarse step.
 """
 import json
 import os
@@ -26,8 +29,9 @@ from paper_1808_02638_b200 import binding, workloads as W
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c5"
 K = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 Ns = [int(x) for x in sys.argv[3:]] or [1, 2, 4, 8]
-wl = W.c5_layered() if cfg == "c5vc" else W.c5()
-d = wl.levels[0].descs
+wl = {"c5vc": W.c5_layered, "c2": W.c2, "c3": W.c3}.get(cfg, W.c5)()
+nlev = len(wl.levels)
+d = wl.levels[-1].descs
 aux = W.media_field(d) if cfg == "c5vc" else None
 dt = wl.dt0() if aux is None else 0.9 * float(d["dx"][0]) / W.max_sound_speed(aux, d)
 t1 = None
@@ -35,26 +39,30 @@ for N in Ns:
     owners = binding.partition(d, N)
     for r in sorted({0, N // 2}):
         g = binding.Claw(wl.domain, wl.bc, wl.limiter, wl.order_trans, device=0, rank=r, world=N,
-                         exchange=1 if N > 1 else 0)
-        g.set_level(1, d)
+                         exchange=1 if N > 1 else 0, dist_level=nlev if nlev > 1 else 0)
+        for L, lv in enumerate(wl.levels, start=1):
+            g.set_level(L, lv.descs)
         if aux is not None:
             g.set_aux(1, aux)
         cells = int((d["mx"].astype(np.int64) * d["my"])[owners == r].sum())
-        g.advance_hierarchy_n(0.0, dt, 5)
+        t = 0.0
+        g.advance_hierarchy_n(t, dt, 5, update=nlev > 1)
+        t += 5 * dt
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         done = 0
         while done < K:
             k = min(10, K - done)
-            g.advance_hierarchy_n(0.0, dt, k)
+            g.advance_hierarchy_n(t, dt, k, update=nlev > 1)
+            t += k * dt
             done += k
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / K
         g.set_profiling(True)
         g.reset_stats()
-        g.advance_hierarchy_n(0.0, dt, 10)
+        g.advance_hierarchy_n(t, dt, 10, update=nlev > 1)
         st = g.stats()
         g.set_profiling(False)
         if N == 1:
