@@ -487,8 +487,12 @@ def main():
     nlev = 1 + len(rat)
     if args.regrid < 0:
         args.regrid = wl.extra.get("regrid_every", 0) if dyn else 0
-    if world > 1 and nlev > 1:
-        raise SystemExit("multi-level configs are single-GPU in this version")
+    if world > 1 and nlev > 1 and (dyn or args.regrid or args.reflux or args.exchange == "host"):
+        raise SystemExit("multi-rank hierarchies: fixed hierarchies only (no regridding, no conservation fix, "
+                         "NCCL exchange)")
+    # multi-rank hierarchies: the coarse levels replicated, the finest
+    # partitioned (claw_config.dist_level)
+    dist_level = nlev if (world > 1 and nlev > 1) else 0
 
     # NCCL unique id for the library's own communicator (plumbing via torch)
     nccl_id = None
@@ -500,7 +504,8 @@ def main():
     stream = torch.cuda.current_stream()
     g = binding.Claw(wl.domain, wl.bc, wl.limiter, wl.order_trans, device=device, rank=rank,
                      world=world, nccl_id=nccl_id, stream=stream.cuda_stream, tile_rows=args.tile_rows,
-                     path=args.path, exchange=1 if host_x else 0, reflux=args.reflux and nlev > 1)
+                     path=args.path, exchange=1 if host_x else 0, reflux=args.reflux and nlev > 1,
+                     dist_level=dist_level)
     comm = None
     if world > 1:
         ci = g.comm_info()   # the communicator as NCCL reports it (None: external exchange)
@@ -517,7 +522,7 @@ def main():
     # through the API; pinned so the e2e leg measures the real H2D path
     host_q = []
     for L, lv in enumerate(wl.levels, start=1):
-        owner = binding.partition(lv.descs, world)
+        owner = binding.partition(lv.descs, world) if (L == max(dist_level, 1)) else np.full(len(lv.descs), rank)
         mine = lv.descs[owner == rank]
         n = 3 * int((mine["mx"].astype(np.int64) * mine["my"]).sum())
         buf = torch.empty(n, dtype=torch.float64, pin_memory=True)
@@ -552,6 +557,9 @@ def main():
     mult = [int(np.prod(rat[:L])) for L in range(nlev)]
     cells_per_step_rank = sum(c * m for c, m in zip(cells_owned, mult))
     total_cells_per_step = wl.levels[0].cells if nlev == 1 else cells_per_step_rank
+    if dist_level:   # (replicated coarse levels count once in the whole-job total)
+        total_cells_per_step = sum(int((lv.descs["mx"].astype(np.int64) * lv.descs["my"]).sum()) * m
+                                   for lv, m in zip(wl.levels, mult))
     t_sim = [0.0]
 
     def host_exchange():
@@ -819,7 +827,9 @@ def main():
                            "cfl_max_seen": max(cfl_seen) if cfl_seen else None,
                            "regrid_ms_mean": statistics.mean(regrid_ms) if regrid_ms else None,
                            "patches_after": [len(g.descs(L)) for L in range(1, nlev + 1)] if nlev > 1 else None,
-                           "parallelism": f"patch-partitioned over {world} rank(s), NCCL halo + max all-reduce"
+                           "parallelism": (f"levels 1..{nlev - 1} replicated, level {nlev} patch-partitioned "
+                                           f"over {world} rank(s); NCCL halo, update exchange, max all-reduce")
+                           if dist_level else f"patch-partitioned over {world} rank(s), NCCL halo + max all-reduce"
                            if world > 1 else "single GPU",
                            "l2": "state per buffer exceeds L2 (126 MB); no flush needed"
                            if total_cells_per_step * 24 > 126e6 else "state fits L2 (latency-bound config)"},
