@@ -283,7 +283,11 @@ int claw_reflux_registers(claw_ctx* ctx, int32_t level, int64_t* n, int32_t* edg
  * all level steps.  Ratios are taken from the levels' dx.  With world > 1
  * that value is reduced across ranks once per call (one 8-byte NCCL max
  * all-reduce per call, not per level step); the levels' own CFL slots
- * (claw_wait_cfl) then hold rank-local maxima. */
+ * (claw_wait_cfl) then hold rank-local maxima.  With exchange = 1
+ * (external) the hierarchy drivers move no halo or update data and reduce
+ * nothing across ranks: drive the levels with the level calls and
+ * claw_halo_* / claw_update_* instead (timing tools use it to run one rank's
+ * launches alone). */
 int claw_advance_hierarchy(claw_ctx* ctx, double t, double dt, int32_t flags, double* cfl_max);
 /* nsteps consecutive coarse steps at the fixed dt (times t + k dt), each
  * exactly as claw_advance_hierarchy would run it, with ONE host
