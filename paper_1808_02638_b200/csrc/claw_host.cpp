@@ -1447,8 +1447,8 @@ int plan_level(claw_ctx* c, int level, Level& L) {
   } else {
     const int64_t want = static_cast<int64_t>(c->nsm) * 8;
     int min_th = 4;
-    if (const char* e = std::getenv("CLAW_MIN_TH"))   // tuning: smallest auto tile height (4 or 8)
-      if (std::atoi(e) == 4 || std::atoi(e) == 8) min_th = std::atoi(e);
+    if (const char* e = std::getenv("CLAW_MIN_TH"))   // tuning: smallest auto tile height (2, 4 or 8)
+      if (std::atoi(e) == 2 || std::atoi(e) == 4 || std::atoi(e) == 8) min_th = std::atoi(e);
     int th = 64;
     while (th > min_th && L.cells_owned / (32ll * th) < want) th /= 2;
     L.th = th;
