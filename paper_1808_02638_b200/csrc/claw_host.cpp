@@ -517,6 +517,7 @@ struct claw_ctx {
   unsigned long long* hier_slot = nullptr;  // set while claw_advance_hierarchy runs
   cudaStream_t comm_stream = nullptr;       // world > 1: halo pack + NCCL send/recv
   cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
+  cudaEvent_t ev_int = nullptr, ev_edge = nullptr;   // split step: q^n ready for, and end of, the edge launch
   DevBuf<unsigned long long> hier_buf;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_free;  // event pool
   uint8_t* h_stage = nullptr;  // pinned staging for flag maps (regrid)
@@ -2139,6 +2140,8 @@ int claw_create(const claw_config* cfg, claw_ctx** out) {
     CUDA_TRY(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_ready, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_halo, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_int, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_edge, cudaEventDisableTiming));
   }
   if (cfg->world > 1 && cfg->exchange == 0) {
     if (!g_nccl.load(ctx->err)) {
@@ -2197,6 +2200,8 @@ int claw_destroy(claw_ctx* ctx) {
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
   if (ctx->ev_ready) cudaEventDestroy(ctx->ev_ready);
   if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
+  if (ctx->ev_int) cudaEventDestroy(ctx->ev_int);
+  if (ctx->ev_edge) cudaEventDestroy(ctx->ev_edge);
   ctx->nf_flag.reset();
   ctx->hier_many.reset();
   if (ctx->h_nf) cudaFreeHost(ctx->h_nf);
@@ -2539,20 +2544,37 @@ int claw_advance_level_async(claw_ctx* ctx, int32_t level, double dt) {
       n_int = L.ntile_interior;
       n_all = 1;
     }
-    if (n_int > 0 && Pi.ntiles > 0) {
+    if (n_int > 0 && Pi.ntiles > 0 && n_all && Pe.ntiles > 0 && !ctx->dry) {
+      // the edge tiles on the comm stream, behind the halo there, so they
+      // fill the SMs the interior launch's last wave leaves idle; they read
+      // q^n and the frame (ready: ev_int, recorded after this level's ghost
+      // fill), write cells the interior tiles do not, and max into the same
+      // CFL slot; the library stream waits for them before anything else
       Pe.level_cfl_reset = nullptr;  // reset once (by the interior launch)
-      if (!ctx->dry) CUDA_TRY(static_cast<cudaError_t>(claw::launch_step(Pi, ctx->stream)));
-      ctx->stats.step_launches++;
-    } else {
-      Pe = P;                        // no split: one launch after the halo
-    }
-    if (L.halo_pending) {
-      CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo, 0));
+      CUDA_TRY(cudaEventRecord(ctx->ev_int, ctx->stream));
+      CUDA_TRY(static_cast<cudaError_t>(claw::launch_step(Pi, ctx->stream)));
+      CUDA_TRY(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_int, 0));
+      CUDA_TRY(static_cast<cudaError_t>(claw::launch_step(Pe, ctx->comm_stream)));
+      CUDA_TRY(cudaEventRecord(ctx->ev_edge, ctx->comm_stream));
+      CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_edge, 0));
       L.halo_pending = false;
-    }
-    if (n_all && Pe.ntiles > 0) {
-      if (!ctx->dry) CUDA_TRY(static_cast<cudaError_t>(claw::launch_step(Pe, ctx->stream)));
-      ctx->stats.step_launches++;
+      ctx->stats.step_launches += 2;
+    } else {
+      if (n_int > 0 && Pi.ntiles > 0) {
+        Pe.level_cfl_reset = nullptr;  // reset once (by the interior launch)
+        if (!ctx->dry) CUDA_TRY(static_cast<cudaError_t>(claw::launch_step(Pi, ctx->stream)));
+        ctx->stats.step_launches++;
+      } else {
+        Pe = P;                        // no split: one launch after the halo
+      }
+      if (L.halo_pending) {
+        CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo, 0));
+        L.halo_pending = false;
+      }
+      if (n_all && Pe.ntiles > 0) {
+        if (!ctx->dry) CUDA_TRY(static_cast<cudaError_t>(claw::launch_step(Pe, ctx->stream)));
+        ctx->stats.step_launches++;
+      }
     }
   } else {
     P.side = L.use_side ? L.side.p : nullptr;
