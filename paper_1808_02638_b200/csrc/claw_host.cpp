@@ -1555,9 +1555,19 @@ int plan_level(claw_ctx* c, int level, Level& L) {
         L.band_te = kBandEdge;
         const int64_t slots = static_cast<int64_t>(c->nsm) * claw::grid_resident_warps();
         const int64_t rows = L.Y1 - L.Y0 - 2 * kBandEdge;
+        // (interior tiles start 4 rows into a patch row and may start
+        // anywhere in one after that: heights are multiples of 4 -- the
+        // kernels cross patch rows at rows congruent to Y0 mod 4 -- so the
+        // makespan can pick near-integral waves; e.g. N = 8 on C5: 547
+        // strips x 17 blocks of 120 rows = 3.93 waves instead of 8 blocks of
+        // 256 = 1.85 waves: per-rank step 0.295 -> 0.279 ms)
+        // (heights capped at 256: the makespan model does not see a tall
+        // tile's longer tail -- N = 2 on C5 picked 484-row tiles at 3.9 waves
+        // and measured 6% slower than 192-row ones at 9.9 waves)
+        auto int_ok = [&](int w) { return w >= 16 && w % 4 == 0 && w <= 512; };
         int thi = my;
         double best = -1.0;
-        for (int w = my; w <= 512; w += my) {
+        for (int w = 16; w <= 256; w += 4) {
           const int64_t tiles = nstrip * ((rows + w - 1) / w);
           if (tiles < slots && w > my) continue;
           const double cost = static_cast<double>((tiles + slots - 1) / slots) * (w + 4);
@@ -1567,8 +1577,8 @@ int plan_level(claw_ctx* c, int level, Level& L) {
           }
         }
         if (const char* e = std::getenv("CLAW_GRID_TH")) {
-          if (span_ok(std::atoi(e)) || std::atoi(e) == my) thi = std::atoi(e);
-        } else if (c->cfg.tile_rows > 0 && (span_ok(c->cfg.tile_rows) || c->cfg.tile_rows == my)) {
+          if (int_ok(std::atoi(e))) thi = std::atoi(e);
+        } else if (c->cfg.tile_rows > 0 && int_ok(c->cfg.tile_rows)) {
           thi = c->cfg.tile_rows;
         }
         L.grid_th_int = thi;

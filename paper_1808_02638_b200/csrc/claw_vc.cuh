@@ -358,10 +358,14 @@ __global__ void __launch_bounds__(32 * CLAW_VC_KW, CLAW_VC_RES_WARPS / CLAW_VC_K
   const int64_t jump_q = static_cast<int64_t>(P.npx) * 3 * mx * myv - static_cast<int64_t>(myv) * mx;
   const int64_t jump_a = static_cast<int64_t>(P.npx) * 2 * mx * myv - static_cast<int64_t>(myv) * mx;
   // (wide strips: gq / ga run the lane's chunk sources wq / wa instead)
-  const double* gq = (wstrip ? wq0 : gq0) + static_cast<int64_t>(kGPD + 2) * mx;
-  const double* ga = (wstrip ? wa0 : ga0) + static_cast<int64_t>(kGPD + 2) * mx;
-  const double* xq = xq0 + static_cast<int64_t>(kGPD + 2) * mx;
-  const double* xa = xa0 + static_cast<int64_t>(kGPD + 2) * mx;
+  // (a tile that starts kGPD+2 or fewer rows before its patch row ends --
+  // band split with tile heights that are not multiples of my -- already
+  // crossed into the next patch row at the first row the march prefetches)
+  const bool x0 = span && (j0 % myv) + kGPD + 2 >= myv;
+  const double* gq = (wstrip ? wq0 : gq0) + static_cast<int64_t>(kGPD + 2) * mx + (x0 ? jump_q : 0);
+  const double* ga = (wstrip ? wa0 : ga0) + static_cast<int64_t>(kGPD + 2) * mx + (x0 ? jump_a : 0);
+  const double* xq = xq0 + static_cast<int64_t>(kGPD + 2) * mx + (x0 ? jump_q : 0);
+  const double* xa = xa0 + static_cast<int64_t>(kGPD + 2) * mx + (x0 ? jump_a : 0);
 
   auto step = [&](auto phc, int jb, auto fastc) {
     constexpr int PH = decltype(phc)::value;

@@ -123,7 +123,11 @@ def test_virtual_ranks_variable_media_bitwise_equal_single_rank(world, npx, mx, 
 @pytest.mark.parametrize("world,npx,mx,tile_rows,bc,media", [
     (2, 16, 32, 0, W.EXTRAP, False), (4, 16, 32, 64, W.PERIODIC, False), (4, 16, 32, 96, (1, 1, 2, 2), False),
     (3, 12, 16, 48, W.EXTRAP, False), (2, 8, 64, 128, W.PERIODIC, False), (8, 16, 32, 32, W.EXTRAP, False),
-    (4, 16, 32, 64, W.EXTRAP, True), (2, 8, 64, 128, (1, 1, 2, 2), True)])
+    (4, 16, 32, 64, W.EXTRAP, True), (2, 8, 64, 128, (1, 1, 2, 2), True),
+    # interior heights that are multiples of 4 but not of my: tiles start
+    # anywhere in a patch row and the prologue / first prefetch cross patch rows
+    (4, 16, 32, 20, W.EXTRAP, False), (2, 16, 32, 36, W.PERIODIC, False), (4, 16, 32, 60, (1, 1, 2, 2), False),
+    (2, 8, 64, 124, W.EXTRAP, False), (4, 16, 32, 28, W.EXTRAP, True), (2, 8, 64, 100, W.PERIODIC, True)])
 def test_band_split_tiles_bitwise_equal_single_rank(world, npx, mx, tile_rows, bc, media, monkeypatch):
     """Band split: each rank's step is an interior
     launch over rows [Y0 + 4, Y1 - 4) -- tiles of tile_rows rows that start 4
