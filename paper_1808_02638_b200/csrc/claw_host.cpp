@@ -996,6 +996,48 @@ void parallel_for(int nthr, int n, F&& f) {
   HostPool::get().run(nthr, n, fn);
 }
 
+// grid tiles spanning whole patch rows: w rows, a multiple of the patch
+// height my (the row pointers step across patch-row boundaries)
+bool span_rows_ok(int w, int my) { return w > my && w % my == 0 && my % 4 == 0 && my >= 8 && w <= 512; }
+
+// Tile height of a large single-rank grid level by the makespan of the
+// launch: ceil(tiles / slots) waves of (th + 4) row steps each (the 4 halo
+// rows are the per-tile prologue); slots = resident warps of the kernel
+// that runs the level.  Ties go to the taller tile; a sub-wave candidate is
+// skipped (latency-bound levels keep th0).
+int makespan_th(int64_t nstrip, int64_t rows, int my, int64_t slots, int th0) {
+  int th = th0;
+  double best = -1.0;
+  for (int w = my; w <= 512; w += my) {
+    if (!(w == my || span_rows_ok(w, my))) continue;
+    const int64_t tiles = nstrip * ((rows + w - 1) / w);
+    if (tiles < slots) continue;
+    const double cost = static_cast<double>((tiles + slots - 1) / slots) * (w + 4);
+    if (best < 0 || cost <= best) {
+      best = cost;
+      th = w;
+    }
+  }
+  return th;
+}
+
+// Interior tile height of a band-split level: any
+// multiple of 4 from 16 to 256 rows, by the same makespan rule.
+int band_int_th(int64_t nstrip, int64_t rows, int my, int64_t slots) {
+  int thi = my;
+  double best = -1.0;
+  for (int w = 16; w <= 256; w += 4) {
+    const int64_t tiles = nstrip * ((rows + w - 1) / w);
+    if (tiles < slots && w > my) continue;
+    const double cost = static_cast<double>((tiles + slots - 1) / slots) * (w + 4);
+    if (best < 0 || cost <= best) {
+      best = cost;
+      thi = w;
+    }
+  }
+  return thi;
+}
+
 int plan_level(claw_ctx* c, int level, Level& L) {
   static const bool trace = std::getenv("CLAW_TRACE_PLAN") != nullptr;
   auto tnow = [] { return std::chrono::steady_clock::now(); };
@@ -1510,7 +1552,7 @@ int plan_level(claw_ctx* c, int level, Level& L) {
       // patches; CLAW_GRID_TH overrides (tuning)
       int th = std::min(L.th, my);
       const int64_t nstrip0 = claw::grid_nstrip(L.nx);
-      auto span_ok = [&](int w) { return w > my && w % my == 0 && my % 4 == 0 && my >= 8 && w <= 512; };
+      auto span_ok = [&](int w) { return span_rows_ok(w, my); };
       if (const char* e = std::getenv("CLAW_GRID_TH")) {
         if (span_ok(std::atoi(e))) th = std::atoi(e);
       } else if (c->cfg.tile_rows > 0) {
@@ -1522,19 +1564,7 @@ int plan_level(claw_ctx* c, int level, Level& L) {
         // prologue); the tail of a partly filled last wave is what one-
         // patch-row or fixed 256-row tiles lose on C4 (3.7 waves of 256-row
         // tiles: the last wave 70% full).  Ties go to the taller tile.
-        const int64_t slots = static_cast<int64_t>(c->nsm) * claw::grid_resident_warps();
-        const int64_t rows = L.Y1 - L.Y0;
-        double best = -1.0;
-        for (int w = my; w <= 512; w += my) {
-          if (!(w == my || span_ok(w))) continue;
-          const int64_t tiles = nstrip0 * ((rows + w - 1) / w);
-          if (tiles < slots) continue;   // sub-wave: keep th <= my (latency-bound levels)
-          const double cost = static_cast<double>((tiles + slots - 1) / slots) * (w + 4);
-          if (best < 0 || cost <= best) {
-            best = cost;
-            th = w;
-          }
-        }
+        th = makespan_th(nstrip0, L.Y1 - L.Y0, my, static_cast<int64_t>(c->nsm) * claw::grid_resident_warps(), th);
       }
       L.grid_th = th;
       const int64_t nstrip = claw::grid_nstrip(L.nx);
@@ -1565,17 +1595,7 @@ int plan_level(claw_ctx* c, int level, Level& L) {
         // tile's longer tail -- N = 2 on C5 picked 484-row tiles at 3.9 waves
         // and measured 6% slower than 192-row ones at 9.9 waves)
         auto int_ok = [&](int w) { return w >= 16 && w % 4 == 0 && w <= 512; };
-        int thi = my;
-        double best = -1.0;
-        for (int w = 16; w <= 256; w += 4) {
-          const int64_t tiles = nstrip * ((rows + w - 1) / w);
-          if (tiles < slots && w > my) continue;
-          const double cost = static_cast<double>((tiles + slots - 1) / slots) * (w + 4);
-          if (best < 0 || cost <= best) {
-            best = cost;
-            thi = w;
-          }
-        }
+        int thi = band_int_th(nstrip, rows, my, slots);
         if (const char* e = std::getenv("CLAW_GRID_TH")) {
           if (int_ok(std::atoi(e))) thi = std::atoi(e);
         } else if (c->cfg.tile_rows > 0 && int_ok(c->cfg.tile_rows)) {
