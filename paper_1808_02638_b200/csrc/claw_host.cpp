@@ -457,6 +457,7 @@ struct Level {
   int64_t ngrid_tiles = 0;
   int64_t ngrid_blocks = 0;   // row blocks of the band (grid mode)
   int grid_th = 0;            // rows per grid tile (> my: tiles span patch rows)
+  int grid_th_base = 0;       // single-rank makespan choice: the th it started from (0: not auto)
   int band_te = 0;            // band split (world > 1): rows of each edge tile (0: row blocks)
   int grid_th_int = 0;        // band split: rows per interior tile
   int64_t ngrid_blocks_int = 0;
@@ -1005,10 +1006,19 @@ bool span_rows_ok(int w, int my) { return w > my && w % my == 0 && my % 4 == 0 &
 // rows are the per-tile prologue); slots = resident warps of the kernel
 // that runs the level.  Ties go to the taller tile; a sub-wave candidate is
 // skipped (latency-bound levels keep th0).
-int makespan_th(int64_t nstrip, int64_t rows, int my, int64_t slots, int th0) {
+// (grid-kernel heights capped at kSpanAutoMax rows: re-swept on the final
+// kernel, C5 measured 129.5 G at 192-row tiles against 126.4 G at the 384
+// the uncapped rule picked, C4 unchanged at 192; the vc kernel and the van
+// Leer limiter keep the uncapped rule -- 384-row tiles on c5vc, 2% faster
+// than 192 -- profiles/r02_grid_tile_rows_final.txt)
+#ifndef CLAW_SPAN_AUTO_MAX
+#define CLAW_SPAN_AUTO_MAX 192
+#endif
+constexpr int kSpanAutoMax = CLAW_SPAN_AUTO_MAX;
+int makespan_th(int64_t nstrip, int64_t rows, int my, int64_t slots, int th0, int cap = kSpanAutoMax) {
   int th = th0;
   double best = -1.0;
-  for (int w = my; w <= 512; w += my) {
+  for (int w = my; w <= cap; w += my) {
     if (!(w == my || span_rows_ok(w, my))) continue;
     const int64_t tiles = nstrip * ((rows + w - 1) / w);
     if (tiles < slots) continue;
@@ -1551,6 +1561,7 @@ int plan_level(claw_ctx* c, int level, Level& L) {
       // patch-row boundaries), which halves the per-tile prologue on 32-row
       // patches; CLAW_GRID_TH overrides (tuning)
       int th = std::min(L.th, my);
+      L.grid_th_base = 0;
       const int64_t nstrip0 = claw::grid_nstrip(L.nx);
       auto span_ok = [&](int w) { return span_rows_ok(w, my); };
       if (const char* e = std::getenv("CLAW_GRID_TH")) {
@@ -1564,7 +1575,11 @@ int plan_level(claw_ctx* c, int level, Level& L) {
         // prologue); the tail of a partly filled last wave is what one-
         // patch-row or fixed 256-row tiles lose on C4 (3.7 waves of 256-row
         // tiles: the last wave 70% full).  Ties go to the taller tile.
-        th = makespan_th(nstrip0, L.Y1 - L.Y0, my, static_cast<int64_t>(c->nsm) * claw::grid_resident_warps(), th);
+        L.grid_th_base = L.band ? 0 : th;
+        // (the cap for the MC limiter only: the paper workload's van Leer
+        // levels measured 3% slower per coarse step with it)
+        th = makespan_th(nstrip0, L.Y1 - L.Y0, my, static_cast<int64_t>(c->nsm) * claw::grid_resident_warps(), th,
+                         c->cfg.limiter == 4 ? kSpanAutoMax : 512);
       }
       L.grid_th = th;
       const int64_t nstrip = claw::grid_nstrip(L.nx);
@@ -2375,6 +2390,19 @@ int claw_set_aux(claw_ctx* ctx, int32_t level, const double* aux) {
     }
   }
   L.vc = true;
+  if (L.grid && L.grid_th_base > 0 && !L.sparse) {
+    // the vc kernel measured faster with the uncapped makespan rule's taller
+    // tiles (c5vc 384 rows: 76.9 G against 75.4 G at 192)
+    const int my = L.desc[0].my;
+    const int th = makespan_th(claw::grid_nstrip(L.nx), L.Y1 - L.Y0, my,
+                               static_cast<int64_t>(ctx->nsm) * claw::grid_resident_warps(), L.grid_th_base, 512);
+    if (th != L.grid_th) {
+      if (!ctx->host_only) drop_graphs(ctx);
+      L.grid_th = th;
+      L.ngrid_blocks = th > my ? ((L.Y1 - L.Y0) + th - 1) / th : ((L.Y1 - L.Y0) / my) * ((my + th - 1) / th);
+      L.ngrid_tiles = claw::grid_nstrip(L.nx) * L.ngrid_blocks;
+    }
+  }
   return CLAW_OK;
 }
 
